@@ -1,0 +1,102 @@
+"""Oracle pins: MAC, kind selection and the LIFO dual traversal.
+
+Pinned by closed-form near-pair counts on full uniform octrees (PAPER.md:168 'theta=0.5 is
+equivalent to a 3x3x3 neighbor list'; tests/golden/near_pair_counts.json), exact pair coverage
+(every ordered particle pair covered by exactly one task), selector forcing and the
+S:338-345 cost examples.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from fmm_inputs import make_particles
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def full_grid(L):
+    """One particle at the centre of each of the 8^L finest cells of [0,1)^3."""
+    g = (np.arange(2 ** L) + 0.5) / 2 ** L
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    xyz = np.stack([X.ravel(), Y.ravel(), Z.ravel()], 1).astype(np.float32)
+    return xyz, np.full(len(xyz), 1.0 / len(xyz), np.float32)
+
+
+@pytest.mark.parametrize("case", json.load(open(os.path.join(GOLD, "near_pair_counts.json")))["cases"],
+                         ids=lambda c: f"L{c['L']}-t{c['theta']}")
+def test_near_pair_closed_form(O, case):
+    xyz, q = full_grid(case["L"])
+    res = O.fmm(xyz, q, 1, case["theta"], 1, O.FMM)
+    lev = res.tree["level"]
+    assert lev.max() == case["L"] and np.sum(lev == case["L"]) == 8 ** case["L"]
+    kinds = res.tasks["kind"]
+    assert np.sum(kinds == O.K_P2P) == case["near"]
+    assert np.sum(kinds == O.K_M2P) == 0
+
+
+def coverage(O, res, n):
+    cov = np.zeros((n, n), np.int32)
+    for kind, tb, tc, sb, sc in O.task_ranges(res):
+        cov[tb:tb + tc, sb:sb + sc] += 1
+    return cov
+
+
+@pytest.mark.parametrize("mode", ["FMM", "TREECODE", "HYBRID"])
+@pytest.mark.parametrize("dist", ["uniform", "shell", "plummer"])
+@pytest.mark.parametrize("ncrit", [1, 20, 50, 200])
+def test_exact_pair_coverage(O, mode, dist, ncrit):
+    # every ordered (target, source) particle pair is covered by exactly one task.
+    for seed in (1, 2, 3):
+        xyz, q = make_particles(400, dist, seed)
+        cost = np.random.default_rng(seed).uniform(1e-9, 1e-6, 3)
+        res = O.fmm(xyz, q, 2, 0.5, ncrit, getattr(O, mode), cost=cost)
+        cov = coverage(O, res, len(q))
+        assert np.all(cov == 1), (mode, dist, ncrit, seed)
+
+
+def test_selector_forcing(O):
+    xyz, q = make_particles(1500, "plummer", 4)
+    fmm = O.fmm(xyz, q, 6, 0.5, 16, O.FMM)
+    hyb0 = O.fmm(xyz, q, 6, 0.5, 16, O.HYBRID, cost=(1e-9, 1e-7, 0.0))  # t_ml = 0 -> always M2L
+    a, b = O.canonical_tasks(fmm.tasks), O.canonical_tasks(hyb0.tasks)
+    assert np.array_equal(a, b)
+    tre = O.fmm(xyz, q, 6, 0.5, 16, O.TREECODE)
+    assert np.all(tre.tasks["kind"] != O.K_M2L)
+    # t_pp = 0 -> every accepted pair is P2P -> the result is the direct sum
+    hp = O.fmm(xyz, q, 6, 0.5, 16, O.HYBRID, cost=(0.0, 1e-7, 1e-5))
+    assert np.all(hp.tasks["kind"] == O.K_P2P)
+    d = O.direct(xyz, q)
+    assert O.rel_l2(hp.phi, d[0]) < 1e-12 and O.rel_l2(hp.grad, d[1]) < 1e-12
+
+
+def test_cost_model_examples(O):
+    # S:338-345 with exactly representable per-unit times (powers of two) so the tie is exact.
+    cost = (2.0 ** -30, 2.0 ** -24, 2.0 ** -16)  # n_t = n_s = 2^7: P2P 2^-16, M2P 2^-17, M2L 2^-16
+    assert O.select_kind(O.HYBRID, cost, 128, 128) == O.K_M2P
+    cost = (2.0 ** -30, 2.0 ** -23, 2.0 ** -16)  # n=128: P2P = M2P = M2L = 2^-16 -> tie -> M2L
+    assert O.select_kind(O.HYBRID, cost, 128, 128) == O.K_M2L
+    cost = (1e-9, 1e-7, 1e-5)
+    assert O.select_kind(O.HYBRID, cost, 10, 10) == O.K_P2P
+    assert O.select_kind(O.HYBRID, cost, 1000, 1000) == O.K_M2L
+    # scale invariance on exactly scaled costs
+    for nt, ns in [(3, 5), (50, 70), (1, 1000), (900, 2)]:
+        k = O.select_kind(O.HYBRID, cost, nt, ns)
+        assert O.select_kind(O.HYBRID, [c * 4.0 for c in cost], nt, ns) == k
+    assert O.select_kind(O.FMM, cost, 1, 1) == O.K_M2L
+    assert O.select_kind(O.TREECODE, cost, 1, 1) == O.K_M2P
+
+
+def test_single_leaf_tree_single_p2p(O):
+    xyz, q = make_particles(10, "uniform", 3)
+    res = O.fmm(xyz, q, 4, 0.5, 16, O.FMM)  # two single-leaf trees -> one P2P
+    assert len(res.tasks["kind"]) == 1 and res.tasks["kind"][0] == O.K_P2P
+
+
+def test_theta_monotonicity(O):
+    xyz, q = make_particles(3000, "uniform", 5)
+    d = O.direct(xyz, q)
+    errs = [O.rel_l2(O.fmm(xyz, q, 4, th, 16, O.FMM, want_structure=False).phi, d[0])
+            for th in (0.7, 0.5, 0.35, 0.25)]
+    assert all(b < a for a, b in zip(errs, errs[1:])), errs
