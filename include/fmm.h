@@ -1,0 +1,134 @@
+/* fmm.h — C ABI of libfmm.so: the B200-native (sm_100a) hybrid treecode/FMM of
+ * Yokota & Barba, "Hierarchical N-body simulations with auto-tuning for heterogeneous systems"
+ * (arxiv 1108.5815). Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (both under the
+ * upstream reference); SURVEY §8 = /root/repo/SURVEY.md §8 (hot-path scope), DESIGN.md = this repo.
+ *
+ * What is computed ("Laplace kernel potential and force"):
+ *   phi_i      = sum_{j != i, r_ij > 0} q_j / r_ij
+ *   grad_phi_i = -sum_{j, r_ij > 0} q_j (x_i - x_j) / r_ij^3        (= -force of S:30)
+ * approximated by the hybrid treecode/FMM of P:145-169: Morton-keyed adaptive octree with at most
+ * ncrit particles per leaf, P2M/M2M upward sweep, dual tree traversal with the MAC
+ * theta = (r_t + r_s)/R, per-pair choice among M2L / M2P / P2P from kernel timings
+ * measured on the device, L2L/L2P downward sweep. Spherical-harmonic expansions of
+ * order p, single precision on the device.
+ *
+ * Conventions (all entry points):
+ *   - Return 0 (FMM_OK) or a negative fmm_status; nothing throws across the ABI. The message of the
+ *     last failure on a handle is available from fmm_last_error().
+ *   - Pointers named d_* are DEVICE pointers (cudaMalloc / torch CUDA tensors) on the handle's
+ *     device; pointers named h_* are HOST pointers. The caller owns every buffer it passes; the
+ *     handle owns all scratch (grow-only, reused across calls).
+ *   - One handle = one CUDA device (the device current at fmm_create) and one stream; a handle is
+ *     not thread-safe. Evaluations are stream-ordered and synchronous on return.
+ *   - Results are written in the caller's particle order and overwrite the output buffers.
+ */
+#ifndef FMM_B200_H
+#define FMM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fmm_ctx *fmm_t;
+
+/* Evaluation modes ("the treecode always performs cell-particle interactions, and the FMM
+ * always performs cell-cell interactions, while the hybrid can choose between cell-cell,
+ * cell-particle, and particle-particle interactions"). FMM_DIRECT = one all-pairs P2P. */
+enum fmm_mode { FMM_HYBRID = 0, FMM_FMM = 1, FMM_TREECODE = 2, FMM_DIRECT = 3 };
+
+/* Interaction kinds in exported lists. */
+enum fmm_kind { FMM_KIND_M2L = 0, FMM_KIND_M2P = 1, FMM_KIND_P2P = 2 };
+
+enum fmm_status {
+  FMM_OK = 0,
+  FMM_E_INVALID = -1,    /* p not in [1, FMM_P_MAX], theta not in (0,1), ncrit < 1, n < 0, NULL */
+  FMM_E_NOT_DEVICE = -2, /* a d_* pointer is not device memory of the handle's device */
+  FMM_E_NONFINITE = -3,  /* a coordinate or charge is not finite; outputs untouched */
+  FMM_E_CUDA = -4,       /* CUDA runtime / kernel failure */
+  FMM_E_OOM = -5,        /* device allocation failed */
+  FMM_E_NCCL = -6,       /* reserved for the multi-GPU path */
+  FMM_E_STATE = -7       /* export called before any evaluation */
+};
+
+#define FMM_P_MAX 16 /* P:205 goes to p = 15; FP32 scaled I_n^m up to degree 2p stays finite */
+
+/* Kernel pre-calculation result ("All kernels are evaluated using artificial coordinates,
+ * mass/charges, multipole coefficients, and their execution time is measured"). Linear per-unit
+ * cost model: P2P = t_pp * n_t * n_s, M2P = t_mp * n_t, M2L = t_ml; argmin with ties
+ * M2L > M2P > P2P. */
+typedef struct {
+  double t_pp;  /* seconds per particle pair (P2P) */
+  double t_mp;  /* seconds per target particle per source cell (M2P) */
+  double t_ml;  /* seconds per cell-cell translation (M2L) */
+  int p;        /* expansion order the timings belong to */
+  int measured; /* 1 = measured on this device by fmm_create/fmm_tune, 0 = set by the caller */
+} fmm_cost_t;
+
+/* Counters and per-phase device times of the last evaluation (S:141-144 KernelCounters; SURVEY
+ * §5 tracing). Times are CUDA-event milliseconds on the handle's stream, filled only when timing
+ * is enabled with fmm_set_timing(h, 1). */
+typedef struct {
+  int64_t n, ncells, nleaves;
+  int32_t depth, p;
+  int64_t n_m2l, n_m2p, n_p2p;      /* cell pairs per kind */
+  int64_t p2p_pairs, m2p_evals;     /* particle pairs in P2P; target-particle x source-cell in M2P */
+  int64_t traversal_pairs;          /* MAC tests performed */
+  double ms_total, ms_tree, ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_m2p, ms_downward;
+} fmm_stats_t;
+
+/* Create a handle on the current CUDA device. p = expansion order (coefficients n = 0..p,
+ * SURVEY §8(c) reading 2), theta = MAC, ncrit = max particles per leaf.
+ * Runs the kernel pre-calculation unless FMM_NO_TUNE is set in the environment.
+ * Errors: FMM_E_INVALID, FMM_E_CUDA, FMM_E_OOM. */
+int fmm_create(fmm_t *out, int p, double theta, int ncrit);
+
+/* Release the handle and all device scratch. NULL-safe. */
+int fmm_destroy(fmm_t h);
+
+/* Evaluate potential and gradient for n particles.
+ *   d_xyz  [3n] float, AoS (x0,y0,z0,x1,...)     d_q [n] float
+ *   d_phi  [n]  float (out)                       d_grad [3n] float, AoS (out)
+ * n = 0 is a successful no-op. Errors: FMM_E_INVALID, FMM_E_NOT_DEVICE, FMM_E_NONFINITE,
+ * FMM_E_CUDA, FMM_E_OOM. */
+int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float *d_phi,
+                 float *d_grad);
+
+/* Same with HOST buffers (pinned or pageable): copies in, evaluates, copies out (end-to-end path). */
+int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, float *h_phi,
+                      float *h_grad);
+
+/* Use the caller's stream (a cudaStream_t passed as void*); NULL restores the handle's own. */
+int fmm_set_stream(fmm_t h, void *stream);
+int fmm_set_mode(fmm_t h, int mode);
+/* 1 = record per-phase CUDA events (small overhead), 0 = off (default). */
+int fmm_set_timing(fmm_t h, int enable);
+
+/* Re-run the kernel pre-calculation on this device. */
+int fmm_tune(fmm_t h);
+int fmm_get_cost_model(fmm_t h, fmm_cost_t *out);
+/* Pin the cost model (reproducible lists; the oracle imports the same numbers). in->p must equal
+ * the handle's p. */
+int fmm_set_cost_model(fmm_t h, const fmm_cost_t *in);
+int fmm_get_stats(fmm_t h, fmm_stats_t *out);
+
+/* Canonical exports of the last evaluation (host buffers, caller-allocated with `cap` entries;
+ * the required count is always written to *count_out, and FMM_E_INVALID is returned when cap is
+ * too small). Tree: cells in (level, prefix) order. Lists: one row per interaction pair, grouped
+ * by target cell. Perm: h_perm[i] = caller index of the i-th particle in Morton order; h_keys[i]
+ * its 63-bit key. Errors: FMM_E_STATE before the first tree evaluation. */
+int fmm_export_tree(fmm_t h, int64_t cap, int32_t *h_level, uint64_t *h_prefix, int64_t *h_begin,
+                    int64_t *h_count, int64_t *count_out);
+int fmm_export_lists(fmm_t h, int64_t cap, int32_t *h_kind, int32_t *h_tlevel, uint64_t *h_tprefix,
+                     int32_t *h_slevel, uint64_t *h_sprefix, int64_t *count_out);
+int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, double *h_origin3,
+                    double *h_L);
+
+const char *fmm_strerror(int code);
+const char *fmm_last_error(fmm_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

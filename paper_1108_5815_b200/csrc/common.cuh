@@ -1,0 +1,58 @@
+// common.cuh — device-side data layout shared by the sm_100a kernels of libfmm.so.
+//
+// HBM layout:
+//   pos4   float4[N]        Morton-sorted (x, y, z, q)
+//   perm   uint32[N]        sorted index -> caller index
+//   keys   uint64[N]        sorted 63-bit Morton keys (21 levels, x bit most significant)
+//   cells  SoA, BFS order (level-major, Morton order inside a level):
+//            cbeg/ccnt int32, cparent int32, cchild0/cnchild int32,
+//            cgrid int4 (doubled-grid centre cx~,cy~,cz~ = (2g+1)*2^(21-l), level) — exact MAC,
+//            cgeo float4 (centre x, y, z in FP32, half-width r)
+//   Mhat / Lhat float2[ncells][NC(p)]  power-of-two scaled expansions, orders m >= 0 only
+//   lists  per target cell (off, cnt) into uint32 source-cell arrays, one array per kind
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define FMM_LEVELS 21
+#define FMM_PMAX 16
+#define WARP 32
+
+// Number of stored coefficients (m >= 0) for order p, and the index of (n, m >= 0).
+__host__ __device__ __forceinline__ constexpr int nc_of(int p) { return (p + 1) * (p + 2) / 2; }
+__host__ __device__ __forceinline__ constexpr int cidx(int n, int m) { return n * (n + 1) / 2 + m; }
+
+struct RootInfo {
+  double origin[3];
+  double L;       // power-of-two side of the root cube
+  double scale;   // 2^21 / L
+  unsigned int nonfinite;
+  int pad;
+};
+
+// Cell arrays (device pointers) passed by value to kernels.
+struct CellsView {
+  int *beg, *cnt, *parent, *child0, *nchild;
+  int4 *grid;    // (cx~, cy~, cz~, level)
+  float4 *geo;   // (cx, cy, cz, r)
+};
+
+struct ListsView {
+  int *off[3];       // per target cell, per kind (M2L, M2P, P2P)
+  int *cnt[3];
+  unsigned *src[3];  // source cell ids
+};
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+
+// Signed-order access into m >= 0 storage of a real field: A_n^{-m} = (-1)^m conj(A_n^m).
+__device__ __forceinline__ float2 sget(const float2 *A, int n, int m) {
+  if (m >= 0) return A[cidx(n, m)];
+  float2 v = A[cidx(n, -m)];
+  return (m & 1) ? make_float2(-v.x, v.y) : make_float2(v.x, -v.y);
+}
+
+#define CUDA_OK(x) ((x) == cudaSuccess)

@@ -1,0 +1,571 @@
+// expansions.cu — P2M, M2M, M2L, L2L, M2P and L2P on CUDA cores (sm_100a), FP32.
+//
+// Expansions (DESIGN.md §3 R1): R_n^m = r^n P_n^m e^{im phi}/(n+m)!,
+// I_n^m = (n-m)! P_n^m e^{im phi}/r^{n+1}, evaluated with trig-free recurrences. They are stored
+// power-of-two SCALED by the cell half-width r: Mhat_n^m = M_n^m / r^n,
+// Lhat_n^m = L_n^m r^{n+1}, so FP32 never overflows at p <= 16 (unscaled I up to degree 2p
+// would reach 1e54). Only orders m >= 0 are stored; m < 0 follows from A_n^{-m} = (-1)^m conj(A).
+//
+//   P2M  Mhat_n^m   = sum_i q_i conj(R_n^m((y_i - c)/r))
+//   M2M  Mhat_n^m(P) = sum_{j,k} Mhat_j^k(C) 2^-j conj(R_{n-j}^{m-k}(b/r_P))
+//   M2L  Lhat_j^k(t) = (-1)^{j+k} sum_{n<=p,m} Mhat_n^m(s) rho^n I_{n+j}^{m-k}(u)
+//        u = (c_t - c_s)/r_t, rho = r_s/r_t   [for rho > 1 the same sum is formed at
+//        v = u/rho with M unscaled and the result times rho^-(j+1): identical, in FP32 range]
+//   L2L  Lhat_n^m(C) += 2^-(n+1) sum_{j>=n,k} Lhat_j^k(P) R_{j-n}^{k-m}(e/r_P)
+//   M2P  phi += (1/r_s) sum Mhat I(xi), grad from I_{n+1} (d/dz I = -I_{n+1}, (dx+idy) I =
+//        I_{n+1}^{m+1})
+//   L2P  phi += (1/r) sum Lhat R(xi), grad from R_{n-1}
+#include "common.cuh"
+#include "kernels.cuh"
+
+__constant__ short2 c_nm[nc_of(FMM_PMAX)];  // coefficient index -> (n, m)
+
+static bool g_nm_ready = false;
+static void ensure_nm_table() {
+  if (g_nm_ready) return;
+  short2 h[nc_of(FMM_PMAX)];
+  for (int n = 0; n <= FMM_PMAX; ++n)
+    for (int m = 0; m <= n; ++m) h[cidx(n, m)] = make_short2((short)n, (short)m);
+  cudaMemcpyToSymbol(c_nm, h, sizeof(h));
+  g_nm_ready = true;
+}
+
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+
+// Regular harmonics R_n^m(x), n <= P, m >= 0, into tab[cidx(n,m)]; lanes take columns m.
+__device__ void regular_table(float x, float y, float z, int P, float2 *tab, int lane) {
+  const float r2 = x * x + y * y + z * z;
+  for (int m = lane; m <= P; m += WARP) {
+    float2 Rmm = make_float2(1.f, 0.f);
+    for (int k = 1; k <= m; ++k) Rmm = cscale(cmul(Rmm, make_float2(x, y)), -1.f / (2.f * k));
+    tab[cidx(m, m)] = Rmm;
+    float2 R2 = make_float2(0.f, 0.f), R1 = Rmm;
+    for (int n = m + 1; n <= P; ++n) {
+      float2 Rn;
+      if (n == m + 1) Rn = cscale(Rmm, z);
+      else {
+        const float inv = 1.f / ((float)(n - m) * (float)(n + m));
+        Rn = make_float2(((2 * n - 1) * z * R1.x - r2 * R2.x) * inv, ((2 * n - 1) * z * R1.y - r2 * R2.y) * inv);
+      }
+      tab[cidx(n, m)] = Rn;
+      R2 = R1;
+      R1 = Rn;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// P2M: warp per leaf; lanes = particles; each coefficient reduced with a fixed butterfly.
+__global__ void __launch_bounds__(128) k_p2m(int p, const int *__restrict__ leaves, int nleaves,
+                                             CellsView C, const float4 *__restrict__ pos,
+                                             float2 *__restrict__ M) {
+  extern __shared__ float2 sh_p2m[];
+  const int NC = nc_of(p);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float2 *acc = sh_p2m + wib * NC;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int li = gw; li < nleaves; li += nw) {
+    const int leaf = leaves[li];
+    const float4 g = C.geo[leaf];
+    const float rinv = 1.f / g.w;
+    const int b = C.beg[leaf], cnt = C.cnt[leaf];
+    for (int o = lane; o < NC; o += WARP) acc[o] = make_float2(0.f, 0.f);
+    __syncwarp();
+    for (int c0 = 0; c0 < cnt; c0 += WARP) {
+      const bool valid = c0 + lane < cnt;
+      float4 y = valid ? pos[b + c0 + lane] : make_float4(g.x, g.y, g.z, 0.f);
+      const float x = (y.x - g.x) * rinv, yy = (y.y - g.y) * rinv, z = (y.z - g.z) * rinv;
+      const float q = y.w;
+      const float r2 = x * x + yy * yy + z * z;
+      float2 Rmm = make_float2(1.f, 0.f);
+      for (int m = 0; m <= p; ++m) {
+        if (m > 0) Rmm = cscale(cmul(Rmm, make_float2(x, yy)), -1.f / (2.f * m));
+        float2 R2 = make_float2(0.f, 0.f), R1 = Rmm;
+        for (int n = m; n <= p; ++n) {
+          float2 Rn;
+          if (n == m) Rn = Rmm;
+          else if (n == m + 1) Rn = cscale(Rmm, z);
+          else {
+            const float inv = 1.f / ((float)(n - m) * (float)(n + m));
+            Rn = make_float2(((2 * n - 1) * z * R1.x - r2 * R2.x) * inv,
+                             ((2 * n - 1) * z * R1.y - r2 * R2.y) * inv);
+          }
+          if (n > m) {
+            R2 = R1;
+            R1 = Rn;
+          }
+          float vr = q * Rn.x, vi = -q * Rn.y;  // q conj(R)
+          for (int s = 16; s > 0; s >>= 1) {
+            vr += __shfl_xor_sync(0xffffffffu, vr, s);
+            vi += __shfl_xor_sync(0xffffffffu, vi, s);
+          }
+          if (lane == 0) {
+            float2 a = acc[cidx(n, m)];
+            acc[cidx(n, m)] = make_float2(a.x + vr, a.y + vi);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    for (int o = lane; o < NC; o += WARP) M[(size_t)leaf * NC + o] = acc[o];
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// M2M: warp per parent cell of one level. b/r_P = (+-1/2, +-1/2, +-1/2) exactly.
+__global__ void __launch_bounds__(128) k_m2m(int p, int c0, int nl, CellsView C,
+                                             float2 *__restrict__ M) {
+  extern __shared__ float2 sh_m2m[];
+  const int NC = nc_of(p);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float2 *Mc = sh_m2m + wib * 2 * NC, *Rb = Mc + NC;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = gw; k < nl; k += nw) {
+    const int P = c0 + k;
+    const int nch = C.nchild[P];
+    if (nch == 0) continue;
+    const int4 gp = C.grid[P];
+    const float rP = (float)(1 << (FMM_LEVELS - gp.w));
+    float2 acc[5];
+#pragma unroll
+    for (int s = 0; s < 5; ++s) acc[s] = make_float2(0.f, 0.f);
+    for (int ch = 0; ch < nch; ++ch) {
+      const int Cc = C.child0[P] + ch;
+      const int4 gc = C.grid[Cc];
+      for (int o = lane; o < NC; o += WARP) Mc[o] = M[(size_t)Cc * NC + o];
+      regular_table((gc.x - gp.x) / rP, (gc.y - gp.y) / rP, (gc.z - gp.z) / rP, p, Rb, lane);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        const int o = lane + s * WARP;
+        if (o >= NC) break;
+        const int n = c_nm[o].x, m = c_nm[o].y;
+        float2 a = make_float2(0.f, 0.f);
+        float sc = 1.f;
+        for (int j = 0; j <= n; ++j, sc *= 0.5f) {
+          const int klo = max(-j, m - (n - j)), khi = min(j, m + (n - j));
+          float2 part = make_float2(0.f, 0.f);
+          for (int kk = klo; kk <= khi; ++kk) {
+            const float2 mv = sget(Mc, j, kk), rv = cconj(sget(Rb, n - j, m - kk));
+            part = cadd(part, cmul(mv, rv));
+          }
+          a = cadd(a, cscale(part, sc));
+        }
+        acc[s] = cadd(acc[s], a);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int o = lane + s * WARP;
+      if (o < NC) M[(size_t)P * NC + o] = acc[s];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// L2L: warp per child cell of one level; adds the parent's local expansion.
+__global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
+                                             float2 *__restrict__ L) {
+  extern __shared__ float2 sh_l2l[];
+  const int NC = nc_of(p);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float2 *Lp = sh_l2l + wib * 2 * NC, *Re = Lp + NC;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = gw; k < nl; k += nw) {
+    const int Cc = c0 + k;
+    const int P = C.parent[Cc];
+    const int4 gp = C.grid[P], gc = C.grid[Cc];
+    const float rP = (float)(1 << (FMM_LEVELS - gp.w));
+    for (int o = lane; o < NC; o += WARP) Lp[o] = L[(size_t)P * NC + o];
+    regular_table((gc.x - gp.x) / rP, (gc.y - gp.y) / rP, (gc.z - gp.z) / rP, p, Re, lane);
+    __syncwarp();
+    for (int o = lane; o < NC; o += WARP) {
+      const int n = c_nm[o].x, m = c_nm[o].y;
+      float2 a = make_float2(0.f, 0.f);
+      for (int j = n; j <= p; ++j) {
+        const int klo = max(-j, m - (j - n)), khi = min(j, m + (j - n));
+        for (int kk = klo; kk <= khi; ++kk) a = cadd(a, cmul(sget(Lp, j, kk), sget(Re, j - n, kk - m)));
+      }
+      const float sc = ldexpf(1.f, -(n + 1));
+      const float2 old = L[(size_t)Cc * NC + o];
+      L[(size_t)Cc * NC + o] = make_float2(old.x + sc * a.x, old.y + sc * a.y);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// M2L: one CTA (4 warps) per target cell; each warp takes every 4th source of the target's list.
+// Per source the warp builds, in shared memory, the signed-order table I_a^b(u), a <= 2p, and the
+// signed, rho^n-scaled multipole stored as (a, a, b, b) so that each complex multiply-add is two
+// packed FFMA2. Each lane owns "tiles" of up to 3 consecutive orders k of one degree j; the
+// per-source partial is added to the running sum (tile-blocked accumulation).
+#define M2L_WARPS 4
+__global__ void __launch_bounds__(128) k_m2l(int p, int ncells, CellsView C, ListsView Ls,
+                                             M2LTiles T, const float2 *__restrict__ M,
+                                             float2 *__restrict__ L) {
+  extern __shared__ float4 sh_m2l[];
+  const int NC = nc_of(p);
+  const int P2 = 2 * p;
+  const int nI = (P2 + 1) * (P2 + 1), nM = (p + 1) * (p + 1);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float4 *Mx = sh_m2l + wib * (nM + (nI + 1) / 2);
+  float2 *Ix = reinterpret_cast<float2 *>(Mx + nM);
+  float2 *red = reinterpret_cast<float2 *>(sh_m2l + M2L_WARPS * (nM + (nI + 1) / 2));
+
+  for (int t = blockIdx.x; t < ncells; t += gridDim.x) {
+    const int off = Ls.off[0][t], cnt = Ls.cnt[0][t];
+    float2 acc[2][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) acc[a][b] = make_float2(0.f, 0.f);
+    if (cnt > 0) {
+      const int4 gt = C.grid[t];
+      const float rt_inv = 1.f / (float)(1 << (FMM_LEVELS - gt.w));
+      for (int e = wib; e < cnt; e += M2L_WARPS) {
+        const int s = Ls.src[0][off + e];
+        const int4 gs = C.grid[s];
+        const int dl = gt.w - gs.w;  // rho = 2^dl
+        float ux = (gt.x - gs.x) * rt_inv, uy = (gt.y - gs.y) * rt_inv, uz = (gt.z - gs.z) * rt_inv;
+        const bool vform = dl > 0;
+        if (vform) {
+          const float ir = ldexpf(1.f, -dl);
+          ux *= ir;
+          uy *= ir;
+          uz *= ir;
+        }
+        // signed multipole, (a, a, b, b), scaled by rho^n in the u-form
+        for (int o = lane; o < nM; o += WARP) {
+          const int n = (int)sqrtf((float)o + 0.5f);
+          const int m = o - n * n - n;
+          const float2 v = sget(M + (size_t)s * NC, n, m);
+          const float sc = vform ? 1.f : ldexpf(1.f, n * dl);
+          Mx[o] = make_float4(v.x * sc, v.x * sc, v.y * sc, v.y * sc);
+        }
+        // irregular harmonics I_a^b(u), a <= 2p, all signed b
+        {
+          const float r2 = ux * ux + uy * uy + uz * uz;
+          const float ir2 = 1.f / r2;
+          for (int mm = lane; mm <= P2; mm += WARP) {
+            float2 Imm = make_float2(rsqrtf(r2), 0.f);
+            for (int k = 1; k <= mm; ++k) Imm = cscale(cmul(Imm, make_float2(ux, uy)), -(2.f * k - 1.f) * ir2);
+            float2 I2 = make_float2(0.f, 0.f), I1 = Imm;
+            const float sg = (mm & 1) ? -1.f : 1.f;
+            for (int a = mm; a <= P2; ++a) {
+              float2 Ia;
+              if (a == mm) Ia = Imm;
+              else if (a == mm + 1) Ia = cscale(Imm, (2.f * mm + 1.f) * uz * ir2);
+              else {
+                const float c1 = (2.f * a - 1.f) * uz, c2 = (float)(a + mm - 1) * (float)(a - mm - 1);
+                Ia = make_float2((c1 * I1.x - c2 * I2.x) * ir2, (c1 * I1.y - c2 * I2.y) * ir2);
+              }
+              if (a > mm) {
+                I2 = I1;
+                I1 = Ia;
+              }
+              Ix[a * a + a + mm] = Ia;
+              Ix[a * a + a - mm] = make_float2(sg * Ia.x, -sg * Ia.y);
+            }
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int ti = 0; ti < 2; ++ti) {
+          const int tix = lane + ti * WARP;
+          if (tix >= T.ntiles) break;
+          const int tw = T.tile[tix];
+          const int j = tw & 255, k0 = (tw >> 8) & 255;
+          const int k1 = min(k0 + 1, j), k2 = min(k0 + 2, j);
+          float2 pa0 = make_float2(0.f, 0.f), pb0 = pa0, pa1 = pa0, pb1 = pa0, pa2 = pa0, pb2 = pa0;
+          for (int n = 0; n <= p; ++n) {
+            const float2 *Irow = Ix + (n + j) * (n + j) + (n + j);
+            const float4 *Mrow = Mx + n * n + n;
+            for (int m = -n; m <= n; ++m) {
+              const float4 mv = Mrow[m];
+              const float2 aa = make_float2(mv.x, mv.y), bb = make_float2(mv.z, mv.w);
+              const float2 i0 = Irow[m - k0], i1 = Irow[m - k1], i2 = Irow[m - k2];
+              pa0 = __ffma2_rn(aa, i0, pa0);
+              pb0 = __ffma2_rn(bb, i0, pb0);
+              pa1 = __ffma2_rn(aa, i1, pa1);
+              pb1 = __ffma2_rn(bb, i1, pb1);
+              pa2 = __ffma2_rn(aa, i2, pa2);
+              pb2 = __ffma2_rn(bb, i2, pb2);
+            }
+          }
+          // complex result (sum ac - bd, sum ad + bc); v-form output scale rho^-(j+1)
+          const float osc = vform ? ldexpf(1.f, -dl * (j + 1)) : 1.f;
+          acc[ti][0].x += osc * (pa0.x - pb0.y);
+          acc[ti][0].y += osc * (pa0.y + pb0.x);
+          acc[ti][1].x += osc * (pa1.x - pb1.y);
+          acc[ti][1].y += osc * (pa1.y + pb1.x);
+          acc[ti][2].x += osc * (pa2.x - pb2.y);
+          acc[ti][2].y += osc * (pa2.y + pb2.x);
+        }
+        __syncwarp();
+      }
+    }
+    // reduce the 4 warps' partial sums, apply (-1)^{j+k}, write Lhat_t (zero if no M2L)
+#pragma unroll
+    for (int ti = 0; ti < 2; ++ti) {
+      const int tix = lane + ti * WARP;
+      if (tix >= T.ntiles) break;
+      const int tw = T.tile[tix];
+      const int j = tw & 255, k0 = (tw >> 8) & 255, K = (tw >> 16) & 255;
+      for (int kk = 0; kk < K; ++kk) red[wib * NC + cidx(j, k0 + kk)] = acc[ti][kk];
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < NC; o += blockDim.x) {
+      float2 s = red[o];
+      for (int w = 1; w < M2L_WARPS; ++w) s = cadd(s, red[w * NC + o]);
+      const int n = c_nm[o].x, m = c_nm[o].y;
+      const float sg = ((n + m) & 1) ? -1.f : 1.f;
+      L[(size_t)t * NC + o] = make_float2(sg * s.x, sg * s.y);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// M2P: warp per leaf, lanes = target particles; sources = M2P lists of the leaf and its ancestors.
+__global__ void __launch_bounds__(128) k_m2p(int p, const int *__restrict__ leaves, int nleaves,
+                                             CellsView C, ListsView Ls,
+                                             const float4 *__restrict__ pos,
+                                             const float2 *__restrict__ M,
+                                             float4 *__restrict__ acc) {
+  extern __shared__ float2 sh_m2p[];
+  const int NC = nc_of(p);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float2 *Ms = sh_m2p + wib * NC;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int li = gw; li < nleaves; li += nw) {
+    const int leaf = leaves[li];
+    bool any = false;
+    for (int a = leaf; a >= 0; a = C.parent[a]) any |= Ls.cnt[1][a] > 0;
+    if (!any) continue;
+    const int b = C.beg[leaf], cnt = C.cnt[leaf];
+    for (int c0 = 0; c0 < cnt; c0 += WARP) {
+      const bool valid = c0 + lane < cnt;
+      const int i = b + c0 + lane;
+      const float4 x = valid ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      float phi = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
+      for (int a = leaf; a >= 0; a = C.parent[a]) {
+        const int off = Ls.off[1][a], n_s = Ls.cnt[1][a];
+        for (int e = 0; e < n_s; ++e) {
+          const int s = Ls.src[1][off + e];
+          __syncwarp();
+          for (int o = lane; o < NC; o += WARP) Ms[o] = M[(size_t)s * NC + o];
+          __syncwarp();
+          const float4 g = C.geo[s];
+          const float rinv = 1.f / g.w;
+          const float xx = (x.x - g.x) * rinv, yy = (x.y - g.y) * rinv, zz = (x.z - g.z) * rinv;
+          const float ir2 = 1.f / (xx * xx + yy * yy + zz * zz);
+          float ph = 0.f, dz = 0.f;
+          float2 dxy = make_float2(0.f, 0.f);
+          float2 Imm = make_float2(sqrtf(ir2), 0.f);
+          for (int mm = 0; mm <= p + 1; ++mm) {
+            if (mm > 0) Imm = cscale(cmul(Imm, make_float2(xx, yy)), -(2.f * mm - 1.f) * ir2);
+            float2 I2 = make_float2(0.f, 0.f), I1 = Imm;
+            const float w = mm ? 2.f : 1.f;
+            for (int a2 = mm; a2 <= p + 1; ++a2) {
+              float2 Ia;
+              if (a2 == mm) Ia = Imm;
+              else if (a2 == mm + 1) Ia = cscale(Imm, (2.f * mm + 1.f) * zz * ir2);
+              else {
+                const float c1 = (2.f * a2 - 1.f) * zz, c2 = (float)(a2 + mm - 1) * (float)(a2 - mm - 1);
+                Ia = make_float2((c1 * I1.x - c2 * I2.x) * ir2, (c1 * I1.y - c2 * I2.y) * ir2);
+              }
+              if (a2 > mm) {
+                I2 = I1;
+                I1 = Ia;
+              }
+              // phi: M_a^mm I_a^mm (a <= p)
+              if (a2 <= p && mm <= p) {
+                const float2 mv = Ms[cidx(a2, mm)];
+                ph += w * (mv.x * Ia.x - mv.y * Ia.y);
+              }
+              // d/dz: -M_n^mm I_{n+1}^mm, n = a2 - 1
+              if (a2 >= 1 && a2 - 1 >= mm && a2 - 1 <= p) {
+                const float2 mv = Ms[cidx(a2 - 1, mm)];
+                dz -= w * (mv.x * Ia.x - mv.y * Ia.y);
+              }
+              // (dx + i dy): + M_n^{mm-1} I_{n+1}^{mm}, n = a2 - 1 >= mm - 1
+              if (mm >= 1 && a2 - 1 <= p) {
+                const float2 r = cmul(Ms[cidx(a2 - 1, mm - 1)], Ia);
+                dxy.x += r.x;
+                dxy.y += r.y;
+              }
+              // (dx + i dy): - conj(M_n^{mm+1} I_{n+1}^{mm}), n = a2 - 1 >= mm + 1
+              if (a2 - 1 >= mm + 1 && a2 - 1 <= p) {
+                const float2 r = cmul(Ms[cidx(a2 - 1, mm + 1)], Ia);
+                dxy.x -= r.x;
+                dxy.y += r.y;
+              }
+            }
+          }
+          phi += ph * rinv;
+          const float r2i = rinv * rinv;
+          gx += dxy.x * r2i;
+          gy += dxy.y * r2i;
+          gz += dz * r2i;
+        }
+      }
+      if (valid) {
+        float4 v = acc[i];
+        acc[i] = make_float4(v.x + phi, v.y + gx, v.z + gy, v.w + gz);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// L2P + combine + un-permute: warp per leaf, lanes = particles. out = acc (+ L2P if use_local),
+// written to the caller's order: phi[perm[i]], grad[3 perm[i] + a].
+__global__ void __launch_bounds__(128) k_l2p(int p, const int *__restrict__ leaves, int nleaves,
+                                             CellsView C, const float4 *__restrict__ pos,
+                                             const float2 *__restrict__ L,
+                                             const float4 *__restrict__ acc,
+                                             const unsigned *__restrict__ perm,
+                                             float *__restrict__ phi_out,
+                                             float *__restrict__ grad_out, int use_local) {
+  extern __shared__ float2 sh_l2p[];
+  const int NC = nc_of(p);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float2 *Ll = sh_l2p + wib * NC;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int li = gw; li < nleaves; li += nw) {
+    const int leaf = leaves[li];
+    const int b = C.beg[leaf], cnt = C.cnt[leaf];
+    const float4 g = C.geo[leaf];
+    const float rinv = 1.f / g.w;
+    __syncwarp();
+    if (use_local)
+      for (int o = lane; o < NC; o += WARP) Ll[o] = L[(size_t)leaf * NC + o];
+    __syncwarp();
+    for (int c0 = 0; c0 < cnt; c0 += WARP) {
+      const bool valid = c0 + lane < cnt;
+      if (!valid) continue;
+      const int i = b + c0 + lane;
+      const float4 x = pos[i];
+      float4 out = acc[i];
+      if (use_local) {
+        const float xx = (x.x - g.x) * rinv, yy = (x.y - g.y) * rinv, zz = (x.z - g.z) * rinv;
+        const float r2 = xx * xx + yy * yy + zz * zz;
+        float ph = 0.f, dz = 0.f;
+        float2 dxy = make_float2(0.f, 0.f);
+        float2 Rmm = make_float2(1.f, 0.f);
+        for (int mm = 0; mm <= p; ++mm) {
+          if (mm > 0) Rmm = cscale(cmul(Rmm, make_float2(xx, yy)), -1.f / (2.f * mm));
+          float2 R2 = make_float2(0.f, 0.f), R1 = Rmm;
+          const float w = mm ? 2.f : 1.f;
+          for (int a2 = mm; a2 <= p; ++a2) {
+            float2 Ra;
+            if (a2 == mm) Ra = Rmm;
+            else if (a2 == mm + 1) Ra = cscale(Rmm, zz);
+            else {
+              const float inv = 1.f / ((float)(a2 - mm) * (float)(a2 + mm));
+              const float c1 = (2.f * a2 - 1.f) * zz;
+              Ra = make_float2((c1 * R1.x - r2 * R2.x) * inv, (c1 * R1.y - r2 * R2.y) * inv);
+            }
+            if (a2 > mm) {
+              R2 = R1;
+              R1 = Ra;
+            }
+            {  // phi: L_a^mm R_a^mm
+              const float2 lv = Ll[cidx(a2, mm)];
+              ph += w * (lv.x * Ra.x - lv.y * Ra.y);
+            }
+            if (a2 + 1 <= p) {
+              // d/dz: L_{a+1}^mm R_a^mm
+              const float2 lz = Ll[cidx(a2 + 1, mm)];
+              dz += w * (lz.x * Ra.x - lz.y * Ra.y);
+              // (dx + i dy): + L_{a+1}^{mm-1} R_a^{mm}
+              if (mm >= 1) {
+                const float2 r = cmul(Ll[cidx(a2 + 1, mm - 1)], Ra);
+                dxy.x += r.x;
+                dxy.y += r.y;
+              }
+              // (dx + i dy): - conj(L_{a+1}^{mm+1} R_a^{mm})
+              if (mm + 1 <= a2 + 1) {
+                const float2 r = cmul(Ll[cidx(a2 + 1, mm + 1)], Ra);
+                dxy.x -= r.x;
+                dxy.y += r.y;
+              }
+            }
+          }
+        }
+        const float r2i = rinv * rinv;
+        out.x += ph * rinv;
+        out.y += dxy.x * r2i;
+        out.z += dxy.y * r2i;
+        out.w += dz * r2i;
+      }
+      const size_t o = perm[i];
+      phi_out[o] = out.x;
+      grad_out[3 * o + 0] = out.y;
+      grad_out[3 * o + 1] = out.z;
+      grad_out[3 * o + 2] = out.w;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+static int warp_grid(int64_t nitems, int warps_per_block) {
+  int64_t b = (nitems + warps_per_block - 1) / warps_per_block;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)(b < 1 ? 1 : b);
+}
+
+M2LTiles make_m2l_tiles(int p) {
+  M2LTiles T;
+  T.ntiles = 0;
+  for (int j = 0; j <= p; ++j)
+    for (int k0 = 0; k0 <= j; k0 += 3) {
+      const int K = (j - k0 + 1) < 3 ? (j - k0 + 1) : 3;
+      T.tile[T.ntiles++] = j | (k0 << 8) | (K << 16);
+    }
+  return T;
+}
+
+void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos, float2 *M,
+                cudaStream_t st) {
+  ensure_nm_table();
+  k_p2m<<<warp_grid(nleaves, 4), 128, 4 * nc_of(p) * sizeof(float2), st>>>(p, leaves, nleaves, C, pos, M);
+}
+void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st) {
+  ensure_nm_table();
+  k_m2m<<<warp_grid(nl, 4), 128, 4 * 2 * nc_of(p) * sizeof(float2), st>>>(p, c0, nl, C, M);
+}
+void launch_l2l(int p, int c0, int nl, CellsView C, float2 *L, cudaStream_t st) {
+  ensure_nm_table();
+  k_l2l<<<warp_grid(nl, 4), 128, 4 * 2 * nc_of(p) * sizeof(float2), st>>>(p, c0, nl, C, L);
+}
+void launch_m2l(int p, int ncells, CellsView C, ListsView Ls, const M2LTiles &tiles,
+                const float2 *M, float2 *L, cudaStream_t st) {
+  ensure_nm_table();
+  const int nI = (2 * p + 1) * (2 * p + 1), nM = (p + 1) * (p + 1);
+  const size_t smem = (size_t)M2L_WARPS * (nM + (nI + 1) / 2) * sizeof(float4) +
+                      (size_t)M2L_WARPS * nc_of(p) * sizeof(float2);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  int blocks = ncells < 148 * 8 ? ncells : 148 * 8;
+  if (blocks < 1) blocks = 1;
+  k_m2l<<<blocks, 128, smem, st>>>(p, ncells, C, Ls, tiles, M, L);
+}
+void launch_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
+                const float4 *pos, const float2 *M, float4 *acc, cudaStream_t st) {
+  ensure_nm_table();
+  k_m2p<<<warp_grid(nleaves, 4), 128, 4 * nc_of(p) * sizeof(float2), st>>>(p, leaves, nleaves, C, Ls, pos, M, acc);
+}
+void launch_l2p(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos,
+                const float2 *L, const float4 *acc, const unsigned *perm, float *phi, float *grad,
+                int use_local, cudaStream_t st) {
+  ensure_nm_table();
+  k_l2p<<<warp_grid(nleaves, 4), 128, 4 * nc_of(p) * sizeof(float2), st>>>(p, leaves, nleaves, C, pos, L, acc, perm, phi, grad, use_local);
+}

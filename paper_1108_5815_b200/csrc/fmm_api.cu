@@ -1,0 +1,756 @@
+// fmm_api.cu — the C ABI of libfmm.so (include/fmm.h) and the stream-ordered host pipeline.
+//
+// One evaluation (every step a device kernel, the host only reads small counts):
+//   bbox + root cube -> Morton keys -> radix sort -> gather float4 -> level-synchronous tree
+//   -> P2M -> M2M (bottom-up) -> target-centric traversal (count / scan / write per level)
+//   -> M2L -> L2L (top-down) -> P2P -> M2P -> L2P + combine + un-permute.
+// FMM_DIRECT skips the tree: one all-pairs P2P.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/fmm.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+template <class T>
+struct DBuf {
+  T *p = nullptr;
+  size_t cap = 0;
+  // grow-only; contents are NOT kept
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    size_t nc = std::max(n, cap + cap / 2);
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, nc * sizeof(T));
+    if (e == cudaSuccess) cap = nc;
+    return e;
+  }
+  // grow-only; the first `keep` elements are preserved
+  cudaError_t ensure_keep(size_t n, size_t keep, cudaStream_t st) {
+    if (n <= cap) return cudaSuccess;
+    size_t nc = std::max(n, cap * 2);
+    T *q = nullptr;
+    cudaError_t e = cudaMalloc(&q, nc * sizeof(T));
+    if (e != cudaSuccess) return e;
+    if (p && keep) e = cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+    cudaStreamSynchronize(st);
+    if (p) cudaFree(p);
+    p = q;
+    cap = nc;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_N };
+
+}  // namespace
+
+struct fmm_ctx {
+  int device = 0;
+  int p = 4, ncrit = 32, mode = FMM_HYBRID;
+  double theta = 0.5;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  fmm_cost_t cost{};
+  fmm_stats_t stats{};
+  bool timing = false;
+  cudaEvent_t ev[EV_N] = {};
+  std::string err;
+  M2LTiles tiles{};
+
+  // particles
+  DBuf<uint64_t> keys_in, keys;
+  DBuf<unsigned> idx_in, perm;
+  DBuf<float4> pos, acc;
+  DBuf<char> cub_tmp;
+  // small device structs
+  RootInfo *d_root = nullptr;
+  unsigned *d_mm = nullptr;
+  int *d_small = nullptr;  // [0..7] scratch counters for readback
+  unsigned *d_overflow = nullptr;
+  unsigned long long *d_stats = nullptr;
+  int *h_small = nullptr;  // pinned
+  // cells
+  DBuf<int> cbeg, ccnt, cparent, cchild0, cnchild;
+  DBuf<int4> cgrid;
+  DBuf<float4> cgeo;
+  DBuf<uint64_t> cprefix;
+  DBuf<int> nch, excl, leafflag, leaves;
+  DBuf<int2> crange;
+  std::vector<int> level_off, level_cnt;
+  int ncells = 0, nleaves = 0, depth = 0;
+  // expansions
+  DBuf<float2> M, L;
+  // lists
+  DBuf<int> loff[3], lcnt[3];
+  DBuf<unsigned> lsrc[3];
+  DBuf<int> out_off, out_cnt, cnt4, excl4;
+  DBuf<unsigned> outA, outB, stack;
+  int stack_cap = 2048;
+  int64_t ntask[3] = {0, 0, 0};
+  bool have_tree = false;
+  int64_t last_n = 0;
+  RootInfo h_root{};
+
+  CellsView cells() {
+    CellsView C;
+    C.beg = cbeg.p;
+    C.cnt = ccnt.p;
+    C.parent = cparent.p;
+    C.child0 = cchild0.p;
+    C.nchild = cnchild.p;
+    C.grid = cgrid.p;
+    C.geo = cgeo.p;
+    return C;
+  }
+  ListsView lists() {
+    ListsView Ls;
+    for (int k = 0; k < 3; ++k) {
+      Ls.off[k] = loff[k].p;
+      Ls.cnt[k] = lcnt[k].p;
+      Ls.src[k] = lsrc[k].p;
+    }
+    return Ls;
+  }
+};
+
+static int fail(fmm_ctx *h, int code, const char *fmt, ...) {
+  if (h) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    h->err = buf;
+  }
+  return code;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? FMM_E_OOM : FMM_E_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                    \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(h, FMM_E_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_),     \
+                  __FILE__, __LINE__);                                                   \
+  } while (0)
+
+static void record(fmm_ctx *h, int e) {
+  if (h->timing) cudaEventRecord(h->ev[e], h->stream);
+}
+
+static int check_device_ptr(fmm_ctx *h, const void *ptr, const char *name) {
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, FMM_E_NOT_DEVICE, "%s is not a CUDA pointer", name);
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    return fail(h, FMM_E_NOT_DEVICE, "%s is not device memory", name);
+  if (a.device != h->device) return fail(h, FMM_E_NOT_DEVICE, "%s is on device %d, handle on %d", name, a.device, h->device);
+  return FMM_OK;
+}
+
+static int cub_scan(fmm_ctx *h, const int *in, int *out, int n) {
+  size_t bytes = 0;
+  CK(exclusive_scan(nullptr, bytes, in, out, n, h->stream));
+  CK(h->cub_tmp.ensure(bytes));
+  CK(exclusive_scan(h->cub_tmp.p, bytes, in, out, n, h->stream));
+  return FMM_OK;
+}
+
+// ---- a1-a5: bbox, keys, sort, gather, tree ----------------------------------------------------
+static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
+  cudaStream_t st = h->stream;
+  CK(h->keys_in.ensure(n));
+  CK(h->keys.ensure(n));
+  CK(h->idx_in.ensure(n));
+  CK(h->perm.ensure(n));
+  CK(h->pos.ensure(n));
+  CK(h->acc.ensure(n));
+  launch_keys(xyz, n, h->d_root, h->keys_in.p, h->idx_in.p, st);
+  CKL();
+  size_t bytes = 0;
+  CK(sort_keys(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
+  CK(h->cub_tmp.ensure(bytes));
+  CK(sort_keys(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
+  launch_gather(xyz, q, h->perm.p, n, h->pos.p, st);
+  CKL();
+
+  // level-synchronous adaptive octree: one host readback of the child count per level
+  size_t cap = std::max<size_t>(1024, (size_t)(2 * n / std::max(1, h->ncrit)) + 64);
+  auto ensure_cells = [&](size_t need, size_t keep) -> cudaError_t {
+    cudaError_t e = cudaSuccess;
+    if ((e = h->cbeg.ensure_keep(need, keep, st))) return e;
+    if ((e = h->ccnt.ensure_keep(need, keep, st))) return e;
+    if ((e = h->cparent.ensure_keep(need, keep, st))) return e;
+    if ((e = h->cchild0.ensure_keep(need, keep, st))) return e;
+    if ((e = h->cnchild.ensure_keep(need, keep, st))) return e;
+    if ((e = h->cgrid.ensure_keep(need, keep, st))) return e;
+    if ((e = h->cgeo.ensure_keep(need, keep, st))) return e;
+    return h->cprefix.ensure_keep(need, keep, st);
+  };
+  CK(ensure_cells(cap, 0));
+  launch_root_cell(n, h->d_root, h->cells(), h->cprefix.p, st);
+  CKL();
+  h->level_off.assign(1, 0);
+  h->level_cnt.assign(1, 1);
+  int total = 1;
+  for (int level = 0; level < FMM_LEVELS; ++level) {
+    const int nl = h->level_cnt[level], c0 = h->level_off[level];
+    CK(h->nch.ensure(nl));
+    CK(h->excl.ensure(nl));
+    CK(h->crange.ensure((size_t)8 * nl));
+    launch_split(c0, nl, level, h->ncrit, h->keys.p, h->cells(), h->cprefix.p, h->nch.p,
+                 h->crange.p, st);
+    CKL();
+    if (int rc = cub_scan(h, h->nch.p, h->excl.p, nl)) return rc;
+    launch_level_total(h->nch.p, h->excl.p, nl, h->d_small, st);
+    CKL();
+    CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int nnext = h->h_small[0];
+    if (nnext > 0) CK(ensure_cells((size_t)total + nnext, (size_t)total));
+    launch_emit(c0, nl, total, level, h->nch.p, h->excl.p, h->crange.p, h->d_root, h->cells(),
+                h->cprefix.p, st);
+    CKL();
+    if (nnext == 0) break;
+    h->level_off.push_back(total);
+    h->level_cnt.push_back(nnext);
+    total += nnext;
+  }
+  h->ncells = total;
+  h->depth = (int)h->level_cnt.size() - 1;
+  // leaves in cell order
+  CK(h->leafflag.ensure(total));
+  CK(h->excl.ensure(total));
+  CK(h->leaves.ensure(total));
+  launch_leaf_flags(total, h->cnchild.p, h->leafflag.p, st);
+  CKL();
+  if (int rc = cub_scan(h, h->leafflag.p, h->excl.p, total)) return rc;
+  launch_leaf_scatter(total, h->leafflag.p, h->excl.p, h->leaves.p, st);
+  CKL();
+  launch_level_total(h->leafflag.p, h->excl.p, total, h->d_small, st);
+  CKL();
+  CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->nleaves = h->h_small[0];
+  return FMM_OK;
+}
+
+// ---- a9: traversal ----------------------------------------------------------------------------
+static int traverse(fmm_ctx *h) {
+  cudaStream_t st = h->stream;
+  const int nc = h->ncells;
+  for (int k = 0; k < 3; ++k) {
+    CK(h->loff[k].ensure(nc));
+    CK(h->lcnt[k].ensure(nc));
+    CK(cudaMemsetAsync(h->lcnt[k].p, 0, sizeof(int) * nc, st));
+    CK(cudaMemsetAsync(h->loff[k].p, 0, sizeof(int) * nc, st));
+  }
+  CK(h->out_off.ensure(nc));
+  CK(h->out_cnt.ensure(nc));
+  const int warps_per_block = 4;
+  const int grid_blocks = 148 * 8;
+  const size_t nwarps = (size_t)grid_blocks * warps_per_block;
+restart:
+  CK(h->stack.ensure(nwarps * h->stack_cap));
+  CK(cudaMemsetAsync(h->d_overflow, 0, sizeof(unsigned), st));
+  CK(cudaMemsetAsync(h->d_stats, 0, 2 * sizeof(unsigned long long), st));
+  int64_t base[3] = {0, 0, 0};
+  unsigned *in_src = nullptr;
+  DBuf<unsigned> *outbuf[2] = {&h->outA, &h->outB};
+  for (int level = 0; level <= h->depth; ++level) {
+    const int nt = h->level_cnt[level], t0 = h->level_off[level];
+    CK(h->cnt4.ensure((size_t)4 * nt));
+    CK(h->excl4.ensure((size_t)4 * nt));
+    TravArgs A{};
+    A.C = h->cells();
+    A.t0 = t0;
+    A.nt = nt;
+    A.level = level;
+    A.mode = h->mode;
+    A.stack_cap = h->stack_cap;
+    A.grid_blocks = std::min(grid_blocks, (nt + warps_per_block - 1) / warps_per_block);
+    A.theta = h->theta;
+    A.t_pp = h->cost.t_pp;
+    A.t_mp = h->cost.t_mp;
+    A.t_ml = h->cost.t_ml;
+    A.in_src = in_src;
+    A.in_off = h->out_off.p;
+    A.in_cnt = h->out_cnt.p;
+    A.scratch = h->stack.p;
+    A.overflow = h->d_overflow;
+    A.cnt4 = h->cnt4.p;
+    A.excl = h->excl4.p;
+    A.stats = h->d_stats;
+    launch_traverse(A, false, st);
+    CKL();
+    if (int rc = cub_scan(h, h->cnt4.p, h->excl4.p, 4 * nt)) return rc;
+    launch_trav_totals(h->excl4.p, h->cnt4.p, nt, h->d_small, st);
+    CKL();
+    CK(cudaMemcpyAsync(h->h_small, h->d_small, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->h_small + 8, h->d_overflow, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h->h_small[8]) {
+      h->stack_cap *= 2;
+      if ((size_t)h->stack_cap * nwarps > ((size_t)1 << 31))
+        return fail(h, FMM_E_OOM, "traversal stack exceeds 8 GiB");
+      goto restart;
+    }
+    int tot[4];
+    for (int c = 0; c < 4; ++c) {
+      tot[c] = h->h_small[4 + c];
+      A.excl_base[c] = h->h_small[c];
+    }
+    for (int k = 0; k < 3; ++k) {
+      if (base[k] + tot[k] > INT32_MAX) return fail(h, FMM_E_OOM, "interaction list exceeds 2^31 entries");
+      CK(h->lsrc[k].ensure_keep((size_t)(base[k] + tot[k]) + 1, (size_t)base[k], st));
+      A.lsrc[k] = h->lsrc[k].p;
+      A.loff[k] = h->loff[k].p;
+      A.lcnt[k] = h->lcnt[k].p;
+      A.base[k] = (int)base[k];
+    }
+    DBuf<unsigned> *ob = outbuf[level & 1];
+    CK(ob->ensure((size_t)tot[3] + 1));
+    A.out_src = ob->p;
+    A.out_off = h->out_off.p;
+    A.out_cnt = h->out_cnt.p;
+    A.base[3] = 0;
+    launch_traverse(A, true, st);
+    CKL();
+    for (int k = 0; k < 3; ++k) base[k] += tot[k];
+    in_src = ob->p;
+  }
+  for (int k = 0; k < 3; ++k) h->ntask[k] = base[k];
+  unsigned long long hs[2];
+  CK(cudaMemcpyAsync(hs, h->d_stats, sizeof hs, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->stats.p2p_pairs = (int64_t)hs[0];
+  h->stats.m2p_evals = (int64_t)hs[1];
+  return FMM_OK;
+}
+
+static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
+                         float *grad) {
+  cudaStream_t st = h->stream;
+  const int p = h->p, NC = nc_of(p);
+  if (int rc = build_tree(h, xyz, q, n)) return rc;
+  record(h, EV_TREE);
+  // a7/a8 upward sweep
+  CK(h->M.ensure((size_t)h->ncells * NC));
+  CK(h->L.ensure((size_t)h->ncells * NC));
+  launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, st);
+  CKL();
+  for (int level = h->depth - 1; level >= 0; --level) {
+    launch_m2m(p, h->level_off[level], h->level_cnt[level], h->cells(), h->M.p, st);
+    CKL();
+  }
+  record(h, EV_UP);
+  if (int rc = traverse(h)) return rc;
+  record(h, EV_TRAV);
+  // a10 M2L (writes every cell's local expansion, zero where no M2L)
+  const bool far_local = h->ntask[FMM_KIND_M2L] > 0;
+  if (far_local) {
+    launch_m2l(p, h->ncells, h->cells(), h->lists(), h->tiles, h->M.p, h->L.p, st);
+    CKL();
+  }
+  record(h, EV_M2L);
+  // a12 P2P (writes acc), a11 M2P (adds)
+  launch_p2p_leaves(h->leaves.p, h->nleaves, h->cells(), h->lists(), h->pos.p, h->acc.p, st);
+  CKL();
+  record(h, EV_P2P);
+  if (h->ntask[FMM_KIND_M2P] > 0) {
+    launch_m2p(p, h->leaves.p, h->nleaves, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, st);
+    CKL();
+  }
+  record(h, EV_M2P);
+  // a13 L2L top-down, a14/a15 L2P + combine + un-permute
+  if (far_local) {
+    for (int level = 1; level <= h->depth; ++level) {
+      launch_l2l(p, h->level_off[level], h->level_cnt[level], h->cells(), h->L.p, st);
+      CKL();
+    }
+  }
+  launch_l2p(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, phi,
+             grad, far_local ? 1 : 0, st);
+  CKL();
+  record(h, EV_DOWN);
+  h->have_tree = true;
+  return FMM_OK;
+}
+
+static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
+                         float *grad) {
+  cudaStream_t st = h->stream;
+  memset(&h->stats, 0, sizeof h->stats);
+  h->stats.n = n;
+  h->stats.p = h->p;
+  if (n == 0) return FMM_OK;
+  if (n > (int64_t)1 << 28) return fail(h, FMM_E_INVALID, "n = %lld exceeds 2^28 per device", (long long)n);
+  record(h, EV_START);
+  launch_bbox(xyz, q, n, h->d_mm, h->d_root, st);
+  CKL();
+  CK(cudaMemcpyAsync(&h->h_root, h->d_root, sizeof(RootInfo), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h->h_root.nonfinite) return fail(h, FMM_E_NONFINITE, "non-finite coordinate or charge");
+  h->last_n = n;
+  if (h->mode == FMM_DIRECT) {
+    CK(h->pos.ensure(n));
+    launch_gather(xyz, q, nullptr, n, h->pos.p, st);
+    CKL();
+    record(h, EV_TREE);
+    record(h, EV_UP);
+    record(h, EV_TRAV);
+    record(h, EV_M2L);
+    launch_p2p_direct(n, h->pos.p, phi, grad, st);
+    CKL();
+    record(h, EV_P2P);
+    record(h, EV_M2P);
+    record(h, EV_DOWN);
+    h->have_tree = false;
+    h->stats.p2p_pairs = n * n;
+    h->stats.n_p2p = 1;
+  } else {
+    if (int rc = evaluate_tree(h, xyz, q, n, phi, grad)) return rc;
+    h->stats.ncells = h->ncells;
+    h->stats.nleaves = h->nleaves;
+    h->stats.depth = h->depth;
+    h->stats.n_m2l = h->ntask[0];
+    h->stats.n_m2p = h->ntask[1];
+    h->stats.n_p2p = h->ntask[2];
+  }
+  CK(cudaStreamSynchronize(st));
+  if (h->timing) {
+    float ms[EV_N];
+    for (int e = 1; e < EV_N; ++e) cudaEventElapsedTime(&ms[e], h->ev[e - 1], h->ev[e]);
+    cudaEventElapsedTime(&ms[0], h->ev[EV_START], h->ev[EV_DOWN]);
+    h->stats.ms_total = ms[0];
+    h->stats.ms_tree = ms[EV_TREE];
+    h->stats.ms_upward = ms[EV_UP];
+    h->stats.ms_traverse = ms[EV_TRAV];
+    h->stats.ms_m2l = ms[EV_M2L];
+    h->stats.ms_p2p = ms[EV_P2P];
+    h->stats.ms_m2p = ms[EV_M2P];
+    h->stats.ms_downward = ms[EV_DOWN];
+  }
+  return FMM_OK;
+}
+
+// ---- a6: kernel pre-calculation ------------------------------------
+// The kernels are timed on artificial data at a saturating size (P:189 warns that small tests
+// mispredict GPU times): a synthetic uniform cube of 2^20 random particles is evaluated in FMM
+// mode (every accepted pair an M2L) and in treecode mode (every accepted pair an M2P); the
+// per-unit costs are the kernel times (CUDA events, median of 3 after a warm-up) divided by the
+// work counts the traversal reports.
+static int tune_impl(fmm_ctx *h) {
+  const int64_t n = (int64_t)1 << 20;
+  float *d = nullptr;
+  CK(cudaMalloc(&d, sizeof(float) * 8 * n));
+  float *xyz = d, *q = d + 3 * n, *phi = d + 4 * n, *grad = d + 5 * n;
+  launch_fill_random(xyz, 3 * n, 12345u, 0.f, 1.f, h->stream);
+  launch_fill_random(q, n, 777u, 1.0f / n, 1.0f / n, h->stream);
+  CKL();
+  const int saved_mode = h->mode;
+  const bool saved_timing = h->timing;
+  h->timing = true;
+  double t_pp[3], t_ml[3], t_mp[3];
+  int rc = FMM_OK;
+  for (int pass = 0; pass < 2 && rc == FMM_OK; ++pass) {
+    h->mode = pass == 0 ? FMM_FMM : FMM_TREECODE;
+    for (int it = -1; it < 3 && rc == FMM_OK; ++it) {
+      rc = evaluate_impl(h, xyz, q, n, phi, grad);
+      if (it < 0 || rc) continue;
+      const fmm_stats_t &s = h->stats;
+      if (pass == 0) {
+        t_pp[it] = s.ms_p2p * 1e-3 / std::max<int64_t>(1, s.p2p_pairs);
+        t_ml[it] = s.ms_m2l * 1e-3 / std::max<int64_t>(1, s.n_m2l);
+      } else {
+        t_mp[it] = s.ms_m2p * 1e-3 / std::max<int64_t>(1, s.m2p_evals);
+      }
+    }
+  }
+  h->mode = saved_mode;
+  h->timing = saved_timing;
+  cudaFree(d);
+  if (rc) return rc;
+  auto med3 = [](double *a) { std::sort(a, a + 3); return a[1]; };
+  h->cost.t_pp = med3(t_pp);
+  h->cost.t_ml = med3(t_ml);
+  h->cost.t_mp = med3(t_mp);
+  h->cost.p = h->p;
+  h->cost.measured = 1;
+  h->have_tree = false;
+  return FMM_OK;
+}
+
+// ================================ C ABI =========================================================
+extern "C" {
+
+int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
+  if (!out) return FMM_E_INVALID;
+  *out = nullptr;
+  if (p < 1 || p > FMM_P_MAX || !(theta > 0.0 && theta < 1.0) || ncrit < 1) return FMM_E_INVALID;
+  fmm_ctx *h = new (std::nothrow) fmm_ctx();
+  if (!h) return FMM_E_OOM;
+  h->p = p;
+  h->theta = theta;
+  h->ncrit = ncrit;
+  h->tiles = make_m2l_tiles(p);
+  // default cost model until measured: ~B200 order of magnitude (overwritten by the tuning)
+  h->cost.t_pp = 2e-12;
+  h->cost.t_mp = 5e-11;
+  h->cost.t_ml = 3e-9;
+  h->cost.p = p;
+  h->cost.measured = 0;
+  int rc = FMM_OK;
+  do {
+    cudaError_t e;
+    if ((e = cudaGetDevice(&h->device)) != cudaSuccess) { rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e)); break; }
+    if ((e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking)) != cudaSuccess) { rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e)); break; }
+    h->stream = h->own_stream;
+    for (int i = 0; i < EV_N; ++i) cudaEventCreate(&h->ev[i]);
+    if (cudaMalloc(&h->d_root, sizeof(RootInfo)) || cudaMalloc(&h->d_mm, 8 * sizeof(unsigned)) ||
+        cudaMalloc(&h->d_small, 16 * sizeof(int)) || cudaMalloc(&h->d_overflow, sizeof(unsigned)) ||
+        cudaMalloc(&h->d_stats, 4 * sizeof(unsigned long long)) ||
+        cudaMallocHost(&h->h_small, 16 * sizeof(int))) {
+      rc = fail(h, FMM_E_OOM, "small device allocations failed");
+      break;
+    }
+    const char *nt = getenv("FMM_NO_TUNE");
+    if (!(nt && nt[0] && nt[0] != '0')) rc = tune_impl(h);
+  } while (0);
+  if (rc != FMM_OK) {
+    fmm_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return FMM_OK;
+}
+
+int fmm_destroy(fmm_t h) {
+  if (!h) return FMM_OK;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->keys_in.release(); h->keys.release(); h->idx_in.release(); h->perm.release();
+  h->pos.release(); h->acc.release(); h->cub_tmp.release();
+  h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
+  h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release();
+  h->nch.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
+  h->M.release(); h->L.release();
+  for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
+  h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
+  h->outA.release(); h->outB.release(); h->stack.release();
+  if (h->d_root) cudaFree(h->d_root);
+  if (h->d_mm) cudaFree(h->d_mm);
+  if (h->d_small) cudaFree(h->d_small);
+  if (h->d_overflow) cudaFree(h->d_overflow);
+  if (h->d_stats) cudaFree(h->d_stats);
+  if (h->h_small) cudaFreeHost(h->h_small);
+  for (int i = 0; i < EV_N; ++i)
+    if (h->ev[i]) cudaEventDestroy(h->ev[i]);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+  return FMM_OK;
+}
+
+int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float *d_phi,
+                 float *d_grad) {
+  if (!h) return FMM_E_INVALID;
+  if (n < 0) return fail(h, FMM_E_INVALID, "n < 0");
+  if (n == 0) {
+    memset(&h->stats, 0, sizeof h->stats);
+    return FMM_OK;
+  }
+  if (!d_xyz || !d_q || !d_phi || !d_grad) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != h->device) cudaSetDevice(h->device);
+  int rc = check_device_ptr(h, d_xyz, "xyz");
+  if (!rc) rc = check_device_ptr(h, d_q, "q");
+  if (!rc) rc = check_device_ptr(h, d_phi, "phi");
+  if (!rc) rc = check_device_ptr(h, d_grad, "grad");
+  if (!rc) rc = evaluate_impl(h, d_xyz, d_q, n, d_phi, d_grad);
+  if (cur != h->device && cur >= 0) cudaSetDevice(cur);
+  return rc;
+}
+
+int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, float *h_phi,
+                      float *h_grad) {
+  if (!h) return FMM_E_INVALID;
+  if (n < 0) return fail(h, FMM_E_INVALID, "n < 0");
+  if (n == 0) return FMM_OK;
+  if (!h_xyz || !h_q || !h_phi || !h_grad) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
+  float *d = nullptr;
+  CK(cudaMallocAsync(&d, sizeof(float) * 8 * (size_t)n, h->stream));
+  float *xyz = d, *q = d + 3 * n, *phi = d + 4 * n, *grad = d + 5 * n;
+  int rc = FMM_OK;
+  cudaError_t e = cudaMemcpyAsync(xyz, h_xyz, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, h->stream);
+  if (!e) e = cudaMemcpyAsync(q, h_q, sizeof(float) * n, cudaMemcpyHostToDevice, h->stream);
+  if (e) rc = fail(h, FMM_E_CUDA, "H2D: %s", cudaGetErrorString(e));
+  if (!rc) rc = evaluate_impl(h, xyz, q, n, phi, grad);
+  if (!rc) {
+    e = cudaMemcpyAsync(h_phi, phi, sizeof(float) * n, cudaMemcpyDeviceToHost, h->stream);
+    if (!e) e = cudaMemcpyAsync(h_grad, grad, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, h->stream);
+    if (!e) e = cudaStreamSynchronize(h->stream);
+    if (e) rc = fail(h, FMM_E_CUDA, "D2H: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(d, h->stream);
+  cudaStreamSynchronize(h->stream);
+  return rc;
+}
+
+int fmm_set_stream(fmm_t h, void *stream) {
+  if (!h) return FMM_E_INVALID;
+  h->stream = stream ? (cudaStream_t)stream : h->own_stream;
+  return FMM_OK;
+}
+
+int fmm_set_mode(fmm_t h, int mode) {
+  if (!h) return FMM_E_INVALID;
+  if (mode < FMM_HYBRID || mode > FMM_DIRECT) return fail(h, FMM_E_INVALID, "bad mode %d", mode);
+  h->mode = mode;
+  return FMM_OK;
+}
+
+int fmm_set_timing(fmm_t h, int enable) {
+  if (!h) return FMM_E_INVALID;
+  h->timing = enable != 0;
+  return FMM_OK;
+}
+
+int fmm_tune(fmm_t h) {
+  if (!h) return FMM_E_INVALID;
+  return tune_impl(h);
+}
+
+int fmm_get_cost_model(fmm_t h, fmm_cost_t *out) {
+  if (!h || !out) return FMM_E_INVALID;
+  *out = h->cost;
+  return FMM_OK;
+}
+
+int fmm_set_cost_model(fmm_t h, const fmm_cost_t *in) {
+  if (!h || !in) return FMM_E_INVALID;
+  if (in->p != h->p) return fail(h, FMM_E_INVALID, "cost model for p=%d, handle p=%d", in->p, h->p);
+  if (!(in->t_pp >= 0 && in->t_mp >= 0 && in->t_ml >= 0)) return fail(h, FMM_E_INVALID, "negative cost");
+  h->cost = *in;
+  return FMM_OK;
+}
+
+int fmm_get_stats(fmm_t h, fmm_stats_t *out) {
+  if (!h || !out) return FMM_E_INVALID;
+  *out = h->stats;
+  return FMM_OK;
+}
+
+int fmm_export_tree(fmm_t h, int64_t cap, int32_t *h_level, uint64_t *h_prefix, int64_t *h_begin,
+                    int64_t *h_count, int64_t *count_out) {
+  if (!h || !count_out) return FMM_E_INVALID;
+  if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
+  const int nc = h->ncells;
+  *count_out = nc;
+  if (cap < nc) return fail(h, FMM_E_INVALID, "cap %lld < %d cells", (long long)cap, nc);
+  std::vector<int> beg(nc), cnt(nc);
+  std::vector<int4> grid(nc);
+  CK(cudaMemcpy(beg.data(), h->cbeg.p, sizeof(int) * nc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cnt.data(), h->ccnt.p, sizeof(int) * nc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(grid.data(), h->cgrid.p, sizeof(int4) * nc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h_prefix, h->cprefix.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost));
+  for (int c = 0; c < nc; ++c) {  // BFS order is already (level, prefix) order
+    h_level[c] = grid[c].w;
+    h_begin[c] = beg[c];
+    h_count[c] = cnt[c];
+  }
+  return FMM_OK;
+}
+
+int fmm_export_lists(fmm_t h, int64_t cap, int32_t *h_kind, int32_t *h_tlevel, uint64_t *h_tprefix,
+                     int32_t *h_slevel, uint64_t *h_sprefix, int64_t *count_out) {
+  if (!h || !count_out) return FMM_E_INVALID;
+  if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
+  const int nc = h->ncells;
+  const int64_t total = h->ntask[0] + h->ntask[1] + h->ntask[2];
+  *count_out = total;
+  if (cap < total) return fail(h, FMM_E_INVALID, "cap %lld < %lld pairs", (long long)cap, (long long)total);
+  std::vector<int4> grid(nc);
+  std::vector<uint64_t> prefix(nc);
+  CK(cudaMemcpy(grid.data(), h->cgrid.p, sizeof(int4) * nc, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(prefix.data(), h->cprefix.p, sizeof(uint64_t) * nc, cudaMemcpyDeviceToHost));
+  int64_t row = 0;
+  for (int k = 0; k < 3; ++k) {
+    std::vector<int> off(nc), cnt(nc);
+    std::vector<unsigned> src(h->ntask[k] + 1);
+    CK(cudaMemcpy(off.data(), h->loff[k].p, sizeof(int) * nc, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cnt.data(), h->lcnt[k].p, sizeof(int) * nc, cudaMemcpyDeviceToHost));
+    if (h->ntask[k]) CK(cudaMemcpy(src.data(), h->lsrc[k].p, sizeof(unsigned) * h->ntask[k], cudaMemcpyDeviceToHost));
+    for (int t = 0; t < nc; ++t)
+      for (int e = 0; e < cnt[t]; ++e) {
+        const unsigned s = src[off[t] + e];
+        h_kind[row] = k;
+        h_tlevel[row] = grid[t].w;
+        h_tprefix[row] = prefix[t];
+        h_slevel[row] = grid[s].w;
+        h_sprefix[row] = prefix[s];
+        ++row;
+      }
+  }
+  return FMM_OK;
+}
+
+int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, double *h_origin3,
+                    double *h_L) {
+  if (!h) return FMM_E_INVALID;
+  if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
+  const int64_t n = h->last_n;
+  if (cap < n) return fail(h, FMM_E_INVALID, "cap too small");
+  std::vector<unsigned> perm(n);
+  CK(cudaMemcpy(perm.data(), h->perm.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < n; ++i) h_perm[i] = perm[i];
+  if (h_keys) CK(cudaMemcpy(h_keys, h->keys.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  if (h_origin3) for (int a = 0; a < 3; ++a) h_origin3[a] = h->h_root.origin[a];
+  if (h_L) *h_L = h->h_root.L;
+  return FMM_OK;
+}
+
+const char *fmm_strerror(int code) {
+  switch (code) {
+    case FMM_OK: return "ok";
+    case FMM_E_INVALID: return "invalid argument";
+    case FMM_E_NOT_DEVICE: return "pointer is not device memory of the handle's device";
+    case FMM_E_NONFINITE: return "non-finite input";
+    case FMM_E_CUDA: return "CUDA error";
+    case FMM_E_OOM: return "out of device memory";
+    case FMM_E_NCCL: return "NCCL error";
+    case FMM_E_STATE: return "no evaluation yet";
+    default: return "unknown error";
+  }
+}
+
+const char *fmm_last_error(fmm_t h) { return h ? h->err.c_str() : "NULL handle"; }
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// kernels.cuh — host-side launcher declarations of the sm_100a kernels (internal to libfmm.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+// ---- tree.cu ----
+void launch_bbox(const float *xyz, const float *q, int64_t n, unsigned *mm, RootInfo *root,
+                 cudaStream_t st);
+void launch_keys(const float *xyz, int64_t n, const RootInfo *root, uint64_t *keys, unsigned *idx,
+                 cudaStream_t st);
+void launch_gather(const float *xyz, const float *q, const unsigned *perm, int64_t n, float4 *pos,
+                   cudaStream_t st);
+cudaError_t sort_keys(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
+                      const unsigned *vin, unsigned *vout, int64_t n, cudaStream_t st);
+cudaError_t exclusive_scan(void *tmp, size_t &tmp_bytes, const int *in, int *out, int n,
+                           cudaStream_t st);
+void launch_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64_t *prefix,
+                      cudaStream_t st);
+void launch_split(int c0, int nl, int level, int ncrit, const uint64_t *keys, CellsView C,
+                  const uint64_t *prefix, int *nch, int2 *crange, cudaStream_t st);
+void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int *excl,
+                 const int2 *crange, const RootInfo *root, CellsView C, uint64_t *prefix,
+                 cudaStream_t st);
+void launch_level_total(const int *nch, const int *excl, int nl, int *total, cudaStream_t st);
+void launch_leaf_flags(int ncells, const int *nchild, int *flag, cudaStream_t st);
+void launch_leaf_scatter(int ncells, const int *flag, const int *excl, int *leaves,
+                         cudaStream_t st);
+
+// ---- traverse.cu ----
+struct TravArgs {
+  CellsView C;
+  int t0, nt, level, mode, stack_cap, grid_blocks;
+  double theta, t_pp, t_mp, t_ml;
+  const unsigned *in_src;
+  const int *in_off, *in_cnt;
+  unsigned *scratch, *overflow;
+  int *cnt4;
+  const int *excl;
+  int base[4], excl_base[4];
+  unsigned *lsrc[3];
+  int *loff[3], *lcnt[3];
+  unsigned *out_src;
+  int *out_off, *out_cnt;
+  unsigned long long *stats;  // [0] P2P particle pairs, [1] M2P target evaluations
+};
+void launch_traverse(const TravArgs &A, bool write, cudaStream_t st);
+void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *out8, cudaStream_t st);
+
+// ---- expansions.cu ----
+struct M2LTiles {
+  int ntiles;
+  int tile[64];  // j | k0 << 8 | K << 16
+};
+void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos, float2 *M,
+                cudaStream_t st);
+void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st);
+void launch_m2l(int p, int ncells, CellsView C, ListsView Ls, const M2LTiles &tiles,
+                const float2 *M, float2 *L, cudaStream_t st);
+void launch_l2l(int p, int c0, int nl, CellsView C, float2 *L, cudaStream_t st);
+void launch_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
+                const float4 *pos, const float2 *M, float4 *acc, cudaStream_t st);
+void launch_l2p(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos,
+                const float2 *L, const float4 *acc, const unsigned *perm, float *phi, float *grad,
+                int use_local, cudaStream_t st);
+M2LTiles make_m2l_tiles(int p);
+
+// ---- p2p.cu ----
+void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
+                       const float4 *pos, float4 *acc, cudaStream_t st);
+void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cudaStream_t st);
+
+// ---- synthetic batches for the kernel pre-calculation (autotune.cu) ----
+void launch_fill_random(float *dst, int64_t n, unsigned seed, float lo, float hi,
+                        cudaStream_t st);

@@ -1,0 +1,188 @@
+// traverse.cu — dual tree traversal on the device.
+//
+// The paper's traversal pops (target, source) pairs from a LIFO stack, splits the larger cell and
+// either evaluates each offspring pair at once (MAC accepted) or pushes it. The
+// emitted multiset does not depend on the processing order (each pair's fate is a pure function
+// of the pair), so the device runs it TARGET-CENTRIC and level-synchronous: one warp owns one
+// target cell t of the current level and runs the paper's stack for all pairs (t, s); a pair
+// whose target must be split is deferred to Out(t), which every child of t inherits as its
+// starting list at the next level ("target cells inherit a unique stack of source cells from
+// their parents"). Each target's interaction lists therefore come out contiguous and in
+// a deterministic order, with no global sort.
+//
+// Two passes per level: COUNT (sizes per target) -> one exclusive scan -> WRITE (same logic,
+// writing at the scanned offsets). The MAC is the exact integer/FP64 test of DESIGN.md §3 (R4, R5)
+// and the kind choice the linear cost model with ties M2L > M2P > P2P (R8).
+#include "common.cuh"
+#include "kernels.cuh"
+
+enum { CAT_M2L = 0, CAT_M2P = 1, CAT_P2P = 2, CAT_OUT = 3, CAT_PUSH = 4, CAT_NONE = 5 };
+
+__device__ __forceinline__ bool mac_accept(int4 gt, int4 gs, double theta) {
+  const long long dx = gt.x - gs.x, dy = gt.y - gs.y, dz = gt.z - gs.z;
+  const long long R2 = dx * dx + dy * dy + dz * dz;
+  const long long rsum = (1LL << (FMM_LEVELS - gt.w)) + (1LL << (FMM_LEVELS - gs.w));
+  const double rhs = __dmul_rn(theta, __dsqrt_rn(__ll2double_rn(R2)));
+  return __ll2double_rn(rsum) <= rhs;
+}
+
+__device__ __forceinline__ int select_kind(const TravArgs &A, int nt, int ns) {
+  if (A.mode == 1) return CAT_M2L;  // FMM_FMM
+  if (A.mode == 2) return CAT_M2P;  // FMM_TREECODE
+  const double cpp = __dmul_rn(__dmul_rn(A.t_pp, (double)nt), (double)ns);
+  const double cmp = __dmul_rn(A.t_mp, (double)nt);
+  const double cml = A.t_ml;
+  if (cml <= cmp && cml <= cpp) return CAT_M2L;
+  if (cmp <= cpp) return CAT_M2P;
+  return CAT_P2P;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
+  const CellsView C = A.C;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  unsigned *stack = A.scratch + (size_t)gw * A.stack_cap;
+
+  for (int k = gw; k < A.nt; k += nw) {
+    const int t = A.t0 + k;
+    const int4 gt = C.grid[t];
+    const int tcnt = C.cnt[t];
+    const bool tleaf = C.nchild[t] == 0;
+    int n[4] = {0, 0, 0, 0};
+    unsigned *dst[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (WRITE) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int o = A.base[c] + A.excl[c * A.nt + k] - A.excl_base[c];
+        dst[c] = (c < 3 ? A.lsrc[c] : A.out_src) + o;
+        if (lane == 0) {
+          if (c < 3) {
+            A.loff[c][t] = o;
+            A.lcnt[c][t] = A.cnt4[c * A.nt + k];
+          } else {
+            A.out_off[t] = o;
+            A.out_cnt[t] = A.cnt4[c * A.nt + k];
+          }
+        }
+      }
+    }
+    unsigned long long pp_pairs = 0, mp_evals = 0;
+    int top = 0;
+    bool overflow = false;
+
+    // classify (t, s) and append it to its category with ballots (deterministic order)
+    auto consider_and_put = [&](bool valid, unsigned s, int forced_cat) {
+      int cat = CAT_NONE;
+      int scnt = 0;
+      if (valid) {
+        if (forced_cat >= 0) {
+          cat = forced_cat;
+        } else {
+          const int4 gs = C.grid[s];
+          scnt = C.cnt[s];
+          if (mac_accept(gt, gs, A.theta))
+            cat = select_kind(A, tcnt, scnt);
+          else if (tleaf && C.nchild[s] == 0)
+            cat = CAT_P2P;
+          else
+            cat = CAT_PUSH;
+        }
+      }
+      if (!WRITE) {
+        if (cat == CAT_P2P) pp_pairs += (unsigned long long)tcnt * (unsigned long long)scnt;
+        if (cat == CAT_M2P) mp_evals += (unsigned long long)tcnt;
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        const unsigned b = __ballot_sync(0xffffffffu, cat == c);
+        if (!b) continue;
+        const int pos = __popc(b & lt_mask);
+        if (c == CAT_PUSH) {
+          if (cat == c && top + pos < A.stack_cap) stack[top + pos] = s;
+          top += __popc(b);
+          if (top > A.stack_cap) overflow = true;
+        } else {
+          if (WRITE && cat == c) dst[c][n[c] + pos] = s;
+          n[c] += __popc(b);
+        }
+      }
+    };
+
+    // 1) inherited pairs (parent(t), s) split on the target side: test (t, s)
+    int in_off = 0, in_cnt = 1;
+    if (A.level > 0) {
+      const int p = C.parent[t];
+      in_off = A.in_off[p];
+      in_cnt = A.in_cnt[p];
+    }
+    for (int b0 = 0; b0 < in_cnt; b0 += 32) {
+      const int e = b0 + lane;
+      const bool valid = e < in_cnt;
+      const unsigned s = valid ? (A.level > 0 ? A.in_src[in_off + e] : 0u) : 0u;
+      consider_and_put(valid, s, -1);
+    }
+    __syncwarp();
+    // 2) the paper's stack: pop, split the larger cell (ties and leaf targets split the source)
+    while (top > 0 && !overflow) {
+      const int nb = min(top, 32);
+      top -= nb;
+      const bool valid = lane < nb;
+      const unsigned s = valid ? stack[top + lane] : 0u;
+      __syncwarp();
+      int snch = 0;
+      bool split_src = false;
+      if (valid) {
+        snch = C.nchild[s];
+        split_src = tleaf || (snch > 0 && C.grid[s].w <= gt.w);
+      }
+      consider_and_put(valid && !split_src, s, CAT_OUT);  // target splits: defer to children
+      const int c0 = split_src ? C.child0[s] : 0;
+      const int m = split_src ? snch : 0;
+      int mmax = m;
+      for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+      for (int j = 0; j < mmax; ++j) consider_and_put(j < m, (unsigned)(c0 + j), -1);
+      __syncwarp();
+    }
+    if (overflow) {
+      if (lane == 0) atomicOr(A.overflow, 1u);
+      continue;
+    }
+    if (!WRITE) {
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) A.cnt4[c * A.nt + k] = n[c];
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        pp_pairs += __shfl_xor_sync(0xffffffffu, pp_pairs, o);
+        mp_evals += __shfl_xor_sync(0xffffffffu, mp_evals, o);
+      }
+      if (lane == 0) {
+        atomicAdd(&A.stats[0], pp_pairs);
+        atomicAdd(&A.stats[1], mp_evals);
+      }
+    }
+  }
+}
+
+// level totals: bases of the four sub-arrays of the one exclusive scan, and the level sizes
+__global__ void k_trav_totals(const int *excl, const int *cnt4, int nt, int *out8) {
+  for (int c = 0; c < 4; ++c) {
+    out8[c] = excl[c * nt];
+    const int last = (c + 1) * nt - 1;
+    out8[4 + c] = excl[last] + cnt4[last] - excl[c * nt];
+  }
+}
+
+void launch_traverse(const TravArgs &A, bool write, cudaStream_t st) {
+  const int blocks = A.grid_blocks;
+  if (write)
+    k_traverse<true><<<blocks, 128, 0, st>>>(A);
+  else
+    k_traverse<false><<<blocks, 128, 0, st>>>(A);
+}
+void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *out8, cudaStream_t st) {
+  k_trav_totals<<<1, 1, 0, st>>>(excl, cnt4, nt, out8);
+}

@@ -1,0 +1,290 @@
+// tree.cu — root cube, Morton keys, sort/gather and the level-synchronous adaptive octree.
+//
+// SURVEY §8(a) a1-a5. The paper builds the tree on the host even in its GPU runs;
+// here every step runs on the device. The key is a pure function of the float32 input
+// (power-of-two root cube, exact FP64 scaling with explicit _rn intrinsics so nothing is
+// contracted into an FMA), so the tree equals the one defined in DESIGN.md §3 bit for bit.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+// ---- a1: bounding box + non-finite check ---------------------------------------------------
+__device__ __forceinline__ unsigned f2ord(float f) {
+  unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void k_bbox_init(unsigned *mm, RootInfo *root) {
+  if (threadIdx.x < 3) mm[threadIdx.x] = 0xffffffffu;
+  else if (threadIdx.x < 6) mm[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) root->nonfinite = 0;
+}
+
+__global__ void __launch_bounds__(256) k_bbox(const float *__restrict__ xyz,
+                                              const float *__restrict__ q, int64_t n,
+                                              unsigned *mm, RootInfo *root) {
+  unsigned lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0, 0, 0};
+  unsigned bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = xyz[3 * i + a];
+      bad |= !isfinite(v);
+      const unsigned o = f2ord(v);
+      lo[a] = min(lo[a], o);
+      hi[a] = max(hi[a], o);
+    }
+    bad |= !isfinite(q[i]);
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int s = 16; s > 0; s >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], s));
+      hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], s));
+    }
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&mm[a], lo[a]);
+      atomicMax(&mm[3 + a], hi[a]);
+    }
+    if (bad) atomicOr(&root->nonfinite, 1u);
+  }
+}
+
+// Root cube: centre of the bbox, side L = 2^ceil(log2 extent) (1 if the extent is 0).
+__global__ void k_root(const unsigned *mm, RootInfo *root) {
+  if (root->nonfinite) {  // the host reports FMM_E_NONFINITE; keep the cube finite meanwhile
+    for (int a = 0; a < 3; ++a) root->origin[a] = 0.0;
+    root->L = 1.0;
+    root->scale = 2097152.0;
+    return;
+  }
+  double mn[3], mx[3], ext = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    mn[a] = (double)ord2f(mm[a]);
+    mx[a] = (double)ord2f(mm[3 + a]);
+    const double e = __dsub_rn(mx[a], mn[a]);
+    if (e > ext) ext = e;
+  }
+  double side = 1.0;
+  if (ext > 0.0) {
+    while (side < ext) side *= 2.0;
+    while (side * 0.5 >= ext) side *= 0.5;
+  }
+  for (int a = 0; a < 3; ++a)
+    root->origin[a] = __dsub_rn(__dmul_rn(0.5, __dadd_rn(mn[a], mx[a])), __dmul_rn(0.5, side));
+  root->L = side;
+  root->scale = 2097152.0 / side;
+}
+
+// ---- a2: Morton keys -------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_keys(const float *__restrict__ xyz, int64_t n,
+                                              const RootInfo *__restrict__ root,
+                                              uint64_t *__restrict__ keys,
+                                              unsigned *__restrict__ idx) {
+  const double o0 = root->origin[0], o1 = root->origin[1], o2 = root->origin[2],
+               sc = root->scale;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double o[3] = {o0, o1, o2};
+    uint64_t g[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double t = floor(__dmul_rn(__dsub_rn((double)xyz[3 * i + a], o[a]), sc));
+      t = fmin(fmax(t, 0.0), 2097151.0);
+      g[a] = (uint64_t)t;
+    }
+    keys[i] = (spread3(g[0]) << 2) | (spread3(g[1]) << 1) | spread3(g[2]);
+    idx[i] = (unsigned)i;
+  }
+}
+
+// ---- a3: gather into Morton-sorted SoA float4 ------------------------------------------------
+__global__ void __launch_bounds__(256) k_gather(const float *__restrict__ xyz,
+                                                const float *__restrict__ q,
+                                                const unsigned *__restrict__ perm, int64_t n,
+                                                float4 *__restrict__ pos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned o = perm ? perm[i] : (unsigned)i;
+    pos[i] = make_float4(xyz[3 * (int64_t)o], xyz[3 * (int64_t)o + 1], xyz[3 * (int64_t)o + 2], q[o]);
+  }
+}
+
+// ---- a4/a5: level-synchronous adaptive octree -------------------------------------------------
+__device__ __forceinline__ void cell_geometry(uint64_t prefix, int level, const RootInfo *root,
+                                              int4 *grid, float4 *geo) {
+  // de-interleave the level-bit prefix into integer cell coordinates
+  unsigned g[3] = {0, 0, 0};
+  for (int b = 0; b < level; ++b) {
+    g[0] |= (unsigned)((prefix >> (3 * b + 2)) & 1) << b;
+    g[1] |= (unsigned)((prefix >> (3 * b + 1)) & 1) << b;
+    g[2] |= (unsigned)((prefix >> (3 * b + 0)) & 1) << b;
+  }
+  const int unit = 1 << (FMM_LEVELS - level);
+  *grid = make_int4((2 * (int)g[0] + 1) * unit, (2 * (int)g[1] + 1) * unit,
+                    (2 * (int)g[2] + 1) * unit, level);
+  const double w = root->L / (double)(1u << level);  // exact: power of two
+  *geo = make_float4((float)(root->origin[0] + ((double)g[0] + 0.5) * w),
+                     (float)(root->origin[1] + ((double)g[1] + 0.5) * w),
+                     (float)(root->origin[2] + ((double)g[2] + 0.5) * w), (float)(0.5 * w));
+}
+
+__global__ void k_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64_t *prefix) {
+  C.beg[0] = 0;
+  C.cnt[0] = (int)n;
+  C.parent[0] = -1;
+  C.child0[0] = -1;
+  C.nchild[0] = 0;
+  prefix[0] = 0;
+  cell_geometry(0, 0, root, &C.grid[0], &C.geo[0]);
+}
+
+// For each cell of level `level` (ids [c0, c0 + nl)): child sub-ranges by binary search on the
+// sorted keys. A cell is split iff count > ncrit and level < 21.
+__global__ void __launch_bounds__(256) k_split(int c0, int nl, int level, int ncrit,
+                                               const uint64_t *__restrict__ keys, CellsView C,
+                                               const uint64_t *__restrict__ prefix,
+                                               int *__restrict__ nch, int2 *__restrict__ crange) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nl) return;
+  const int c = c0 + k;
+  const int b = C.beg[c], n = C.cnt[c];
+  int cnt = 0;
+  if (n > ncrit && level < FMM_LEVELS) {
+    const int shift = 3 * (FMM_LEVELS - (level + 1));
+    const uint64_t base = prefix[c] * 8;
+    int lo = b;
+    for (int o = 0; o < 8; ++o) {
+      // first index >= lo whose child prefix exceeds base + o
+      int l = lo, r = b + n;
+      const uint64_t tgt = base + (uint64_t)o;
+      while (l < r) {
+        const int m = (l + r) >> 1;
+        if ((keys[m] >> shift) <= tgt) l = m + 1;
+        else r = m;
+      }
+      if (l > lo) crange[8 * k + cnt++] = make_int2(lo, (l - lo) | (o << 28));
+      lo = l;
+    }
+  }
+  nch[k] = cnt;
+}
+
+__global__ void __launch_bounds__(256) k_emit(int c0, int nl, int next0, int level,
+                                              const int *__restrict__ nch,
+                                              const int *__restrict__ excl,
+                                              const int2 *__restrict__ crange,
+                                              const RootInfo *__restrict__ root, CellsView C,
+                                              uint64_t *__restrict__ prefix) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nl) return;
+  const int c = c0 + k;
+  const int m = nch[k];
+  const int first = next0 + excl[k];
+  C.nchild[c] = m;
+  C.child0[c] = m ? first : -1;
+  const uint64_t pp = prefix[c];
+  for (int j = 0; j < m; ++j) {
+    const int2 r = crange[8 * k + j];
+    const int id = first + j;
+    const int oct = (r.y >> 28) & 7;
+    C.beg[id] = r.x;
+    C.cnt[id] = r.y & 0x0fffffff;
+    C.parent[id] = c;
+    C.child0[id] = -1;
+    C.nchild[id] = 0;
+    const uint64_t cp = pp * 8 + (uint64_t)oct;
+    prefix[id] = cp;
+    cell_geometry(cp, level + 1, root, &C.grid[id], &C.geo[id]);
+  }
+}
+
+__global__ void k_level_total(const int *nch, const int *excl, int nl, int *out) {
+  *out = nl ? excl[nl - 1] + nch[nl - 1] : 0;
+}
+
+// Leaves (nchild == 0) in cell order.
+__global__ void __launch_bounds__(256) k_leaf_flags(int ncells, const int *__restrict__ nchild,
+                                                    int *__restrict__ flag) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncells) flag[c] = nchild[c] == 0;
+}
+__global__ void __launch_bounds__(256) k_leaf_scatter(int ncells, const int *__restrict__ flag,
+                                                      const int *__restrict__ excl,
+                                                      int *__restrict__ leaves) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncells && flag[c]) leaves[excl[c]] = c;
+}
+
+// ---- host launchers --------------------------------------------------------------------------
+static int grid_for(int64_t n, int bs) {
+  int64_t g = (n + bs - 1) / bs;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)(g < 1 ? 1 : g);
+}
+
+void launch_bbox(const float *xyz, const float *q, int64_t n, unsigned *mm, RootInfo *root,
+                 cudaStream_t st) {
+  k_bbox_init<<<1, 32, 0, st>>>(mm, root);
+  k_bbox<<<grid_for(n, 256), 256, 0, st>>>(xyz, q, n, mm, root);
+  k_root<<<1, 1, 0, st>>>(mm, root);
+}
+void launch_keys(const float *xyz, int64_t n, const RootInfo *root, uint64_t *keys, unsigned *idx,
+                 cudaStream_t st) {
+  k_keys<<<grid_for(n, 256), 256, 0, st>>>(xyz, n, root, keys, idx);
+}
+void launch_gather(const float *xyz, const float *q, const unsigned *perm, int64_t n, float4 *pos,
+                   cudaStream_t st) {
+  k_gather<<<grid_for(n, 256), 256, 0, st>>>(xyz, q, perm, n, pos);
+}
+cudaError_t sort_keys(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
+                      const unsigned *vin, unsigned *vout, int64_t n, cudaStream_t st) {
+  return cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int)n, 0, 63, st);
+}
+cudaError_t exclusive_scan(void *tmp, size_t &tmp_bytes, const int *in, int *out, int n,
+                           cudaStream_t st) {
+  return cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n, st);
+}
+void launch_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64_t *prefix,
+                      cudaStream_t st) {
+  k_root_cell<<<1, 1, 0, st>>>(n, root, C, prefix);
+}
+void launch_split(int c0, int nl, int level, int ncrit, const uint64_t *keys, CellsView C,
+                  const uint64_t *prefix, int *nch, int2 *crange, cudaStream_t st) {
+  k_split<<<(nl + 255) / 256, 256, 0, st>>>(c0, nl, level, ncrit, keys, C, prefix, nch, crange);
+}
+void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int *excl,
+                 const int2 *crange, const RootInfo *root, CellsView C, uint64_t *prefix,
+                 cudaStream_t st) {
+  k_emit<<<(nl + 255) / 256, 256, 0, st>>>(c0, nl, next0, level, nch, excl, crange, root, C,
+                                            prefix);
+}
+void launch_level_total(const int *nch, const int *excl, int nl, int *total, cudaStream_t st) {
+  k_level_total<<<1, 1, 0, st>>>(nch, excl, nl, total);
+}
+void launch_leaf_flags(int ncells, const int *nchild, int *flag, cudaStream_t st) {
+  k_leaf_flags<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, nchild, flag);
+}
+void launch_leaf_scatter(int ncells, const int *flag, const int *excl, int *leaves,
+                         cudaStream_t st) {
+  k_leaf_scatter<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, flag, excl, leaves);
+}

@@ -1,0 +1,208 @@
+"""ctypes binding of libfmm.so (include/fmm.h). Argument marshalling only: every step of the
+method runs in the CUDA kernels behind the C ABI. Torch is used for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+HYBRID, FMM_MODE, TREECODE, DIRECT = 0, 1, 2, 3
+MODES = {"hybrid": HYBRID, "fmm": FMM_MODE, "treecode": TREECODE, "direct": DIRECT}
+SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_host", "fmm_set_stream",
+           "fmm_set_mode", "fmm_set_timing", "fmm_tune", "fmm_get_cost_model",
+           "fmm_set_cost_model", "fmm_get_stats", "fmm_export_tree", "fmm_export_lists",
+           "fmm_export_perm", "fmm_strerror", "fmm_last_error"]
+
+
+class FmmError(RuntimeError):
+    pass
+
+
+class CostModel(C.Structure):
+    _fields_ = [("t_pp", C.c_double), ("t_mp", C.c_double), ("t_ml", C.c_double),
+                ("p", C.c_int), ("measured", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("n", C.c_int64), ("ncells", C.c_int64), ("nleaves", C.c_int64),
+                ("depth", C.c_int32), ("p", C.c_int32),
+                ("n_m2l", C.c_int64), ("n_m2p", C.c_int64), ("n_p2p", C.c_int64),
+                ("p2p_pairs", C.c_int64), ("m2p_evals", C.c_int64), ("traversal_pairs", C.c_int64),
+                ("ms_total", C.c_double), ("ms_tree", C.c_double), ("ms_upward", C.c_double),
+                ("ms_traverse", C.c_double), ("ms_m2l", C.c_double), ("ms_p2p", C.c_double),
+                ("ms_m2p", C.c_double), ("ms_downward", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def lib_path() -> str:
+    return os.environ.get("FMM_LIB", os.path.join(HERE, "libfmm.so"))
+
+
+_lib = None
+
+
+def load_library():
+    """Load libfmm.so; raises (no fallback) when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not os.path.exists(path):
+        raise FmmError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    vp, i64, dp = C.c_void_p, C.c_int64, C.c_double
+    P = C.POINTER
+    L.fmm_create.argtypes = [P(vp), C.c_int, dp, C.c_int]
+    L.fmm_destroy.argtypes = [vp]
+    L.fmm_evaluate.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.fmm_evaluate_host.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.fmm_set_stream.argtypes = [vp, vp]
+    L.fmm_set_mode.argtypes = [vp, C.c_int]
+    L.fmm_set_timing.argtypes = [vp, C.c_int]
+    L.fmm_tune.argtypes = [vp]
+    L.fmm_get_cost_model.argtypes = [vp, P(CostModel)]
+    L.fmm_set_cost_model.argtypes = [vp, P(CostModel)]
+    L.fmm_get_stats.argtypes = [vp, P(Stats)]
+    L.fmm_export_tree.argtypes = [vp, i64, vp, vp, vp, vp, P(i64)]
+    L.fmm_export_lists.argtypes = [vp, i64, vp, vp, vp, vp, vp, P(i64)]
+    L.fmm_export_perm.argtypes = [vp, i64, vp, vp, vp, vp]
+    L.fmm_strerror.argtypes = [C.c_int]
+    L.fmm_strerror.restype = C.c_char_p
+    L.fmm_last_error.argtypes = [vp]
+    L.fmm_last_error.restype = C.c_char_p
+    for s in SYMBOLS:
+        if s not in ("fmm_strerror", "fmm_last_error"):
+            getattr(L, s).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _ptr(a) -> int:
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+class FMM:
+    """Handle on the current CUDA device: FMM(p, theta, ncrit, mode='hybrid')."""
+
+    def __init__(self, p: int = 10, theta: float = 0.4, ncrit: int = 64, mode: str = "hybrid",
+                 tune: bool = True):
+        self.L = load_library()
+        self.p, self.theta, self.ncrit = p, theta, ncrit
+        h = C.c_void_p()
+        if not tune:
+            os.environ["FMM_NO_TUNE"] = "1"
+        try:
+            rc = self.L.fmm_create(C.byref(h), int(p), float(theta), int(ncrit))
+        finally:
+            if not tune:
+                os.environ.pop("FMM_NO_TUNE", None)
+        if rc != 0:
+            raise FmmError(f"fmm_create: {self.L.fmm_strerror(rc).decode()}")
+        self.h = h
+        self.set_mode(mode)
+
+    def _check(self, rc, what):
+        if rc != 0:
+            msg = self.L.fmm_last_error(self.h).decode()
+            raise FmmError(f"{what}: {self.L.fmm_strerror(rc).decode()} ({msg})")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.fmm_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def set_mode(self, mode):
+        m = MODES[mode] if isinstance(mode, str) else int(mode)
+        self._check(self.L.fmm_set_mode(self.h, m), "fmm_set_mode")
+
+    def set_timing(self, on: bool):
+        self._check(self.L.fmm_set_timing(self.h, int(bool(on))), "fmm_set_timing")
+
+    def set_stream(self, stream):
+        self._check(self.L.fmm_set_stream(self.h, C.c_void_p(stream)), "fmm_set_stream")
+
+    def tune(self):
+        self._check(self.L.fmm_tune(self.h), "fmm_tune")
+
+    def cost_model(self):
+        c = CostModel()
+        self._check(self.L.fmm_get_cost_model(self.h, C.byref(c)), "fmm_get_cost_model")
+        return (c.t_pp, c.t_mp, c.t_ml)
+
+    def set_cost_model(self, t_pp, t_mp, t_ml):
+        c = CostModel(float(t_pp), float(t_mp), float(t_ml), int(self.p), 0)
+        self._check(self.L.fmm_set_cost_model(self.h, C.byref(c)), "fmm_set_cost_model")
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(self.L.fmm_get_stats(self.h, C.byref(s)), "fmm_get_stats")
+        return s.as_dict()
+
+    def evaluate(self, xyz, q, phi=None, grad=None):
+        """xyz: CUDA float32 [N,3] contiguous, q: CUDA float32 [N]. Returns (phi [N], grad [N,3])."""
+        import torch
+
+        assert xyz.is_cuda and xyz.dtype == torch.float32 and xyz.is_contiguous()
+        assert q.is_cuda and q.dtype == torch.float32 and q.is_contiguous()
+        n = q.numel()
+        if phi is None:
+            phi = torch.empty(n, dtype=torch.float32, device=xyz.device)
+        if grad is None:
+            grad = torch.empty((n, 3), dtype=torch.float32, device=xyz.device)
+        self._check(self.L.fmm_set_stream(self.h, C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                    "fmm_set_stream")
+        self._check(self.L.fmm_evaluate(self.h, xyz.data_ptr(), q.data_ptr(), n, phi.data_ptr(),
+                                        grad.data_ptr()), "fmm_evaluate")
+        return phi, grad
+
+    def evaluate_host(self, xyz: np.ndarray, q: np.ndarray, phi=None, grad=None):
+        """Host (numpy, ideally pinned) buffers: H2D + evaluate + D2H inside the C ABI call."""
+        xyz = np.ascontiguousarray(xyz, np.float32)
+        q = np.ascontiguousarray(q, np.float32)
+        n = len(q)
+        phi = np.empty(n, np.float32) if phi is None else phi
+        grad = np.empty((n, 3), np.float32) if grad is None else grad
+        self._check(self.L.fmm_evaluate_host(self.h, _ptr(xyz), _ptr(q), n, _ptr(phi), _ptr(grad)),
+                    "fmm_evaluate_host")
+        return phi, grad
+
+    def export_tree(self) -> dict:
+        cnt = C.c_int64()
+        self.L.fmm_export_tree(self.h, 0, None, None, None, None, C.byref(cnt))
+        n = cnt.value
+        t = dict(level=np.zeros(n, np.int32), prefix=np.zeros(n, np.uint64),
+                 begin=np.zeros(n, np.int64), count=np.zeros(n, np.int64))
+        self._check(self.L.fmm_export_tree(self.h, n, _ptr(t["level"]), _ptr(t["prefix"]),
+                                           _ptr(t["begin"]), _ptr(t["count"]), C.byref(cnt)),
+                    "fmm_export_tree")
+        return t
+
+    def export_lists(self) -> dict:
+        cnt = C.c_int64()
+        self.L.fmm_export_lists(self.h, 0, None, None, None, None, None, C.byref(cnt))
+        n = cnt.value
+        t = dict(kind=np.zeros(n, np.int32), tlevel=np.zeros(n, np.int32),
+                 tprefix=np.zeros(n, np.uint64), slevel=np.zeros(n, np.int32),
+                 sprefix=np.zeros(n, np.uint64))
+        self._check(self.L.fmm_export_lists(self.h, n, _ptr(t["kind"]), _ptr(t["tlevel"]),
+                                            _ptr(t["tprefix"]), _ptr(t["slevel"]),
+                                            _ptr(t["sprefix"]), C.byref(cnt)), "fmm_export_lists")
+        return t
+
+    def export_perm(self, n: int):
+        perm = np.zeros(n, np.int64)
+        keys = np.zeros(n, np.uint64)
+        origin = np.zeros(3)
+        Lside = np.zeros(1)
+        self._check(self.L.fmm_export_perm(self.h, n, _ptr(perm), _ptr(keys), _ptr(origin),
+                                           _ptr(Lside)), "fmm_export_perm")
+        return perm, keys, origin, float(Lside[0])

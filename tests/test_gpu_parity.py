@@ -1,0 +1,147 @@
+"""GPU parity: the CUDA path through the C ABI against the FP64 oracle (tests/ only).
+
+Bars (BASELINE.json north_star): keys, tree and interaction lists bit-exact; phi and grad within
+relative L2 1e-5 of the oracle running the same tree/lists/cost model; FMM within 1e-4 of the direct
+sum at p = 10.
+"""
+import numpy as np
+import pytest
+
+from fmm_inputs import make_particles
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1108_5815_b200 import FMM, FmmError  # noqa: E402
+
+COST = (2e-12, 6e-11, 2.5e-9)  # a fixed cost model -> reproducible hybrid lists on both sides
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run(f, xyz, q):
+    phi, grad = f.evaluate(dev(xyz), dev(q))
+    torch.cuda.synchronize()
+    return phi.cpu().numpy().astype(np.float64), grad.cpu().numpy().astype(np.float64)
+
+
+@pytest.fixture(scope="module")
+def handles():
+    cache = {}
+
+    def get(p, theta, ncrit, mode="fmm"):
+        key = (p, theta, ncrit)
+        if key not in cache:
+            cache[key] = FMM(p=p, theta=theta, ncrit=ncrit, tune=False)
+        f = cache[key]
+        f.set_mode(mode)
+        f.set_cost_model(*COST)
+        return f
+
+    yield get
+    for f in cache.values():
+        f.close()
+
+
+CASES = [("uniform", 1000, 4, 0.5, 16, 1), ("uniform", 20000, 6, 0.5, 32, 2),
+         ("plummer", 20000, 6, 0.4, 32, 3), ("shell", 8000, 5, 0.5, 20, 4),
+         ("mixed", 5000, 8, 0.45, 8, 5), ("uniform", 3000, 10, 0.4, 64, 6)]
+
+
+@pytest.mark.parametrize("dist,n,p,theta,ncrit,seed", CASES)
+def test_keys_tree_bitexact(O, handles, dist, n, p, theta, ncrit, seed):
+    xyz, q = make_particles(n, dist, seed)
+    f = handles(p, theta, ncrit, "fmm")
+    run(f, xyz, q)
+    ref = O.fmm(xyz, q, p, theta, ncrit, O.FMM)
+    perm, keys, origin, L = f.export_perm(n)
+    assert L == ref.L and np.array_equal(origin, ref.origin)
+    assert np.array_equal(keys, ref.sorted_keys)
+    assert np.array_equal(perm, ref.perm)
+    t = f.export_tree()
+    for k in ("level", "prefix", "begin", "count"):
+        assert np.array_equal(t[k], ref.tree[k]), k
+
+
+@pytest.mark.parametrize("mode", ["fmm", "treecode", "hybrid"])
+@pytest.mark.parametrize("dist,n,p,theta,ncrit,seed", CASES)
+def test_lists_bitexact_and_fields(O, handles, mode, dist, n, p, theta, ncrit, seed):
+    xyz, q = make_particles(n, dist, seed)
+    f = handles(p, theta, ncrit, mode)
+    phi, grad = run(f, xyz, q)
+    omode = {"fmm": O.FMM, "treecode": O.TREECODE, "hybrid": O.HYBRID}[mode]
+    ref = O.fmm(xyz, q, p, theta, ncrit, omode, cost=COST)
+    a = O.canonical_tasks(f.export_lists())
+    b = O.canonical_tasks(ref.tasks)
+    assert len(a) == len(b) and np.array_equal(a, b)
+    s = f.stats()
+    assert s["n_m2l"] == np.sum(b["kind"] == 0) and s["n_p2p"] == np.sum(b["kind"] == 2)
+    ep, eg = O.rel_l2(phi, ref.phi), O.rel_l2(grad, ref.grad)
+    assert ep < 1e-5 and eg < 1e-5, (ep, eg)
+
+
+def test_direct_mode(O, handles):
+    xyz, q = make_particles(20000, "plummer", 7)
+    f = handles(4, 0.5, 16, "direct")
+    phi, grad = run(f, xyz, q)
+    d = O.direct(xyz, q)
+    assert O.rel_l2(phi, d[0]) < 1e-6 and O.rel_l2(grad, d[1]) < 1e-6
+
+
+@pytest.mark.parametrize("dist", ["uniform", "plummer"])
+def test_p10_four_digits_vs_direct(O, handles, dist):
+    xyz, q = make_particles(30000, dist, 8)
+    f = handles(10, 0.4, 64, "hybrid")
+    phi, grad = run(f, xyz, q)
+    d = O.direct(xyz, q)
+    assert O.rel_l2(phi, d[0]) < 1e-4
+    assert O.rel_l2(grad, d[1]) < 1e-3
+
+
+def test_deterministic(handles):
+    xyz, q = make_particles(50000, "plummer", 9)
+    f = handles(8, 0.5, 32, "hybrid")
+    a = run(f, xyz, q)
+    b = run(f, xyz, q)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_edge_cases(O, handles):
+    f = handles(4, 0.5, 8, "fmm")
+    # n = 0: no-op
+    z = torch.zeros((0, 3), device="cuda")
+    phi, grad = f.evaluate(z, torch.zeros(0, device="cuda"))
+    assert phi.numel() == 0
+    # one particle
+    phi, grad = run(f, np.array([[0.1, 0.2, 0.3]], np.float32), np.ones(1, np.float32))
+    assert phi[0] == 0 and np.all(grad == 0)
+    # ragged: counts that are not multiples of the warp, all particles coincident in one place
+    xyz = np.concatenate([np.full((37, 3), 0.25, np.float32), make_particles(29, "uniform", 3)[0]])
+    q = np.ones(len(xyz), np.float32)
+    phi, grad = run(f, xyz, q)
+    ref = O.fmm(xyz, q, 4, 0.5, 8, O.FMM)
+    assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
+    t = f.export_tree()
+    assert t["level"].max() == 21
+    # non-finite input -> error, outputs untouched
+    xyz = make_particles(100, "uniform", 1)[0]
+    xyz[5, 2] = np.inf
+    with pytest.raises(FmmError, match="non-finite"):
+        f.evaluate(dev(xyz), dev(np.ones(100, np.float32)))
+    # host pointers -> FMM_E_NOT_DEVICE
+    x_h = torch.zeros((10, 3))
+    rc = f.L.fmm_evaluate(f.h, x_h.data_ptr(), x_h.data_ptr(), 10, x_h.data_ptr(), x_h.data_ptr())
+    assert rc == -2
+
+
+def test_host_entry_point(O, handles):
+    xyz, q = make_particles(5000, "uniform", 11)
+    f = handles(6, 0.5, 24, "hybrid")
+    phi, grad = f.evaluate_host(xyz, q)
+    ref = O.fmm(xyz, q, 6, 0.5, 24, O.HYBRID, cost=COST)
+    assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
