@@ -76,6 +76,8 @@ typedef struct {
   int64_t p2p_pairs, m2p_evals;     /* particle pairs in P2P; target-particle x source-cell in M2P */
   int64_t traversal_pairs;          /* MAC tests performed */
   double ms_total, ms_tree, ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_m2p, ms_downward;
+  int64_t launches;                 /* libfmm kernels launched by the evaluation (CUB's excluded) */
+  int64_t cub_calls;                /* CUB radix-sort / scan calls (library kernels) */
 } fmm_stats_t;
 
 /* Create a handle on the current CUDA device. p = expansion order (coefficients n = 0..p,

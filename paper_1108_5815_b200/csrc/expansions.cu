@@ -18,10 +18,10 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
-__constant__ short2 c_nm[nc_of(FMM_PMAX)];  // coefficient index -> (n, m)
+__constant__ short2 c_nm[nc_of(FMM_PMAX)];  // coefficient index -> (n, m) (also used by m2l.cu)
 
 static bool g_nm_ready = false;
-static void ensure_nm_table() {
+void ensure_nm_table() {
   if (g_nm_ready) return;
   short2 h[nc_of(FMM_PMAX)];
   for (int n = 0; n <= FMM_PMAX; ++n)
@@ -194,138 +194,6 @@ __global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
       L[(size_t)Cc * NC + o] = make_float2(old.x + sc * a.x, old.y + sc * a.y);
     }
     __syncwarp();
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// M2L: one CTA (4 warps) per target cell; each warp takes every 4th source of the target's list.
-// Per source the warp builds, in shared memory, the signed-order table I_a^b(u), a <= 2p, and the
-// signed, rho^n-scaled multipole stored as (a, a, b, b) so that each complex multiply-add is two
-// packed FFMA2. Each lane owns "tiles" of up to 3 consecutive orders k of one degree j; the
-// per-source partial is added to the running sum (tile-blocked accumulation).
-#define M2L_WARPS 4
-__global__ void __launch_bounds__(128) k_m2l(int p, int ncells, CellsView C, ListsView Ls,
-                                             M2LTiles T, const float2 *__restrict__ M,
-                                             float2 *__restrict__ L) {
-  extern __shared__ float4 sh_m2l[];
-  const int NC = nc_of(p);
-  const int P2 = 2 * p;
-  const int nI = (P2 + 1) * (P2 + 1), nM = (p + 1) * (p + 1);
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float4 *Mx = sh_m2l + wib * (nM + (nI + 1) / 2);
-  float2 *Ix = reinterpret_cast<float2 *>(Mx + nM);
-  float2 *red = reinterpret_cast<float2 *>(sh_m2l + M2L_WARPS * (nM + (nI + 1) / 2));
-
-  for (int t = blockIdx.x; t < ncells; t += gridDim.x) {
-    const int off = Ls.off[0][t], cnt = Ls.cnt[0][t];
-    float2 acc[2][3];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) acc[a][b] = make_float2(0.f, 0.f);
-    if (cnt > 0) {
-      const int4 gt = C.grid[t];
-      const float rt_inv = 1.f / (float)(1 << (FMM_LEVELS - gt.w));
-      for (int e = wib; e < cnt; e += M2L_WARPS) {
-        const int s = Ls.src[0][off + e];
-        const int4 gs = C.grid[s];
-        const int dl = gt.w - gs.w;  // rho = 2^dl
-        float ux = (gt.x - gs.x) * rt_inv, uy = (gt.y - gs.y) * rt_inv, uz = (gt.z - gs.z) * rt_inv;
-        const bool vform = dl > 0;
-        if (vform) {
-          const float ir = ldexpf(1.f, -dl);
-          ux *= ir;
-          uy *= ir;
-          uz *= ir;
-        }
-        // signed multipole, (a, a, b, b), scaled by rho^n in the u-form
-        for (int o = lane; o < nM; o += WARP) {
-          const int n = (int)sqrtf((float)o + 0.5f);
-          const int m = o - n * n - n;
-          const float2 v = sget(M + (size_t)s * NC, n, m);
-          const float sc = vform ? 1.f : ldexpf(1.f, n * dl);
-          Mx[o] = make_float4(v.x * sc, v.x * sc, v.y * sc, v.y * sc);
-        }
-        // irregular harmonics I_a^b(u), a <= 2p, all signed b
-        {
-          const float r2 = ux * ux + uy * uy + uz * uz;
-          const float ir2 = 1.f / r2;
-          for (int mm = lane; mm <= P2; mm += WARP) {
-            float2 Imm = make_float2(rsqrtf(r2), 0.f);
-            for (int k = 1; k <= mm; ++k) Imm = cscale(cmul(Imm, make_float2(ux, uy)), -(2.f * k - 1.f) * ir2);
-            float2 I2 = make_float2(0.f, 0.f), I1 = Imm;
-            const float sg = (mm & 1) ? -1.f : 1.f;
-            for (int a = mm; a <= P2; ++a) {
-              float2 Ia;
-              if (a == mm) Ia = Imm;
-              else if (a == mm + 1) Ia = cscale(Imm, (2.f * mm + 1.f) * uz * ir2);
-              else {
-                const float c1 = (2.f * a - 1.f) * uz, c2 = (float)(a + mm - 1) * (float)(a - mm - 1);
-                Ia = make_float2((c1 * I1.x - c2 * I2.x) * ir2, (c1 * I1.y - c2 * I2.y) * ir2);
-              }
-              if (a > mm) {
-                I2 = I1;
-                I1 = Ia;
-              }
-              Ix[a * a + a + mm] = Ia;
-              Ix[a * a + a - mm] = make_float2(sg * Ia.x, -sg * Ia.y);
-            }
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int ti = 0; ti < 2; ++ti) {
-          const int tix = lane + ti * WARP;
-          if (tix >= T.ntiles) break;
-          const int tw = T.tile[tix];
-          const int j = tw & 255, k0 = (tw >> 8) & 255;
-          const int k1 = min(k0 + 1, j), k2 = min(k0 + 2, j);
-          float2 pa0 = make_float2(0.f, 0.f), pb0 = pa0, pa1 = pa0, pb1 = pa0, pa2 = pa0, pb2 = pa0;
-          for (int n = 0; n <= p; ++n) {
-            const float2 *Irow = Ix + (n + j) * (n + j) + (n + j);
-            const float4 *Mrow = Mx + n * n + n;
-            for (int m = -n; m <= n; ++m) {
-              const float4 mv = Mrow[m];
-              const float2 aa = make_float2(mv.x, mv.y), bb = make_float2(mv.z, mv.w);
-              const float2 i0 = Irow[m - k0], i1 = Irow[m - k1], i2 = Irow[m - k2];
-              pa0 = __ffma2_rn(aa, i0, pa0);
-              pb0 = __ffma2_rn(bb, i0, pb0);
-              pa1 = __ffma2_rn(aa, i1, pa1);
-              pb1 = __ffma2_rn(bb, i1, pb1);
-              pa2 = __ffma2_rn(aa, i2, pa2);
-              pb2 = __ffma2_rn(bb, i2, pb2);
-            }
-          }
-          // complex result (sum ac - bd, sum ad + bc); v-form output scale rho^-(j+1)
-          const float osc = vform ? ldexpf(1.f, -dl * (j + 1)) : 1.f;
-          acc[ti][0].x += osc * (pa0.x - pb0.y);
-          acc[ti][0].y += osc * (pa0.y + pb0.x);
-          acc[ti][1].x += osc * (pa1.x - pb1.y);
-          acc[ti][1].y += osc * (pa1.y + pb1.x);
-          acc[ti][2].x += osc * (pa2.x - pb2.y);
-          acc[ti][2].y += osc * (pa2.y + pb2.x);
-        }
-        __syncwarp();
-      }
-    }
-    // reduce the 4 warps' partial sums, apply (-1)^{j+k}, write Lhat_t (zero if no M2L)
-#pragma unroll
-    for (int ti = 0; ti < 2; ++ti) {
-      const int tix = lane + ti * WARP;
-      if (tix >= T.ntiles) break;
-      const int tw = T.tile[tix];
-      const int j = tw & 255, k0 = (tw >> 8) & 255, K = (tw >> 16) & 255;
-      for (int kk = 0; kk < K; ++kk) red[wib * NC + cidx(j, k0 + kk)] = acc[ti][kk];
-    }
-    __syncthreads();
-    for (int o = threadIdx.x; o < NC; o += blockDim.x) {
-      float2 s = red[o];
-      for (int w = 1; w < M2L_WARPS; ++w) s = cadd(s, red[w * NC + o]);
-      const int n = c_nm[o].x, m = c_nm[o].y;
-      const float sg = ((n + m) & 1) ? -1.f : 1.f;
-      L[(size_t)t * NC + o] = make_float2(sg * s.x, sg * s.y);
-    }
-    __syncthreads();
   }
 }
 
@@ -542,21 +410,6 @@ void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st) 
 void launch_l2l(int p, int c0, int nl, CellsView C, float2 *L, cudaStream_t st) {
   ensure_nm_table();
   k_l2l<<<warp_grid(nl, 4), 128, 4 * 2 * nc_of(p) * sizeof(float2), st>>>(p, c0, nl, C, L);
-}
-void launch_m2l(int p, int ncells, CellsView C, ListsView Ls, const M2LTiles &tiles,
-                const float2 *M, float2 *L, cudaStream_t st) {
-  ensure_nm_table();
-  const int nI = (2 * p + 1) * (2 * p + 1), nM = (p + 1) * (p + 1);
-  const size_t smem = (size_t)M2L_WARPS * (nM + (nI + 1) / 2) * sizeof(float4) +
-                      (size_t)M2L_WARPS * nc_of(p) * sizeof(float2);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = smem;
-  }
-  int blocks = ncells < 148 * 8 ? ncells : 148 * 8;
-  if (blocks < 1) blocks = 1;
-  k_m2l<<<blocks, 128, smem, st>>>(p, ncells, C, Ls, tiles, M, L);
 }
 void launch_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
                 const float4 *pos, const float2 *M, float4 *acc, cudaStream_t st) {

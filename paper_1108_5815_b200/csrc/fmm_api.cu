@@ -59,7 +59,7 @@ struct DBuf {
   }
 };
 
-enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_N };
+enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L_PREP, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_N };
 
 }  // namespace
 
@@ -98,6 +98,12 @@ struct fmm_ctx {
   int ncells = 0, nleaves = 0, depth = 0;
   // expansions
   DBuf<float2> M, L;
+  // M2L class batching
+  DBuf<int> m2l_pair_t, m2l_flag, m2l_cid, m2l_cstart, m2l_counters;
+  DBuf<unsigned long long> m2l_keys_in, m2l_keys;
+  DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small;
+  DBuf<int4> m2l_items;
+  DBuf<float> m2l_Y;
   // lists
   DBuf<int> loff[3], lcnt[3];
   DBuf<unsigned> lsrc[3];
@@ -153,6 +159,7 @@ static int fail(fmm_ctx *h, int code, const char *fmt, ...) {
 
 #define CKL()                                                                            \
   do {                                                                                   \
+    ++h->stats.launches;                                                                 \
     cudaError_t e_ = cudaGetLastError();                                                 \
     if (e_ != cudaSuccess)                                                               \
       return fail(h, FMM_E_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_),     \
@@ -178,6 +185,7 @@ static int check_device_ptr(fmm_ctx *h, const void *ptr, const char *name) {
 
 static int cub_scan(fmm_ctx *h, const int *in, int *out, int n) {
   size_t bytes = 0;
+  ++h->stats.cub_calls;
   CK(exclusive_scan(nullptr, bytes, in, out, n, h->stream));
   CK(h->cub_tmp.ensure(bytes));
   CK(exclusive_scan(h->cub_tmp.p, bytes, in, out, n, h->stream));
@@ -199,6 +207,7 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
   CK(sort_keys(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
   CK(h->cub_tmp.ensure(bytes));
   CK(sort_keys(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
+  ++h->stats.cub_calls;
   launch_gather(xyz, q, h->perm.p, n, h->pos.p, st);
   CKL();
 
@@ -374,11 +383,50 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   record(h, EV_UP);
   if (int rc = traverse(h)) return rc;
   record(h, EV_TRAV);
+  record(h, EV_M2L_PREP);  // re-recorded after the class sort when there are M2L pairs
   // a10 M2L (writes every cell's local expansion, zero where no M2L)
   const bool far_local = h->ntask[FMM_KIND_M2L] > 0;
   if (far_local) {
-    launch_m2l(p, h->ncells, h->cells(), h->lists(), h->tiles, h->M.p, h->L.p, st);
-    CKL();
+    const int np = (int)h->ntask[FMM_KIND_M2L];
+    CK(h->m2l_pair_t.ensure(np));
+    CK(h->m2l_keys_in.ensure(np));
+    CK(h->m2l_keys.ensure(np));
+    CK(h->m2l_idx_in.ensure(np));
+    CK(h->m2l_sidx.ensure(np));
+    CK(h->m2l_flag.ensure(np));
+    CK(h->m2l_cid.ensure(np));
+    CK(h->m2l_cstart.ensure((size_t)np + 1));
+    CK(h->m2l_counters.ensure(4));
+    CK(h->m2l_items.ensure((size_t)np + 1));
+    CK(h->m2l_small.ensure(np));
+    CK(h->m2l_Y.ensure((size_t)np * m2l_y_stride(p)));
+    CK(h->cub_tmp.ensure(m2l_temp_bytes(np)));
+    M2LWork W{};
+    W.C = h->cells();
+    W.off = h->loff[0].p;
+    W.cnt = h->lcnt[0].p;
+    W.src = h->lsrc[0].p;
+    W.pair_t = h->m2l_pair_t.p;
+    W.keys_in = h->m2l_keys_in.p;
+    W.keys = h->m2l_keys.p;
+    W.idx_in = h->m2l_idx_in.p;
+    W.sidx = h->m2l_sidx.p;
+    W.flag = h->m2l_flag.p;
+    W.cid = h->m2l_cid.p;
+    W.cstart = h->m2l_cstart.p;
+    W.counters = h->m2l_counters.p;
+    W.items = h->m2l_items.p;
+    W.small = h->m2l_small.p;
+    W.Y = h->m2l_Y.p;
+    W.tmp = h->cub_tmp.p;
+    W.tmp_bytes = h->cub_tmp.cap;
+    W.direct_all = m2l_gemm_supported(p) ? 0 : 1;
+    CK(m2l_prepare(W, np, h->ncells, st));
+    h->stats.launches += 6;
+    h->stats.cub_calls += 2;
+    record(h, EV_M2L_PREP);
+    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st));
+    h->stats.launches += 3;
   }
   record(h, EV_M2L);
   // a12 P2P (writes acc), a11 M2P (adds)
@@ -414,7 +462,8 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   if (n == 0) return FMM_OK;
   if (n > (int64_t)1 << 28) return fail(h, FMM_E_INVALID, "n = %lld exceeds 2^28 per device", (long long)n);
   record(h, EV_START);
-  launch_bbox(xyz, q, n, h->d_mm, h->d_root, st);
+  launch_bbox(xyz, q, n, h->d_mm, h->d_root, st);  // 3 kernels
+  h->stats.launches += 2;
   CKL();
   CK(cudaMemcpyAsync(&h->h_root, h->d_root, sizeof(RootInfo), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -427,6 +476,7 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     record(h, EV_TREE);
     record(h, EV_UP);
     record(h, EV_TRAV);
+    record(h, EV_M2L_PREP);
     record(h, EV_M2L);
     launch_p2p_direct(n, h->pos.p, phi, grad, st);
     CKL();
@@ -453,7 +503,7 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.ms_total = ms[0];
     h->stats.ms_tree = ms[EV_TREE];
     h->stats.ms_upward = ms[EV_UP];
-    h->stats.ms_traverse = ms[EV_TRAV];
+    h->stats.ms_traverse = ms[EV_TRAV] + ms[EV_M2L_PREP];  // class sort counted as bookkeeping
     h->stats.ms_m2l = ms[EV_M2L];
     h->stats.ms_p2p = ms[EV_P2P];
     h->stats.ms_m2p = ms[EV_M2P];
@@ -562,6 +612,10 @@ int fmm_destroy(fmm_t h) {
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release();
   h->nch.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
+  h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
+  h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
+  h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
+  h->m2l_Y.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();

@@ -56,8 +56,6 @@ struct M2LTiles {
 void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos, float2 *M,
                 cudaStream_t st);
 void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st);
-void launch_m2l(int p, int ncells, CellsView C, ListsView Ls, const M2LTiles &tiles,
-                const float2 *M, float2 *L, cudaStream_t st);
 void launch_l2l(int p, int c0, int nl, CellsView C, float2 *L, cudaStream_t st);
 void launch_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
                 const float4 *pos, const float2 *M, float4 *acc, cudaStream_t st);
@@ -65,6 +63,30 @@ void launch_l2p(int p, const int *leaves, int nleaves, CellsView C, const float4
                 const float2 *L, const float4 *acc, const unsigned *perm, float *phi, float *grad,
                 int use_local, cudaStream_t st);
 M2LTiles make_m2l_tiles(int p);
+
+// ---- m2l.cu ----
+struct M2LWork {
+  CellsView C;
+  const int *off, *cnt;     // per target cell: M2L list segment
+  const unsigned *src;      // source cell of each pair
+  int *pair_t;              // target cell of each pair
+  unsigned long long *keys_in, *keys;
+  unsigned *idx_in, *sidx;  // pair indices sorted by class key
+  int *flag, *cid, *cstart, *counters;
+  int4 *items;              // GEMM work items (first sorted position, count, representative pair)
+  unsigned *small;          // pairs on the direct path
+  float *Y;                 // per-pair results [npairs][m2l_y_stride(p)]
+  void *tmp;
+  size_t tmp_bytes;
+  int direct_all;           // 1: every pair on the direct path (p > 12)
+};
+size_t m2l_gemm_smem(int p);
+bool m2l_gemm_supported(int p);
+int m2l_y_stride(int p);
+size_t m2l_temp_bytes(int npairs);
+cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st);
+cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
+                        float2 *L, cudaStream_t st);
 
 // ---- p2p.cu ----
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,

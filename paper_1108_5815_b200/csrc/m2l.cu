@@ -1,0 +1,434 @@
+// m2l.cu — M2L ("O(p^4) cell-cell interaction kernel") as
+// class-batched dense products on the FP32 CUDA cores.
+//
+// The translation of one pair is the linear map  Lhat_j^k(t) += (-1)^{j+k} sum_{n,m} Mhat_n^m(s)
+// rho^n I_{n+j}^{m-k}(u),  u = (c_t - c_s)/r_t, rho = r_s/r_t  (expansions.cu header). It depends
+// on the pair only through (level difference, integer offset) — its "class". Written over the
+// real degrees of freedom of a real field (Re/Im of m >= 0 coefficients), it is a real matrix
+// T_class of size 2NC x 2NC. Pairs are sorted by class key, and one CTA per work item (class,
+// up to M2L_ITEM pairs) builds T_class in shared memory from the I table of the class and
+// multiplies it with the gathered multipoles of the item's sources, 64 pairs per chunk, in a
+// register-tiled FP32 product (packed FFMA2). Each pair's result goes to its own slot Y[pair];
+// k_m2l_reduce then sums every target's slots in list order, so the result is deterministic and
+// independent of how pairs were grouped. The arithmetic is the paper's translation operator
+// unchanged; only the evaluation order differs from the direct double loop.
+//
+// Rare classes (< M2L_SMALL pairs) and orders p > 12 (T too large for shared memory) use
+// k_m2l_pairs: one warp per pair evaluating the double loop directly.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+#define M2L_ITEM 512
+#define M2L_CHUNK 64
+#define M2L_SMALL 4
+
+// coefficient index c = n(n+1)/2 + m  ->  (n, m)
+__device__ __forceinline__ short2 nm_of(int c) {
+  int n = (int)((sqrtf(8.f * c + 1.f) - 1.f) * 0.5f);
+  while ((n + 1) * (n + 2) / 2 <= c) ++n;
+  while (n * (n + 1) / 2 > c) --n;
+  return make_short2((short)n, (short)(c - n * (n + 1) / 2));
+}
+
+__device__ __forceinline__ float2 cmul2(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// I_a^b(u) for a <= P2 and every signed b, into tab[a*a + a + b]; thread `col` owns column |b|.
+__device__ void irregular_table(float ux, float uy, float uz, int P2, float2 *tab, int col,
+                                int ncol_threads) {
+  const float r2 = ux * ux + uy * uy + uz * uz;
+  const float ir2 = 1.f / r2;
+  for (int mm = col; mm <= P2; mm += ncol_threads) {
+    float2 Imm = make_float2(rsqrtf(r2), 0.f);
+    for (int k = 1; k <= mm; ++k) {
+      const float2 t = cmul2(Imm, make_float2(ux, uy));
+      const float s = -(2.f * k - 1.f) * ir2;
+      Imm = make_float2(t.x * s, t.y * s);
+    }
+    float2 I2 = make_float2(0.f, 0.f), I1 = Imm;
+    const float sg = (mm & 1) ? -1.f : 1.f;
+    for (int a = mm; a <= P2; ++a) {
+      float2 Ia;
+      if (a == mm) Ia = Imm;
+      else if (a == mm + 1) {
+        const float s = (2.f * mm + 1.f) * uz * ir2;
+        Ia = make_float2(Imm.x * s, Imm.y * s);
+      } else {
+        const float c1 = (2.f * a - 1.f) * uz, c2 = (float)(a + mm - 1) * (float)(a - mm - 1);
+        Ia = make_float2((c1 * I1.x - c2 * I2.x) * ir2, (c1 * I1.y - c2 * I2.y) * ir2);
+      }
+      if (a > mm) {
+        I2 = I1;
+        I1 = Ia;
+      }
+      tab[a * a + a + mm] = Ia;
+      tab[a * a + a - mm] = make_float2(sg * Ia.x, -sg * Ia.y);
+    }
+  }
+}
+
+// Geometry of a pair: target-units offset (u-form when rho <= 1, v = u/rho when rho > 1).
+struct PairGeo {
+  float ux, uy, uz;
+  int dl;
+  bool vform;
+};
+__device__ __forceinline__ PairGeo pair_geo(int4 gt, int4 gs) {
+  PairGeo g;
+  const float rt_inv = 1.f / (float)(1 << (FMM_LEVELS - gt.w));
+  g.dl = gt.w - gs.w;  // rho = 2^dl
+  g.ux = (gt.x - gs.x) * rt_inv;
+  g.uy = (gt.y - gs.y) * rt_inv;
+  g.uz = (gt.z - gs.z) * rt_inv;
+  g.vform = g.dl > 0;
+  if (g.vform) {
+    const float ir = ldexpf(1.f, -g.dl);
+    g.ux *= ir;
+    g.uy *= ir;
+    g.uz *= ir;
+  }
+  return g;
+}
+
+// ---- pair bookkeeping -------------------------------------------------------------------------
+__global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
+                                   const int *__restrict__ cnt, int *__restrict__ pair_t) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < ncells; t += nw) {
+    const int o = off[t], c = cnt[t];
+    for (int e = lane; e < c; e += 32) pair_t[o + e] = t;
+  }
+}
+
+__global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
+                          const unsigned *__restrict__ src, CellsView C,
+                          unsigned long long *__restrict__ keys, unsigned *__restrict__ idx) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
+    const int4 gt = C.grid[pair_t[e]], gs = C.grid[src[e]];
+    const int dl = gt.w - gs.w;
+    const int sh = FMM_LEVELS - max(gt.w, gs.w);
+    const int dx = (gt.x - gs.x) >> sh, dy = (gt.y - gs.y) >> sh, dz = (gt.z - gs.z) >> sh;
+    const int lim = 1 << 18;
+    unsigned long long key;
+    if (abs(dx) < lim && abs(dy) < lim && abs(dz) < lim)
+      key = ((unsigned long long)(dl + 32) << 57) | ((unsigned long long)(dx + lim) << 38) |
+            ((unsigned long long)(dy + lim) << 19) | (unsigned long long)(dz + lim);
+    else
+      key = (1ull << 63) | (unsigned long long)e;  // out of key range: a class of its own
+    keys[e] = key;
+    idx[e] = (unsigned)e;
+  }
+}
+
+__global__ void k_m2l_class_flags(int npairs, const unsigned long long *__restrict__ skeys,
+                                  int *__restrict__ flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_m2l_class_start(int npairs, const int *__restrict__ flag,
+                                  const int *__restrict__ cid, int *__restrict__ cstart,
+                                  int *__restrict__ counters) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    if (flag[i]) cstart[cid[i]] = i;
+    if (i == npairs - 1) {
+      const int ncls = cid[i] + flag[i];
+      cstart[ncls] = npairs;
+      counters[0] = ncls;
+    }
+  }
+}
+
+// counters: [0] classes, [1] GEMM work items, [2] pairs on the direct path
+__global__ void k_m2l_items(int npairs, int direct_all, const int *__restrict__ flag,
+                            const int *__restrict__ cid, const int *__restrict__ cstart,
+                            const unsigned *__restrict__ sidx, int4 *__restrict__ items,
+                            unsigned *__restrict__ small, int *__restrict__ counters) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    if (!flag[i]) continue;
+    const int c = cid[i];
+    const int n = cstart[c + 1] - i;
+    if (!direct_all && n >= M2L_SMALL) {
+      const int ni = (n + M2L_ITEM - 1) / M2L_ITEM;
+      const int base = atomicAdd(&counters[1], ni);
+      for (int a = 0; a < ni; ++a)
+        items[base + a] = make_int4(i + a * M2L_ITEM, min(M2L_ITEM, n - a * M2L_ITEM), (int)sidx[i], 0);
+    } else {
+      const int base = atomicAdd(&counters[2], n);
+      for (int b = 0; b < n; ++b) small[base + b] = sidx[i + b];
+    }
+  }
+}
+
+// ---- class GEMM -------------------------------------------------------------------------------
+// Block = (Rpad/12) x 16 threads; thread (rg, cg) owns rows [12 rg, 12 rg + 12) x columns
+// [4 cg, 4 cg + 4) of the 2NC x 64 chunk product.
+__global__ void k_m2l_gemm(int p, const int4 *__restrict__ items, const int *__restrict__ counters,
+                           const unsigned *__restrict__ sidx, const int *__restrict__ pair_t,
+                           const unsigned *__restrict__ src, CellsView C,
+                           const float *__restrict__ M, float *__restrict__ Y) {
+  extern __shared__ float4 sh_gemm4[];
+  float *sh = reinterpret_cast<float *>(sh_gemm4);
+  const int NC = nc_of(p), KR = 2 * NC;
+  const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
+  float *Ts = sh;                       // [Kpad][Rpad]
+  const int XSK = Kpad + 1;             // odd row stride of Xs
+  float *Xs = sh + Kpad * Rpad;         // [M2L_CHUNK][XSK]
+  float2 *Itab = reinterpret_cast<float2 *>(Xs);  // aliased during the T build
+  int *colsrc = reinterpret_cast<int *>(Xs + M2L_CHUNK * XSK);  // [M2L_CHUNK] source cells
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int rg = tid / 16, cg = tid % 16;
+  const int nitems = counters[1];
+
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int4 item = items[it];
+    const int pos0 = item.x, cnt = item.y, rep = item.z;
+    const PairGeo g = pair_geo(C.grid[pair_t[rep]], C.grid[src[rep]]);
+    __syncthreads();  // previous item's readers of Xs are done
+    irregular_table(g.ux, g.uy, g.uz, 2 * p, Itab, tid, nthr);
+    __syncthreads();
+    // T[kcol][row]: row = output real index (2 c_out + re/im), kcol = input real index
+    for (int id = tid; id < Kpad * Rpad; id += nthr) {
+      const int kcol = id / Rpad, row = id - kcol * Rpad;
+      float v = 0.f;
+      if (row < KR && kcol < KR) {
+        const short2 jo = nm_of(row >> 1), ni = nm_of(kcol >> 1);
+        const int j = jo.x, k = jo.y, n = ni.x, m = ni.y;
+        const int rim = row & 1, cim = kcol & 1;
+        if (!(k == 0 && rim) && !(m == 0 && cim)) {
+          const float sgn = ((j + k) & 1) ? -1.f : 1.f;
+          const float sc = sgn * (g.vform ? ldexpf(1.f, -g.dl * (j + 1)) : ldexpf(1.f, n * g.dl));
+          const int a = n + j;
+          const float2 Cp = Itab[a * a + a + (m - k)];
+          if (m == 0) {
+            v = sc * (rim ? Cp.y : Cp.x);
+          } else {
+            const float2 Cm = Itab[a * a + a + (-m - k)];
+            const float sm = (m & 1) ? -1.f : 1.f;
+            if (!cim) {  // coefficient of Re M: A = Cp + (-1)^m Cm
+              v = sc * (rim ? (Cp.y + sm * Cm.y) : (Cp.x + sm * Cm.x));
+            } else {     // coefficient of Im M: i (Cp - (-1)^m Cm)
+              v = sc * (rim ? (Cp.x - sm * Cm.x) : -(Cp.y - sm * Cm.y));
+            }
+          }
+        }
+      }
+      Ts[kcol * Rpad + row] = v;
+    }
+    for (int c0 = 0; c0 < cnt; c0 += M2L_CHUNK) {
+      const int ncol = min(M2L_CHUNK, cnt - c0);
+      __syncthreads();  // T ready / previous chunk consumed
+      // gather the multipoles of the chunk's sources: Xs[col][k], odd row stride (bank-free)
+      for (int c = tid; c < M2L_CHUNK; c += nthr) colsrc[c] = c < ncol ? (int)src[sidx[pos0 + c0 + c]] : -1;
+      __syncthreads();
+      for (int id = tid; id < (Kpad / 4) * M2L_CHUNK; id += nthr) {
+        const int q = id / M2L_CHUNK, col = id - q * M2L_CHUNK;
+        const int s = colsrc[col];
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s >= 0) {
+          const float *Mr = M + (size_t)s * KR + 4 * q;
+          if (4 * q + 3 < KR) {
+            if ((KR & 3) == 0) v = *reinterpret_cast<const float4 *>(Mr);  // 16-byte aligned rows
+            else {
+              const float2 a = *reinterpret_cast<const float2 *>(Mr);
+              const float2 b = *reinterpret_cast<const float2 *>(Mr + 2);
+              v = make_float4(a.x, a.y, b.x, b.y);
+            }
+          } else {
+            if (4 * q + 0 < KR) v.x = Mr[0];
+            if (4 * q + 1 < KR) v.y = Mr[1];
+            if (4 * q + 2 < KR) v.z = Mr[2];
+          }
+        }
+        float *xd = Xs + col * XSK + 4 * q;
+        xd[0] = v.x;
+        xd[1] = v.y;
+        xd[2] = v.z;
+        xd[3] = v.w;
+      }
+      __syncthreads();
+      if (rg * 12 < Rpad) {
+        float2 acc[6][4];
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = make_float2(0.f, 0.f);
+        const float *Tp = Ts + rg * 12;
+        const float *Xp = Xs + cg * XSK;  // columns cg, cg + 16, cg + 32, cg + 48
+#pragma unroll 2
+        for (int k = 0; k < Kpad; ++k) {
+          const float4 t0 = *reinterpret_cast<const float4 *>(Tp + k * Rpad);
+          const float4 t1 = *reinterpret_cast<const float4 *>(Tp + k * Rpad + 4);
+          const float4 t2 = *reinterpret_cast<const float4 *>(Tp + k * Rpad + 8);
+          const float x0 = Xp[k], x1 = Xp[16 * XSK + k], x2 = Xp[32 * XSK + k], x3 = Xp[48 * XSK + k];
+          const float2 tr[6] = {make_float2(t0.x, t0.y), make_float2(t0.z, t0.w),
+                                make_float2(t1.x, t1.y), make_float2(t1.z, t1.w),
+                                make_float2(t2.x, t2.y), make_float2(t2.z, t2.w)};
+          const float2 xc[4] = {make_float2(x0, x0), make_float2(x1, x1), make_float2(x2, x2),
+                                make_float2(x3, x3)};
+#pragma unroll
+          for (int a = 0; a < 6; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = __ffma2_rn(tr[a], xc[b], acc[a][b]);
+        }
+        const int YS = Kpad;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int col = cg + 16 * b;
+          if (col >= ncol) continue;
+          float *yr = Y + (size_t)sidx[pos0 + c0 + col] * YS + rg * 12;
+#pragma unroll
+          for (int a = 0; a < 6; ++a) {
+            const int r = rg * 12 + 2 * a;
+            if (r + 1 < KR) *reinterpret_cast<float2 *>(yr + 2 * a) = acc[a][b];
+            else if (r < KR) yr[2 * a] = acc[a][b].x;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---- direct per-pair path (rare classes, p > 12) -------------------------------------------------
+__global__ void __launch_bounds__(128) k_m2l_pairs(int p, const unsigned *__restrict__ list,
+                                                   const int *__restrict__ counters,
+                                                   const int *__restrict__ pair_t,
+                                                   const unsigned *__restrict__ src, CellsView C,
+                                                   const float2 *__restrict__ M,
+                                                   float *__restrict__ Y) {
+  extern __shared__ float2 sh_pairs[];
+  const int NC = nc_of(p), KR = 2 * NC, YS = (KR + 3) & ~3;
+  const int P2 = 2 * p, nI = (P2 + 1) * (P2 + 1), nM = (p + 1) * (p + 1);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float2 *Mx = sh_pairs + wib * (nM + nI);
+  float2 *Ix = Mx + nM;
+  const int npairs = counters[2];
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int q = gw; q < npairs; q += nw) {
+    const int e = list[q];
+    const int s = src[e];
+    const PairGeo g = pair_geo(C.grid[pair_t[e]], C.grid[s]);
+    __syncwarp();
+    for (int o = lane; o < nM; o += 32) {
+      const int n = (int)sqrtf((float)o + 0.5f);
+      const int m = o - n * n - n;
+      const float2 v = sget(M + (size_t)s * NC, n, m);
+      const float sc = g.vform ? 1.f : ldexpf(1.f, n * g.dl);
+      Mx[o] = make_float2(v.x * sc, v.y * sc);
+    }
+    irregular_table(g.ux, g.uy, g.uz, P2, Ix, lane, 32);
+    __syncwarp();
+    for (int o = lane; o < NC; o += 32) {
+      const short2 jk = nm_of(o);
+      const int j = jk.x, k = jk.y;
+      float re = 0.f, im = 0.f;
+      for (int n = 0; n <= p; ++n) {
+        const float2 *Irow = Ix + (n + j) * (n + j) + (n + j);
+        const float2 *Mrow = Mx + n * n + n;
+        for (int m = -n; m <= n; ++m) {
+          const float2 a = Mrow[m], b = Irow[m - k];
+          re += a.x * b.x - a.y * b.y;
+          im += a.x * b.y + a.y * b.x;
+        }
+      }
+      const float sgn = ((j + k) & 1) ? -1.f : 1.f;
+      const float sc = sgn * (g.vform ? ldexpf(1.f, -g.dl * (j + 1)) : 1.f);
+      Y[(size_t)e * YS + 2 * o] = sc * re;
+      Y[(size_t)e * YS + 2 * o + 1] = (k == 0) ? 0.f : sc * im;
+    }
+  }
+}
+
+// ---- per-target sum of the pair slots, in list order -------------------------------------------
+__global__ void __launch_bounds__(128) k_m2l_reduce(int p, int ncells, const int *__restrict__ off,
+                                                    const int *__restrict__ cnt,
+                                                    const float *__restrict__ Y,
+                                                    float *__restrict__ L) {
+  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3;
+  for (int t = blockIdx.x; t < ncells; t += gridDim.x) {
+    const int o = off[t], c = cnt[t];
+    for (int r = threadIdx.x; r < KR; r += blockDim.x) {
+      float s = 0.f;
+      for (int e = 0; e < c; ++e) s += Y[(size_t)(o + e) * YS + r];
+      L[(size_t)t * KR + r] = s;
+    }
+  }
+}
+
+// ---- host orchestration -----------------------------------------------------------------------
+size_t m2l_gemm_smem(int p) {
+  const int KR = 2 * nc_of(p);
+  const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
+  return (size_t)(Kpad * Rpad + M2L_CHUNK * (Kpad + 1) + M2L_CHUNK) * sizeof(float);
+}
+bool m2l_gemm_supported(int p) { return m2l_gemm_smem(p) <= 227 * 1024; }
+int m2l_y_stride(int p) { return (2 * nc_of(p) + 3) & ~3; }
+
+cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st) {
+  k_m2l_pair_targets<<<148 * 8, 128, 0, st>>>(ncells, W.off, W.cnt, W.pair_t);
+  const int b = (npairs + 255) / 256 < 148 * 16 ? (npairs + 255) / 256 : 148 * 16;
+  k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.keys_in, W.idx_in);
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, W.idx_in,
+                                                  W.sidx, npairs, 0, 64, st);
+  if (e) return e;
+  if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
+  e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
+                                      64, st);
+  if (e) return e;
+  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.flag);
+  bytes = 0;
+  e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, W.flag, W.cid, npairs, st);
+  if (e) return e;
+  if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
+  e = cub::DeviceScan::ExclusiveSum(W.tmp, bytes, W.flag, W.cid, npairs, st);
+  if (e) return e;
+  cudaMemsetAsync(W.counters, 0, 4 * sizeof(int), st);
+  k_m2l_class_start<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.flag, W.cid, W.cstart, W.counters);
+  k_m2l_items<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.direct_all, W.flag, W.cid, W.cstart, W.sidx,
+                                             W.items, W.small, W.counters);
+  return cudaGetLastError();
+}
+
+size_t m2l_temp_bytes(int npairs) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long *)nullptr,
+                                  (unsigned long long *)nullptr, (unsigned *)nullptr,
+                                  (unsigned *)nullptr, npairs, 0, 64);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, npairs);
+  return a > b ? a : b;
+}
+
+cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
+                        float2 *L, cudaStream_t st) {
+  if (!W.direct_all) {
+    const size_t smem = m2l_gemm_smem(p);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(k_m2l_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured = smem;
+    }
+    const int KR = 2 * nc_of(p);
+    const int nthr = ((KR + 11) / 12) * 16;
+    const int per_sm = (int)((227 * 1024) / smem) < 2 ? 1 : 2;
+    k_m2l_gemm<<<148 * per_sm, nthr, smem, st>>>(p, W.items, W.counters, W.sidx, W.pair_t, W.src,
+                                                  W.C, reinterpret_cast<const float *>(M), W.Y);
+  }
+  {
+    const int nI = (2 * p + 1) * (2 * p + 1), nM = (p + 1) * (p + 1);
+    const size_t smem = (size_t)4 * (nI + nM) * sizeof(float2);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(k_m2l_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured = smem;
+    }
+    k_m2l_pairs<<<148 * 4, 128, smem, st>>>(p, W.small, W.counters, W.pair_t, W.src, W.C, M, W.Y);
+  }
+  k_m2l_reduce<<<ncells < 148 * 16 ? (ncells > 0 ? ncells : 1) : 148 * 16, 128, 0, st>>>(
+      p, ncells, W.off, W.cnt, W.Y, reinterpret_cast<float *>(L));
+  return cudaGetLastError();
+}

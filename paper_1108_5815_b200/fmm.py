@@ -33,7 +33,8 @@ class Stats(C.Structure):
                 ("p2p_pairs", C.c_int64), ("m2p_evals", C.c_int64), ("traversal_pairs", C.c_int64),
                 ("ms_total", C.c_double), ("ms_tree", C.c_double), ("ms_upward", C.c_double),
                 ("ms_traverse", C.c_double), ("ms_m2l", C.c_double), ("ms_p2p", C.c_double),
-                ("ms_m2p", C.c_double), ("ms_downward", C.c_double)]
+                ("ms_m2p", C.c_double), ("ms_downward", C.c_double),
+                ("launches", C.c_int64), ("cub_calls", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

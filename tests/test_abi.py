@@ -43,7 +43,7 @@ def test_binary_is_sm100a_cuda_core_code(libpath):
     funcs = {}
     for chunk in sass.split("Function : ")[1:]:
         funcs[chunk.split()[0]] = chunk
-    m2l = [v for k, v in funcs.items() if "k_m2l" in k]
+    m2l = [v for k, v in funcs.items() if "k_m2l_gemm" in k]
     assert m2l and "FFMA2" in m2l[0]  # packed FP32 FMA on the M2L hot loop
     assert "MUFU.RSQ" in [v for k, v in funcs.items() if "p2p" in k][0]
 

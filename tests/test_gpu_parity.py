@@ -50,7 +50,8 @@ def handles():
 
 CASES = [("uniform", 1000, 4, 0.5, 16, 1), ("uniform", 20000, 6, 0.5, 32, 2),
          ("plummer", 20000, 6, 0.4, 32, 3), ("shell", 8000, 5, 0.5, 20, 4),
-         ("mixed", 5000, 8, 0.45, 8, 5), ("uniform", 3000, 10, 0.4, 64, 6)]
+         ("mixed", 5000, 8, 0.45, 8, 5), ("uniform", 3000, 10, 0.4, 64, 6),
+         ("plummer", 4000, 13, 0.5, 32, 12)]  # p > 12: M2L on the direct per-pair path
 
 
 @pytest.mark.parametrize("dist,n,p,theta,ncrit,seed", CASES)
