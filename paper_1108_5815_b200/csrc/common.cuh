@@ -8,7 +8,7 @@
 //            cbeg/ccnt int32, cparent int32, cchild0/cnchild int32,
 //            cgrid int4 (doubled-grid centre cx~,cy~,cz~ = (2g+1)*2^(21-l), level) — exact MAC,
 //            cgeo float4 (centre x, y, z in FP32, half-width r)
-//   Mhat / Lhat float2[ncells][NC(p)]  power-of-two scaled expansions, orders m >= 0 only
+//   Mhat / Lhat float2[ncells][nc_stride(p)]  power-of-two scaled expansions, orders m >= 0 only
 //   lists  per target cell (off, cnt) into uint32 source-cell arrays, one array per kind
 #pragma once
 #include <cuda_runtime.h>
@@ -21,6 +21,9 @@
 // Number of stored coefficients (m >= 0) for order p, and the index of (n, m >= 0).
 __host__ __device__ __forceinline__ constexpr int nc_of(int p) { return (p + 1) * (p + 2) / 2; }
 __host__ __device__ __forceinline__ constexpr int cidx(int n, int m) { return n * (n + 1) / 2 + m; }
+// Per-cell row stride (complex entries) of the Mhat / Lhat arrays: NC rounded up to even, so
+// every row starts 16-byte aligned (TMA bulk copies); the pad entry is kept at zero.
+__host__ __device__ __forceinline__ constexpr int nc_stride(int p) { return (nc_of(p) + 1) & ~1; }
 
 struct RootInfo {
   double origin[3];

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(128) k_p2m(int p, const int *__restrict__ leav
                                              CellsView C, const float4 *__restrict__ pos,
                                              float2 *__restrict__ M) {
   extern __shared__ float2 sh_p2m[];
-  const int NC = nc_of(p);
+  const int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *acc = sh_p2m + wib * NC;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(128) k_p2m(int p, const int *__restrict__ leav
       }
     }
     __syncwarp();
-    for (int o = lane; o < NC; o += WARP) M[(size_t)leaf * NC + o] = acc[o];
+    for (int o = lane; o < NC; o += WARP) M[(size_t)leaf * NCS + o] = acc[o];
     __syncwarp();
   }
 }
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(128) k_p2m(int p, const int *__restrict__ leav
 __global__ void __launch_bounds__(128) k_m2m(int p, int c0, int nl, CellsView C,
                                              float2 *__restrict__ M) {
   extern __shared__ float2 sh_m2m[];
-  const int NC = nc_of(p);
+  const int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *Mc = sh_m2m + wib * 2 * NC, *Rb = Mc + NC;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(128) k_m2m(int p, int c0, int nl, CellsView C,
     for (int ch = 0; ch < nch; ++ch) {
       const int Cc = C.child0[P] + ch;
       const int4 gc = C.grid[Cc];
-      for (int o = lane; o < NC; o += WARP) Mc[o] = M[(size_t)Cc * NC + o];
+      for (int o = lane; o < NC; o += WARP) Mc[o] = M[(size_t)Cc * NCS + o];
       regular_table((gc.x - gp.x) / rP, (gc.y - gp.y) / rP, (gc.z - gp.z) / rP, p, Rb, lane);
       __syncwarp();
 #pragma unroll
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128) k_m2m(int p, int c0, int nl, CellsView C,
 #pragma unroll
     for (int s = 0; s < 5; ++s) {
       const int o = lane + s * WARP;
-      if (o < NC) M[(size_t)P * NC + o] = acc[s];
+      if (o < NC) M[(size_t)P * NCS + o] = acc[s];
     }
   }
 }
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(128) k_m2m(int p, int c0, int nl, CellsView C,
 __global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
                                              float2 *__restrict__ L) {
   extern __shared__ float2 sh_l2l[];
-  const int NC = nc_of(p);
+  const int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *Lp = sh_l2l + wib * 2 * NC, *Re = Lp + NC;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
     const int P = C.parent[Cc];
     const int4 gp = C.grid[P], gc = C.grid[Cc];
     const float rP = (float)(1 << (FMM_LEVELS - gp.w));
-    for (int o = lane; o < NC; o += WARP) Lp[o] = L[(size_t)P * NC + o];
+    for (int o = lane; o < NC; o += WARP) Lp[o] = L[(size_t)P * NCS + o];
     regular_table((gc.x - gp.x) / rP, (gc.y - gp.y) / rP, (gc.z - gp.z) / rP, p, Re, lane);
     __syncwarp();
     for (int o = lane; o < NC; o += WARP) {
@@ -190,8 +190,8 @@ __global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
         for (int kk = klo; kk <= khi; ++kk) a = cadd(a, cmul(sget(Lp, j, kk), sget(Re, j - n, kk - m)));
       }
       const float sc = ldexpf(1.f, -(n + 1));
-      const float2 old = L[(size_t)Cc * NC + o];
-      L[(size_t)Cc * NC + o] = make_float2(old.x + sc * a.x, old.y + sc * a.y);
+      const float2 old = L[(size_t)Cc * NCS + o];
+      L[(size_t)Cc * NCS + o] = make_float2(old.x + sc * a.x, old.y + sc * a.y);
     }
     __syncwarp();
   }
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(128) k_m2p(int p, const int *__restrict__ leav
                                              const float2 *__restrict__ M,
                                              float4 *__restrict__ acc) {
   extern __shared__ float2 sh_m2p[];
-  const int NC = nc_of(p);
+  const int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *Ms = sh_m2p + wib * NC;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(128) k_m2p(int p, const int *__restrict__ leav
         for (int e = 0; e < n_s; ++e) {
           const int s = Ls.src[1][off + e];
           __syncwarp();
-          for (int o = lane; o < NC; o += WARP) Ms[o] = M[(size_t)s * NC + o];
+          for (int o = lane; o < NC; o += WARP) Ms[o] = M[(size_t)s * NCS + o];
           __syncwarp();
           const float4 g = C.geo[s];
           const float rinv = 1.f / g.w;
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(128) k_l2p(int p, const int *__restrict__ leav
                                              float *__restrict__ phi_out,
                                              float *__restrict__ grad_out, int use_local) {
   extern __shared__ float2 sh_l2p[];
-  const int NC = nc_of(p);
+  const int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *Ll = sh_l2p + wib * NC;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(128) k_l2p(int p, const int *__restrict__ leav
     const float rinv = 1.f / g.w;
     __syncwarp();
     if (use_local)
-      for (int o = lane; o < NC; o += WARP) Ll[o] = L[(size_t)leaf * NC + o];
+      for (int o = lane; o < NC; o += WARP) Ll[o] = L[(size_t)leaf * NCS + o];
     __syncwarp();
     for (int c0 = 0; c0 < cnt; c0 += WARP) {
       const bool valid = c0 + lane < cnt;

@@ -101,7 +101,8 @@ struct fmm_ctx {
   // M2L class batching
   DBuf<int> m2l_pair_t, m2l_flag, m2l_cid, m2l_cstart, m2l_counters;
   DBuf<unsigned long long> m2l_keys_in, m2l_keys;
-  DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small;
+  DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep;
+  DBuf<float> m2l_T;
   DBuf<int4> m2l_items;
   DBuf<float> m2l_Y;
   // lists
@@ -372,8 +373,10 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   if (int rc = build_tree(h, xyz, q, n)) return rc;
   record(h, EV_TREE);
   // a7/a8 upward sweep
-  CK(h->M.ensure((size_t)h->ncells * NC));
-  CK(h->L.ensure((size_t)h->ncells * NC));
+  const int NCS = nc_stride(p);
+  CK(h->M.ensure((size_t)h->ncells * NCS));
+  CK(h->L.ensure((size_t)h->ncells * NCS));
+  if (NCS != NC) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
   launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, st);
   CKL();
   for (int level = h->depth - 1; level >= 0; --level) {
@@ -421,9 +424,18 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     W.tmp = h->cub_tmp.p;
     W.tmp_bytes = h->cub_tmp.cap;
     W.direct_all = m2l_gemm_supported(p) ? 0 : 1;
+    CK(h->m2l_class_rep.ensure(np));
+    W.class_rep = h->m2l_class_rep.p;
     CK(m2l_prepare(W, np, h->ncells, st));
     h->stats.launches += 6;
     h->stats.cub_calls += 2;
+    CK(cudaMemcpyAsync(h->h_small, h->m2l_counters.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int ngclass = h->h_small[3];
+    CK(h->m2l_T.ensure((size_t)std::max(1, ngclass) * m2l_T_floats(p)));
+    W.Tg = h->m2l_T.p;
+    CK(m2l_build_T(p, W, ngclass, st));
+    h->stats.launches += 1;
     record(h, EV_M2L_PREP);
     CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st));
     h->stats.launches += 3;
@@ -615,7 +627,7 @@ int fmm_destroy(fmm_t h) {
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
-  h->m2l_Y.release();
+  h->m2l_Y.release(); h->m2l_class_rep.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();

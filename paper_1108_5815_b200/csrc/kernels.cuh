@@ -75,6 +75,8 @@ struct M2LWork {
   int *flag, *cid, *cstart, *counters;
   int4 *items;              // GEMM work items (first sorted position, count, representative pair)
   unsigned *small;          // pairs on the direct path
+  unsigned *class_rep;      // representative pair of every GEMM class
+  float *Tg;                // translation matrices of the GEMM classes [ngclass][m2l_T_floats(p)]
   float *Y;                 // per-pair results [npairs][m2l_y_stride(p)]
   void *tmp;
   size_t tmp_bytes;
@@ -85,6 +87,8 @@ bool m2l_gemm_supported(int p);
 int m2l_y_stride(int p);
 size_t m2l_temp_bytes(int npairs);
 cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st);
+size_t m2l_T_floats(int p);
+cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st);
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
                         float2 *L, cudaStream_t st);
 

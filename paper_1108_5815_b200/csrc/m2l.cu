@@ -20,9 +20,11 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
-#define M2L_ITEM 512
+#define M2L_ITEM 1024
+#define M2L_PREF 12  // float4 per thread staged for the next chunk (= max over p <= 12 of ceil(Kpad/4*64/threads))
 #define M2L_CHUNK 64
-#define M2L_SMALL 4
+#define M2L_SMALL 16
+#define M2L_XCH 32  // pair columns per chunk (double-buffered)
 
 // coefficient index c = n(n+1)/2 + m  ->  (n, m)
 __device__ __forceinline__ short2 nm_of(int c) {
@@ -143,11 +145,12 @@ __global__ void k_m2l_class_start(int npairs, const int *__restrict__ flag,
   }
 }
 
-// counters: [0] classes, [1] GEMM work items, [2] pairs on the direct path
+// counters: [0] classes, [1] GEMM work items, [2] pairs on the direct path, [3] GEMM classes
 __global__ void k_m2l_items(int npairs, int direct_all, const int *__restrict__ flag,
                             const int *__restrict__ cid, const int *__restrict__ cstart,
                             const unsigned *__restrict__ sidx, int4 *__restrict__ items,
-                            unsigned *__restrict__ small, int *__restrict__ counters) {
+                            unsigned *__restrict__ small, unsigned *__restrict__ class_rep,
+                            int *__restrict__ counters) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
     if (!flag[i]) continue;
     const int c = cid[i];
@@ -155,8 +158,10 @@ __global__ void k_m2l_items(int npairs, int direct_all, const int *__restrict__ 
     if (!direct_all && n >= M2L_SMALL) {
       const int ni = (n + M2L_ITEM - 1) / M2L_ITEM;
       const int base = atomicAdd(&counters[1], ni);
+      const int gid = atomicAdd(&counters[3], 1);
+      class_rep[gid] = sidx[i];
       for (int a = 0; a < ni; ++a)
-        items[base + a] = make_int4(i + a * M2L_ITEM, min(M2L_ITEM, n - a * M2L_ITEM), (int)sidx[i], 0);
+        items[base + a] = make_int4(i + a * M2L_ITEM, min(M2L_ITEM, n - a * M2L_ITEM), (int)sidx[i], gid);
     } else {
       const int base = atomicAdd(&counters[2], n);
       for (int b = 0; b < n; ++b) small[base + b] = sidx[i + b];
@@ -164,35 +169,26 @@ __global__ void k_m2l_items(int npairs, int direct_all, const int *__restrict__ 
   }
 }
 
-// ---- class GEMM -------------------------------------------------------------------------------
-// Block = (Rpad/12) x 16 threads; thread (rg, cg) owns rows [12 rg, 12 rg + 12) x columns
-// [4 cg, 4 cg + 4) of the 2NC x 64 chunk product.
-__global__ void k_m2l_gemm(int p, const int4 *__restrict__ items, const int *__restrict__ counters,
-                           const unsigned *__restrict__ sidx, const int *__restrict__ pair_t,
-                           const unsigned *__restrict__ src, CellsView C,
-                           const float *__restrict__ M, float *__restrict__ Y) {
-  extern __shared__ float4 sh_gemm4[];
-  float *sh = reinterpret_cast<float *>(sh_gemm4);
+// ---- class translation matrices ---------------------------------------------------------------
+// T_g[kcol][row] (Kpad x Rpad floats) for GEMM class g: row = output real index (2 c_out + re/im),
+// kcol = input real index (2 c_in + re/im); derived from I(u) of the class representative.
+__global__ void __launch_bounds__(256) k_m2l_build_T(int p, const int *__restrict__ counters,
+                                                     const unsigned *__restrict__ class_rep,
+                                                     const int *__restrict__ pair_t,
+                                                     const unsigned *__restrict__ src,
+                                                     CellsView C, float *__restrict__ Tg) {
+  extern __shared__ float2 sh_itab[];
   const int NC = nc_of(p), KR = 2 * NC;
   const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
-  float *Ts = sh;                       // [Kpad][Rpad]
-  const int XSK = Kpad + 1;             // odd row stride of Xs
-  float *Xs = sh + Kpad * Rpad;         // [M2L_CHUNK][XSK]
-  float2 *Itab = reinterpret_cast<float2 *>(Xs);  // aliased during the T build
-  int *colsrc = reinterpret_cast<int *>(Xs + M2L_CHUNK * XSK);  // [M2L_CHUNK] source cells
-  const int tid = threadIdx.x, nthr = blockDim.x;
-  const int rg = tid / 16, cg = tid % 16;
-  const int nitems = counters[1];
-
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const int4 item = items[it];
-    const int pos0 = item.x, cnt = item.y, rep = item.z;
+  const int ng = counters[3];
+  for (int gid = blockIdx.x; gid < ng; gid += gridDim.x) {
+    const int rep = class_rep[gid];
     const PairGeo g = pair_geo(C.grid[pair_t[rep]], C.grid[src[rep]]);
-    __syncthreads();  // previous item's readers of Xs are done
-    irregular_table(g.ux, g.uy, g.uz, 2 * p, Itab, tid, nthr);
     __syncthreads();
-    // T[kcol][row]: row = output real index (2 c_out + re/im), kcol = input real index
-    for (int id = tid; id < Kpad * Rpad; id += nthr) {
+    irregular_table(g.ux, g.uy, g.uz, 2 * p, sh_itab, threadIdx.x, blockDim.x);
+    __syncthreads();
+    float *T = Tg + (size_t)gid * Kpad * Rpad;
+    for (int id = threadIdx.x; id < Kpad * Rpad; id += blockDim.x) {
       const int kcol = id / Rpad, row = id - kcol * Rpad;
       float v = 0.f;
       if (row < KR && kcol < KR) {
@@ -203,84 +199,157 @@ __global__ void k_m2l_gemm(int p, const int4 *__restrict__ items, const int *__r
           const float sgn = ((j + k) & 1) ? -1.f : 1.f;
           const float sc = sgn * (g.vform ? ldexpf(1.f, -g.dl * (j + 1)) : ldexpf(1.f, n * g.dl));
           const int a = n + j;
-          const float2 Cp = Itab[a * a + a + (m - k)];
+          const float2 Cp = sh_itab[a * a + a + (m - k)];
           if (m == 0) {
             v = sc * (rim ? Cp.y : Cp.x);
           } else {
-            const float2 Cm = Itab[a * a + a + (-m - k)];
+            const float2 Cm = sh_itab[a * a + a + (-m - k)];
             const float sm = (m & 1) ? -1.f : 1.f;
-            if (!cim) {  // coefficient of Re M: A = Cp + (-1)^m Cm
+            if (!cim)  // coefficient of Re M: Cp + (-1)^m Cm
               v = sc * (rim ? (Cp.y + sm * Cm.y) : (Cp.x + sm * Cm.x));
-            } else {     // coefficient of Im M: i (Cp - (-1)^m Cm)
+            else       // coefficient of Im M: i (Cp - (-1)^m Cm)
               v = sc * (rim ? (Cp.x - sm * Cm.x) : -(Cp.y - sm * Cm.y));
-            }
           }
         }
       }
-      Ts[kcol * Rpad + row] = v;
+      T[id] = v;
     }
-    for (int c0 = 0; c0 < cnt; c0 += M2L_CHUNK) {
-      const int ncol = min(M2L_CHUNK, cnt - c0);
-      __syncthreads();  // T ready / previous chunk consumed
-      // gather the multipoles of the chunk's sources: Xs[col][k], odd row stride (bank-free)
-      for (int c = tid; c < M2L_CHUNK; c += nthr) colsrc[c] = c < ncol ? (int)src[sidx[pos0 + c0 + c]] : -1;
-      __syncthreads();
-      for (int id = tid; id < (Kpad / 4) * M2L_CHUNK; id += nthr) {
-        const int q = id / M2L_CHUNK, col = id - q * M2L_CHUNK;
-        const int s = colsrc[col];
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (s >= 0) {
-          const float *Mr = M + (size_t)s * KR + 4 * q;
-          if (4 * q + 3 < KR) {
-            if ((KR & 3) == 0) v = *reinterpret_cast<const float4 *>(Mr);  // 16-byte aligned rows
-            else {
-              const float2 a = *reinterpret_cast<const float2 *>(Mr);
-              const float2 b = *reinterpret_cast<const float2 *>(Mr + 2);
-              v = make_float4(a.x, a.y, b.x, b.y);
-            }
-          } else {
-            if (4 * q + 0 < KR) v.x = Mr[0];
-            if (4 * q + 1 < KR) v.y = Mr[1];
-            if (4 * q + 2 < KR) v.z = Mr[2];
-          }
-        }
-        float *xd = Xs + col * XSK + 4 * q;
-        xd[0] = v.x;
-        xd[1] = v.y;
-        xd[2] = v.z;
-        xd[3] = v.w;
+  }
+}
+
+// ---- TMA bulk copies + mbarriers (sm_90+ PTX; SASS UBLKCP / SYNCS) ------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n }" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---- class GEMM -------------------------------------------------------------------------------
+// One CTA per work item (class g, up to M2L_ITEM pairs). T_g arrives by one TMA bulk copy; the
+// multipoles of M2L_XCH source cells per chunk arrive by one bulk copy per cell into a double
+// buffer, so chunk c+1 streams in while chunk c is multiplied. Thread (rg, cg) owns rows
+// [12 rg, 12 rg + 12) and pair columns {cg, cg + 16}; every inner step is 12 packed FFMA2 per
+// 3 broadcast LDS.128 of T and 2 LDS.128 of X per 4 k.
+__global__ void __launch_bounds__(256, 2) k_m2l_gemm(int p, const int4 *__restrict__ items,
+                                                     const int *__restrict__ counters,
+                                                     const unsigned *__restrict__ sidx,
+                                                     const unsigned *__restrict__ src,
+                                                     const float *__restrict__ Tg,
+                                                     const float *__restrict__ M,
+                                                     float *__restrict__ Y) {
+  extern __shared__ __align__(128) float sh_gemm[];
+  const int NC = nc_of(p), KR = 2 * NC;
+  const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
+  const int XKS = ((Kpad >> 2) & 1) ? Kpad : Kpad + 4;  // X row stride: odd number of 16-B slots
+  float *Ts = sh_gemm;
+  float *Xs0 = Ts + Kpad * Rpad;
+  float *Xs1 = Xs0 + M2L_XCH * XKS;
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xs1 + M2L_XCH * XKS);
+  const int tid = threadIdx.x;
+  const int rg = tid >> 4, cg = tid & 15;
+  const unsigned tbytes = (unsigned)(Kpad * Rpad * sizeof(float));
+  const unsigned rbytes = (unsigned)(Kpad * sizeof(float));
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned ph_t = 0, ph_x0 = 0, ph_x1 = 0;
+  const int nitems = counters[1];
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int4 item = items[it];
+    const int pos0 = item.x, cnt = item.y, gid = item.w;
+    const int nchunk = (cnt + M2L_XCH - 1) / M2L_XCH;
+    __syncthreads();  // Ts / Xs of the previous item are no longer read
+    auto issue = [&](int c, float *Xb, unsigned long long *bar) {
+      const int ncol = min(M2L_XCH, cnt - c * M2L_XCH);
+      if (tid == 0) mbar_expect_tx(bar, ncol * rbytes);
+      if (tid < ncol) {
+        fence_proxy_async();
+        const int s = src[sidx[pos0 + c * M2L_XCH + tid]];
+        bulk_g2s(Xb + tid * XKS, M + (size_t)s * Kpad, rbytes, bar);
       }
-      __syncthreads();
+    };
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&bars[0], tbytes);
+      bulk_g2s(Ts, Tg + (size_t)gid * Kpad * Rpad, tbytes, &bars[0]);
+    }
+    issue(0, Xs0, &bars[1]);
+    mbar_wait(&bars[0], ph_t);
+    ph_t ^= 1;
+    for (int c = 0; c < nchunk; ++c) {
+      const bool odd = c & 1;
+      float *Xb = odd ? Xs1 : Xs0;
+      if (odd) {
+        mbar_wait(&bars[2], ph_x1);
+        ph_x1 ^= 1;
+      } else {
+        mbar_wait(&bars[1], ph_x0);
+        ph_x0 ^= 1;
+      }
+      if (c + 1 < nchunk) issue(c + 1, odd ? Xs0 : Xs1, odd ? &bars[1] : &bars[2]);
+      const int ncol = min(M2L_XCH, cnt - c * M2L_XCH);
       if (rg * 12 < Rpad) {
-        float2 acc[6][4];
+        float2 acc[6][2];
 #pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = make_float2(0.f, 0.f);
+        for (int a = 0; a < 6; ++a) acc[a][0] = acc[a][1] = make_float2(0.f, 0.f);
         const float *Tp = Ts + rg * 12;
-        const float *Xp = Xs + cg * XSK;  // columns cg, cg + 16, cg + 32, cg + 48
-#pragma unroll 2
-        for (int k = 0; k < Kpad; ++k) {
-          const float4 t0 = *reinterpret_cast<const float4 *>(Tp + k * Rpad);
-          const float4 t1 = *reinterpret_cast<const float4 *>(Tp + k * Rpad + 4);
-          const float4 t2 = *reinterpret_cast<const float4 *>(Tp + k * Rpad + 8);
-          const float x0 = Xp[k], x1 = Xp[16 * XSK + k], x2 = Xp[32 * XSK + k], x3 = Xp[48 * XSK + k];
-          const float2 tr[6] = {make_float2(t0.x, t0.y), make_float2(t0.z, t0.w),
-                                make_float2(t1.x, t1.y), make_float2(t1.z, t1.w),
-                                make_float2(t2.x, t2.y), make_float2(t2.z, t2.w)};
-          const float2 xc[4] = {make_float2(x0, x0), make_float2(x1, x1), make_float2(x2, x2),
-                                make_float2(x3, x3)};
+        const float *x0p = Xb + cg * XKS, *x1p = Xb + (cg + 16) * XKS;
+        for (int k = 0; k < Kpad; k += 4) {
+          const float4 xa = *reinterpret_cast<const float4 *>(x0p + k);
+          const float4 xb = *reinterpret_cast<const float4 *>(x1p + k);
+          const float xav[4] = {xa.x, xa.y, xa.z, xa.w}, xbv[4] = {xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
-          for (int a = 0; a < 6; ++a)
+          for (int kk = 0; kk < 4; ++kk) {
+            const float *tr = Tp + (k + kk) * Rpad;
+            const float4 t0 = *reinterpret_cast<const float4 *>(tr);
+            const float4 t1 = *reinterpret_cast<const float4 *>(tr + 4);
+            const float4 t2 = *reinterpret_cast<const float4 *>(tr + 8);
+            const float2 tv[6] = {make_float2(t0.x, t0.y), make_float2(t0.z, t0.w),
+                                  make_float2(t1.x, t1.y), make_float2(t1.z, t1.w),
+                                  make_float2(t2.x, t2.y), make_float2(t2.z, t2.w)};
+            const float2 xs0 = make_float2(xav[kk], xav[kk]), xs1 = make_float2(xbv[kk], xbv[kk]);
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = __ffma2_rn(tr[a], xc[b], acc[a][b]);
+            for (int a = 0; a < 6; ++a) {
+              acc[a][0] = __ffma2_rn(tv[a], xs0, acc[a][0]);
+              acc[a][1] = __ffma2_rn(tv[a], xs1, acc[a][1]);
+            }
+          }
         }
         const int YS = Kpad;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < 2; ++b) {
           const int col = cg + 16 * b;
           if (col >= ncol) continue;
-          float *yr = Y + (size_t)sidx[pos0 + c0 + col] * YS + rg * 12;
+          float *yr = Y + (size_t)sidx[pos0 + c * M2L_XCH + col] * YS + rg * 12;
 #pragma unroll
           for (int a = 0; a < 6; ++a) {
             const int r = rg * 12 + 2 * a;
@@ -289,6 +358,7 @@ __global__ void k_m2l_gemm(int p, const int4 *__restrict__ items, const int *__r
           }
         }
       }
+      __syncthreads();  // this chunk's buffer may be refilled by the next iteration
     }
   }
 }
@@ -316,7 +386,7 @@ __global__ void __launch_bounds__(128) k_m2l_pairs(int p, const unsigned *__rest
     for (int o = lane; o < nM; o += 32) {
       const int n = (int)sqrtf((float)o + 0.5f);
       const int m = o - n * n - n;
-      const float2 v = sget(M + (size_t)s * NC, n, m);
+      const float2 v = sget(M + (size_t)s * nc_stride(p), n, m);
       const float sc = g.vform ? 1.f : ldexpf(1.f, n * g.dl);
       Mx[o] = make_float2(v.x * sc, v.y * sc);
     }
@@ -354,7 +424,7 @@ __global__ void __launch_bounds__(128) k_m2l_reduce(int p, int ncells, const int
     for (int r = threadIdx.x; r < KR; r += blockDim.x) {
       float s = 0.f;
       for (int e = 0; e < c; ++e) s += Y[(size_t)(o + e) * YS + r];
-      L[(size_t)t * KR + r] = s;
+      L[(size_t)t * YS + r] = s;
     }
   }
 }
@@ -363,9 +433,17 @@ __global__ void __launch_bounds__(128) k_m2l_reduce(int p, int ncells, const int
 size_t m2l_gemm_smem(int p) {
   const int KR = 2 * nc_of(p);
   const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
-  return (size_t)(Kpad * Rpad + M2L_CHUNK * (Kpad + 1) + M2L_CHUNK) * sizeof(float);
+  const int XKS = ((Kpad >> 2) & 1) ? Kpad : Kpad + 4;
+  return (size_t)(Kpad * Rpad + 2 * M2L_XCH * XKS) * sizeof(float) + 4 * sizeof(unsigned long long);
 }
-bool m2l_gemm_supported(int p) { return m2l_gemm_smem(p) <= 227 * 1024; }
+size_t m2l_T_floats(int p) {
+  const int KR = 2 * nc_of(p);
+  return (size_t)((KR + 3) & ~3) * (((KR + 11) / 12) * 12);
+}
+bool m2l_gemm_supported(int p) {
+  const int KR = 2 * nc_of(p), nthr = ((KR + 11) / 12) * 16;
+  return m2l_gemm_smem(p) <= 227 * 1024 && nthr <= 256 && nthr >= M2L_XCH;
+}
 int m2l_y_stride(int p) { return (2 * nc_of(p) + 3) & ~3; }
 
 cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st) {
@@ -390,7 +468,7 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   cudaMemsetAsync(W.counters, 0, 4 * sizeof(int), st);
   k_m2l_class_start<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.flag, W.cid, W.cstart, W.counters);
   k_m2l_items<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.direct_all, W.flag, W.cid, W.cstart, W.sidx,
-                                             W.items, W.small, W.counters);
+                                             W.items, W.small, W.class_rep, W.counters);
   return cudaGetLastError();
 }
 
@@ -401,6 +479,14 @@ size_t m2l_temp_bytes(int npairs) {
                                   (unsigned *)nullptr, npairs, 0, 64);
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, npairs);
   return a > b ? a : b;
+}
+
+cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st) {
+  if (ngclass <= 0) return cudaSuccess;
+  const size_t smem = (size_t)(2 * p + 1) * (2 * p + 1) * sizeof(float2);
+  k_m2l_build_T<<<ngclass < 148 * 4 ? ngclass : 148 * 4, 256, smem, st>>>(
+      p, W.counters, W.class_rep, W.pair_t, W.src, W.C, W.Tg);
+  return cudaGetLastError();
 }
 
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
@@ -415,8 +501,8 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
     const int KR = 2 * nc_of(p);
     const int nthr = ((KR + 11) / 12) * 16;
     const int per_sm = (int)((227 * 1024) / smem) < 2 ? 1 : 2;
-    k_m2l_gemm<<<148 * per_sm, nthr, smem, st>>>(p, W.items, W.counters, W.sidx, W.pair_t, W.src,
-                                                  W.C, reinterpret_cast<const float *>(M), W.Y);
+    k_m2l_gemm<<<148 * per_sm, nthr, smem, st>>>(p, W.items, W.counters, W.sidx, W.src, W.Tg,
+                                                  reinterpret_cast<const float *>(M), W.Y);
   }
   {
     const int nI = (2 * p + 1) * (2 * p + 1), nM = (p + 1) * (p + 1);
