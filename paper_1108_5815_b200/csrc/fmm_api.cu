@@ -101,7 +101,7 @@ struct fmm_ctx {
   // M2L class batching
   DBuf<int> m2l_pair_t, m2l_flag, m2l_cid, m2l_cstart, m2l_counters;
   DBuf<unsigned long long> m2l_keys_in, m2l_keys;
-  DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep;
+  DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep, m2l_ssrc;
   DBuf<float> m2l_T;
   DBuf<int4> m2l_items;
   DBuf<float> m2l_Y;
@@ -425,7 +425,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     W.tmp_bytes = h->cub_tmp.cap;
     W.direct_all = m2l_gemm_supported(p) ? 0 : 1;
     CK(h->m2l_class_rep.ensure(np));
+    CK(h->m2l_ssrc.ensure(np));
     W.class_rep = h->m2l_class_rep.p;
+    W.ssrc = h->m2l_ssrc.p;
     CK(m2l_prepare(W, np, h->ncells, st));
     h->stats.launches += 6;
     h->stats.cub_calls += 2;
@@ -627,7 +629,7 @@ int fmm_destroy(fmm_t h) {
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
-  h->m2l_Y.release(); h->m2l_class_rep.release(); h->m2l_T.release();
+  h->m2l_Y.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();

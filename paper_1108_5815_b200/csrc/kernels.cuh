@@ -72,6 +72,7 @@ struct M2LWork {
   int *pair_t;              // target cell of each pair
   unsigned long long *keys_in, *keys;
   unsigned *idx_in, *sidx;  // pair indices sorted by class key
+  unsigned *ssrc;           // source cell of each class-sorted pair
   int *flag, *cid, *cstart, *counters;
   int4 *items;              // GEMM work items (first sorted position, count, representative pair)
   unsigned *small;          // pairs on the direct path

@@ -106,19 +106,25 @@ __global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
   }
 }
 
+// Class key = (level difference, integer offset in units of the smaller cell); the source cell
+// id fills the low bits so that, after the radix sort, each class lists its pairs in source
+// order (consecutive source cells -> contiguous multipole rows -> one bulk copy per chunk).
+#define M2L_SRC_BITS 25
 __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
                           const unsigned *__restrict__ src, CellsView C,
                           unsigned long long *__restrict__ keys, unsigned *__restrict__ idx) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
-    const int4 gt = C.grid[pair_t[e]], gs = C.grid[src[e]];
+    const unsigned s = src[e];
+    const int4 gt = C.grid[pair_t[e]], gs = C.grid[s];
     const int dl = gt.w - gs.w;
     const int sh = FMM_LEVELS - max(gt.w, gs.w);
     const int dx = (gt.x - gs.x) >> sh, dy = (gt.y - gs.y) >> sh, dz = (gt.z - gs.z) >> sh;
-    const int lim = 1 << 18;
+    const int lim = 1 << 10;
     unsigned long long key;
-    if (abs(dx) < lim && abs(dy) < lim && abs(dz) < lim)
-      key = ((unsigned long long)(dl + 32) << 57) | ((unsigned long long)(dx + lim) << 38) |
-            ((unsigned long long)(dy + lim) << 19) | (unsigned long long)(dz + lim);
+    if (abs(dx) < lim && abs(dy) < lim && abs(dz) < lim && s < (1u << M2L_SRC_BITS))
+      key = ((unsigned long long)(dl + 16) << 58) | ((unsigned long long)(dx + lim) << 47) |
+            ((unsigned long long)(dy + lim) << 36) | ((unsigned long long)(dz + lim) << 25) |
+            (unsigned long long)s;
     else
       key = (1ull << 63) | (unsigned long long)e;  // out of key range: a class of its own
     keys[e] = key;
@@ -127,9 +133,14 @@ __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
 }
 
 __global__ void k_m2l_class_flags(int npairs, const unsigned long long *__restrict__ skeys,
-                                  int *__restrict__ flag) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x)
-    flag[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1 : 0;
+                                  const unsigned *__restrict__ sidx,
+                                  const unsigned *__restrict__ src, int *__restrict__ flag,
+                                  unsigned *__restrict__ ssrc) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    const unsigned long long ck = skeys[i] >> M2L_SRC_BITS;  // class part of the key
+    flag[i] = (i == 0 || ck != (skeys[i - 1] >> M2L_SRC_BITS) || (skeys[i] >> 63)) ? 1 : 0;
+    ssrc[i] = src[sidx[i]];  // source cell in class-sorted order (one coalesced load later)
+  }
 }
 
 __global__ void k_m2l_class_start(int npairs, const int *__restrict__ flag,
@@ -250,15 +261,20 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 // ---- class GEMM -------------------------------------------------------------------------------
-// One CTA per work item (class g, up to M2L_ITEM pairs). T_g arrives by one TMA bulk copy; the
-// multipoles of M2L_XCH source cells per chunk arrive by one bulk copy per cell into a double
-// buffer, so chunk c+1 streams in while chunk c is multiplied. Thread (rg, cg) owns rows
-// [12 rg, 12 rg + 12) and pair columns {cg, cg + 16}; every inner step is 12 packed FFMA2 per
-// 3 broadcast LDS.128 of T and 2 LDS.128 of X per 4 k.
-__global__ void __launch_bounds__(256, 2) k_m2l_gemm(int p, const int4 *__restrict__ items,
+// Warp-specialised CTA per group of work items (class g, up to M2L_ITEM pairs each):
+//   * producer warp: TMA bulk copy of T_g (one copy) and, per chunk of M2L_XCH pairs, one bulk
+//     copy per source cell's multipole row into a double-buffered tile; full/empty mbarriers;
+//   * consumer warps: thread (rg, cg) owns rows [12 rg, 12 rg + 12) and pair columns {cg, cg+16}
+//     of the 2NC x M2L_XCH chunk product: 12 packed FFMA2 per 3 broadcast LDS.128 of T and
+//     2 LDS.128 of X every 4 k. No CTA-wide barrier inside the item loop.
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restrict__ items,
                                                      const int *__restrict__ counters,
                                                      const unsigned *__restrict__ sidx,
-                                                     const unsigned *__restrict__ src,
+                                                     const unsigned *__restrict__ ssrc,
                                                      const float *__restrict__ Tg,
                                                      const float *__restrict__ M,
                                                      float *__restrict__ Y) {
@@ -266,62 +282,83 @@ __global__ void __launch_bounds__(256, 2) k_m2l_gemm(int p, const int4 *__restri
   const int NC = nc_of(p), KR = 2 * NC;
   const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
   const int XKS = ((Kpad >> 2) & 1) ? Kpad : Kpad + 4;  // X row stride: odd number of 16-B slots
+  const int ncons = (Rpad / 12) * 16;                    // consumer threads
+  const int ncw = (ncons + 31) / 32;                     // consumer warps; the next warp produces
   float *Ts = sh_gemm;
-  float *Xs0 = Ts + Kpad * Rpad;
-  float *Xs1 = Xs0 + M2L_XCH * XKS;
-  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xs1 + M2L_XCH * XKS);
-  const int tid = threadIdx.x;
-  const int rg = tid >> 4, cg = tid & 15;
+  float *Xs0 = Ts + Kpad * Rpad;  // double buffer: Xs0 + b * M2L_XCH * XKS
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xs0 + 2 * M2L_XCH * XKS);
+  unsigned long long *t_full = &bars[0], *t_empty = &bars[1];
+  unsigned long long *x_full = &bars[2], *x_empty = &bars[4];  // [2] each
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned tbytes = (unsigned)(Kpad * Rpad * sizeof(float));
   const unsigned rbytes = (unsigned)(Kpad * sizeof(float));
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], 1);
+    mbar_init(t_full, 1);
+    mbar_init(t_empty, ncw);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&x_full[b], 1);
+      mbar_init(&x_empty[b], ncw);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  unsigned ph_t = 0, ph_x0 = 0, ph_x1 = 0;
   const int nitems = counters[1];
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const int4 item = items[it];
-    const int pos0 = item.x, cnt = item.y, gid = item.w;
-    const int nchunk = (cnt + M2L_XCH - 1) / M2L_XCH;
-    __syncthreads();  // Ts / Xs of the previous item are no longer read
-    auto issue = [&](int c, float *Xb, unsigned long long *bar) {
-      const int ncol = min(M2L_XCH, cnt - c * M2L_XCH);
-      if (tid == 0) mbar_expect_tx(bar, ncol * rbytes);
-      if (tid < ncol) {
+
+  if (warp == ncw) {  // ---------------- producer ----------------
+    int g = 0, ii = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ii) {
+      const int4 item = items[it];
+      const int pos0 = item.x, cnt = item.y, gid = item.w;
+      if (ii > 0) mbar_wait(t_empty, (ii - 1) & 1);
+      if (lane == 0) {
         fence_proxy_async();
-        const int s = src[sidx[pos0 + c * M2L_XCH + tid]];
-        bulk_g2s(Xb + tid * XKS, M + (size_t)s * Kpad, rbytes, bar);
+        mbar_expect_tx(t_full, tbytes);
+        bulk_g2s(Ts, Tg + (size_t)gid * Kpad * Rpad, tbytes, t_full);
       }
-    };
-    if (tid == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(&bars[0], tbytes);
-      bulk_g2s(Ts, Tg + (size_t)gid * Kpad * Rpad, tbytes, &bars[0]);
+      for (int c0 = 0; c0 < cnt; c0 += M2L_XCH, ++g) {
+        const int b = g & 1, use = g >> 1;
+        if (use > 0) mbar_wait(&x_empty[b], (use - 1) & 1);
+        const int ncol = min(M2L_XCH, cnt - c0);
+        const int s = lane < ncol ? (int)ssrc[pos0 + c0 + lane] : 0;
+        const int s0 = __shfl_sync(0xffffffffu, s, 0), sl = __shfl_sync(0xffffffffu, s, ncol - 1);
+        const bool contiguous = (XKS == Kpad) && (sl - s0 == ncol - 1) &&
+                                __all_sync(0xffffffffu, lane >= ncol || s == s0 + lane);
+        if (lane == 0) mbar_expect_tx(&x_full[b], ncol * rbytes);
+        __syncwarp();
+        if (contiguous) {  // consecutive source cells: one copy of ncol rows
+          if (lane == 0) {
+            fence_proxy_async();
+            bulk_g2s(Xs0 + b * M2L_XCH * XKS, M + (size_t)s0 * Kpad, ncol * rbytes, &x_full[b]);
+          }
+        } else if (lane < ncol) {
+          fence_proxy_async();
+          bulk_g2s(Xs0 + b * M2L_XCH * XKS + lane * XKS, M + (size_t)s * Kpad, rbytes, &x_full[b]);
+        }
+      }
     }
-    issue(0, Xs0, &bars[1]);
-    mbar_wait(&bars[0], ph_t);
-    ph_t ^= 1;
-    for (int c = 0; c < nchunk; ++c) {
-      const bool odd = c & 1;
-      float *Xb = odd ? Xs1 : Xs0;
-      if (odd) {
-        mbar_wait(&bars[2], ph_x1);
-        ph_x1 ^= 1;
-      } else {
-        mbar_wait(&bars[1], ph_x0);
-        ph_x0 ^= 1;
-      }
-      if (c + 1 < nchunk) issue(c + 1, odd ? Xs0 : Xs1, odd ? &bars[1] : &bars[2]);
-      const int ncol = min(M2L_XCH, cnt - c * M2L_XCH);
-      if (rg * 12 < Rpad) {
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int rg = tid >> 4, cg = tid & 15;
+  const bool active = tid < ncons;
+  int g = 0, ii = 0;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ii) {
+    const int4 item = items[it];
+    const int pos0 = item.x, cnt = item.y;
+    mbar_wait(t_full, ii & 1);
+    for (int c0 = 0; c0 < cnt; c0 += M2L_XCH, ++g) {
+      const int b = g & 1, use = g >> 1;
+      const int ncol = min(M2L_XCH, cnt - c0);
+      // output rows of this thread's two pair columns, fetched before the product
+      const unsigned y0 = cg < ncol ? sidx[pos0 + c0 + cg] : 0u;
+      const unsigned y1 = cg + 16 < ncol ? sidx[pos0 + c0 + cg + 16] : 0u;
+      mbar_wait(&x_full[b], use & 1);
+      if (active) {
         float2 acc[6][2];
 #pragma unroll
         for (int a = 0; a < 6; ++a) acc[a][0] = acc[a][1] = make_float2(0.f, 0.f);
         const float *Tp = Ts + rg * 12;
+        const float *Xb = Xs0 + b * M2L_XCH * XKS;
         const float *x0p = Xb + cg * XKS, *x1p = Xb + (cg + 16) * XKS;
         for (int k = 0; k < Kpad; k += 4) {
           const float4 xa = *reinterpret_cast<const float4 *>(x0p + k);
@@ -344,22 +381,28 @@ __global__ void __launch_bounds__(256, 2) k_m2l_gemm(int p, const int4 *__restri
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&x_empty[b]);  // this warp is done reading Xs[b]
         const int YS = Kpad;
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int col = cg + 16 * b;
+        for (int bb = 0; bb < 2; ++bb) {
+          const int col = cg + 16 * bb;
           if (col >= ncol) continue;
-          float *yr = Y + (size_t)sidx[pos0 + c * M2L_XCH + col] * YS + rg * 12;
+          float *yr = Y + (size_t)(bb ? y1 : y0) * YS + rg * 12;
 #pragma unroll
           for (int a = 0; a < 6; ++a) {
             const int r = rg * 12 + 2 * a;
-            if (r + 1 < KR) *reinterpret_cast<float2 *>(yr + 2 * a) = acc[a][b];
-            else if (r < KR) yr[2 * a] = acc[a][b].x;
+            if (r + 1 < KR) *reinterpret_cast<float2 *>(yr + 2 * a) = acc[a][bb];
+            else if (r < KR) yr[2 * a] = acc[a][bb].x;
           }
         }
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&x_empty[b]);
       }
-      __syncthreads();  // this chunk's buffer may be refilled by the next iteration
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(t_empty);  // this warp no longer reads Ts
   }
 }
 
@@ -434,15 +477,15 @@ size_t m2l_gemm_smem(int p) {
   const int KR = 2 * nc_of(p);
   const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
   const int XKS = ((Kpad >> 2) & 1) ? Kpad : Kpad + 4;
-  return (size_t)(Kpad * Rpad + 2 * M2L_XCH * XKS) * sizeof(float) + 4 * sizeof(unsigned long long);
+  return (size_t)(Kpad * Rpad + 2 * M2L_XCH * XKS) * sizeof(float) + 8 * sizeof(unsigned long long);
 }
 size_t m2l_T_floats(int p) {
   const int KR = 2 * nc_of(p);
   return (size_t)((KR + 3) & ~3) * (((KR + 11) / 12) * 12);
 }
 bool m2l_gemm_supported(int p) {
-  const int KR = 2 * nc_of(p), nthr = ((KR + 11) / 12) * 16;
-  return m2l_gemm_smem(p) <= 227 * 1024 && nthr <= 256 && nthr >= M2L_XCH;
+  const int KR = 2 * nc_of(p), nthr = (((KR + 11) / 12) * 16 + 31) / 32 * 32 + 32;
+  return m2l_gemm_smem(p) <= 227 * 1024 && nthr <= 288;
 }
 int m2l_y_stride(int p) { return (2 * nc_of(p) + 3) & ~3; }
 
@@ -458,7 +501,7 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
                                       64, st);
   if (e) return e;
-  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.flag);
+  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.src, W.flag, W.ssrc);
   bytes = 0;
   e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, W.flag, W.cid, npairs, st);
   if (e) return e;
@@ -499,9 +542,9 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
       configured = smem;
     }
     const int KR = 2 * nc_of(p);
-    const int nthr = ((KR + 11) / 12) * 16;
+    const int nthr = (((KR + 11) / 12) * 16 + 31) / 32 * 32 + 32;  // consumer warps + producer
     const int per_sm = (int)((227 * 1024) / smem) < 2 ? 1 : 2;
-    k_m2l_gemm<<<148 * per_sm, nthr, smem, st>>>(p, W.items, W.counters, W.sidx, W.src, W.Tg,
+    k_m2l_gemm<<<148 * per_sm, nthr, smem, st>>>(p, W.items, W.counters, W.sidx, W.ssrc, W.Tg,
                                                   reinterpret_cast<const float *>(M), W.Y);
   }
   {

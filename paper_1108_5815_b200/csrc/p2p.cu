@@ -3,107 +3,245 @@
 //
 //   phi_i  += sum_j q_j / r_ij          grad_i += sum_j q_j (x_j - x_i) / r_ij^3
 //
-// Target-parallel: one lane per target particle, sources staged through shared memory in tiles
-// and read back as broadcast LDS.128; rsqrt on the MUFU pipe, the rest FP32 FMA. Pairs with r = 0
-// (the particle itself, coincident particles) contribute nothing; they only occur when the source
-// cell IS the target leaf, so only that case pays for the mask. Accumulation is tile-blocked:
-// each tile's sum is formed separately and then added to the running total (keeps the FP32 error
-// of long sums at ~1e-7, SURVEY §8(a) a12 accumulation rule).
+// Target-parallel, one warp per (target leaf, chunk of <= 64 targets). Every lane holds TWO
+// targets in packed float2 registers, so each source costs 13 packed FP32 instructions
+// (FADD2/FMUL2/FFMA2 with the source value as the broadcast operand) + 2 MUFU.RSQ for 2 pairs.
+// Small leaves use a 2-D lane mapping: G target groups x S = 32/G source slices (slice h takes
+// sources h, h+S, ...), reduced with shuffles at the end. The sources of the leaf's P2P list and
+// of its ancestors' lists (a P2P pair with a non-leaf target applies to every particle under it)
+// are concatenated into shared-memory tiles of P2P_TILE particles; the target leaf itself is
+// processed in its own masked tiles (r = 0 pairs: the particle itself and coincident particles,
+// which can only share a leaf). Accumulation is tile-blocked (per-tile partial sums added to the
+// running total) to keep the FP32 error of long sums near 1e-7.
 #include "common.cuh"
 #include "kernels.cuh"
 
 #define P2P_TILE 128
 #define P2P_WARPS 8
 
-template <bool MASK>
-__device__ __forceinline__ void p2p_tile(const float4 *__restrict__ sp, int ns, float4 t,
-                                         float &phi, float &gx, float &gy, float &gz) {
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 8
-  for (int j = 0; j < ns; ++j) {
-    const float4 s = sp[j];
-    const float dx = s.x - t.x, dy = s.y - t.y, dz = s.z - t.z;
-    const float r2 = dx * dx + dy * dy + dz * dz;
-    float rinv = rsqrtf(r2);
-    if (MASK) rinv = r2 > 0.f ? rinv : 0.f;
-    const float qr = s.w * rinv;
-    const float qr3 = qr * rinv * rinv;
-    a0 += qr;
-    a1 += qr3 * dx;
-    a2 += qr3 * dy;
-    a3 += qr3 * dz;
-  }
-  phi += a0;
-  gx += a1;
-  gy += a2;
-  gz += a3;
+__device__ __forceinline__ float rsqrt_approx(float x) {  // MUFU.RSQ, no denormal fix-up
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
-// Warp per (leaf, chunk of 32 targets); sources = P2P lists of the leaf and all its ancestors
-// (a P2P pair with a non-leaf target applies to every particle under it).
-__global__ void __launch_bounds__(P2P_WARPS * 32) k_p2p_leaves(const int *__restrict__ leaves,
+// Packed f32x2 arithmetic on 64-bit registers (PTX add/mul/fma.rn.f32x2, sm_100+): keeping the
+// pairs in .b64 values makes the register allocator hold them in aligned register pairs, so the
+// compiler emits FADD2/FMUL2/FFMA2 without re-pairing MOVs.
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x pk(float a, float b) {
+  f2x r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk(f2x v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+  f2x d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+  f2x d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+  f2x d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// one source against the lane's two targets (tx = -x of the two targets)
+__device__ __forceinline__ void ld_src(const float4 *sp, int j, f2x &xx, f2x &yy, f2x &zz,
+                                       f2x &qq) {
+  const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(sp + 2 * j);
+  const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(sp + 2 * j + 1);
+  xx = a.x;
+  yy = a.y;
+  zz = b.x;
+  qq = b.y;
+}
+__device__ __forceinline__ void st_src(float4 *sp, int j, float4 v) {
+  sp[2 * j] = make_float4(v.x, v.x, v.y, v.y);
+  sp[2 * j + 1] = make_float4(v.z, v.z, v.w, v.w);
+}
+
+template <bool MASK>
+__device__ __forceinline__ void p2p_pair2(const float4 *sp, int j, const f2x tx, const f2x ty,
+                                          const f2x tz, f2x &ph, f2x &gx, f2x &gy, f2x &gz) {
+  f2x sx, sy, sz, sq;
+  ld_src(sp, j, sx, sy, sz, sq);
+  const f2x dx = add2(sx, tx);
+  const f2x dy = add2(sy, ty);
+  const f2x dz = add2(sz, tz);
+  f2x r2 = mul2(dx, dx);
+  r2 = fma2(dy, dy, r2);
+  r2 = fma2(dz, dz, r2);
+  const float2 r2f = upk(r2);
+  float rx = rsqrt_approx(r2f.x), ry = rsqrt_approx(r2f.y);
+  if (MASK) {
+    rx = r2f.x > 0.f ? rx : 0.f;
+    ry = r2f.y > 0.f ? ry : 0.f;
+  }
+  const f2x ri = pk(rx, ry);
+  const f2x qr = mul2(sq, ri);
+  ph = add2(ph, qr);
+  const f2x qr3 = mul2(qr, mul2(ri, ri));
+  gx = fma2(dx, qr3, gx);
+  gy = fma2(dy, qr3, gy);
+  gz = fma2(dz, qr3, gz);
+}
+
+template <bool MASK>
+__device__ __forceinline__ void p2p_tile2(const float4 *__restrict__ sp, int ns, int h, int S,
+                                          f2x tx, f2x ty, f2x tz, f2x acc[4]) {
+  f2x ph = 0ull, gx = 0ull, gy = 0ull, gz = 0ull;  // +0.0f pairs
+  int j = h;
+  for (; j + 3 * S < ns; j += 4 * S) {
+    p2p_pair2<MASK>(sp, j, tx, ty, tz, ph, gx, gy, gz);
+    p2p_pair2<MASK>(sp, j + S, tx, ty, tz, ph, gx, gy, gz);
+    p2p_pair2<MASK>(sp, j + 2 * S, tx, ty, tz, ph, gx, gy, gz);
+    p2p_pair2<MASK>(sp, j + 3 * S, tx, ty, tz, ph, gx, gy, gz);
+  }
+  for (; j < ns; j += S) p2p_pair2<MASK>(sp, j, tx, ty, tz, ph, gx, gy, gz);
+  acc[0] = add2(acc[0], ph);
+  acc[1] = add2(acc[1], gx);
+  acc[2] = add2(acc[2], gy);
+  acc[3] = add2(acc[3], gz);
+}
+
+__global__ void __launch_bounds__(P2P_WARPS * 32, 2) k_p2p_leaves(const int *__restrict__ leaves,
                                                                int nleaves, CellsView C,
                                                                ListsView Ls,
                                                                const float4 *__restrict__ pos,
-                                                               float4 *__restrict__ acc) {
-  __shared__ float4 sh[P2P_WARPS][P2P_TILE];
+                                                               float4 *__restrict__ acc_out,
+                                                               float m1) {
+  __shared__ float4 sh[P2P_WARPS][2 * P2P_TILE];
+  __shared__ float4 shq[P2P_WARPS][64];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float4 *sp = sh[wib];
+  float4 *tq = shq[wib];
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int li = gw; li < nleaves; li += nw) {
     const int leaf = leaves[li];
     const int tb = C.beg[leaf], tn = C.cnt[leaf];
-    for (int c0 = 0; c0 < tn; c0 += WARP) {
-      const bool valid = c0 + lane < tn;
-      const int i = tb + c0 + lane;
-      const float4 t = valid ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-      float phi = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
+    for (int c0 = 0; c0 < tn; c0 += 64) {
+      const int nt = min(64, tn - c0);
+      // G target groups (2 targets each) x S source slices
+      const int G = nt <= 8 ? 4 : nt <= 16 ? 8 : nt <= 32 ? 16 : 32;
+      const int S = 32 / G;
+      const int grp = lane % G, h = lane / G;
+      const int i0 = c0 + 2 * grp, i1 = i0 + 1;
+      const float4 t0 = i0 < tn ? pos[tb + i0] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 t1 = i1 < tn ? pos[tb + i1] : t0;
+      // -x of the two targets as register pairs, round-tripped through shared memory so that
+      // they are loaded as 64-bit values (no per-use re-pairing MOVs)
+      __syncwarp();
+      tq[2 * lane] = make_float4(m1 * t0.x, m1 * t1.x, m1 * t0.y, m1 * t1.y);
+      tq[2 * lane + 1] = make_float4(m1 * t0.z, m1 * t1.z, 0.f, 0.f);
+      __syncwarp();
+      const ulonglong2 ta = *reinterpret_cast<const ulonglong2 *>(&tq[2 * lane]);
+      const ulonglong2 tb2 = *reinterpret_cast<const ulonglong2 *>(&tq[2 * lane + 1]);
+      const f2x tx = ta.x, ty = ta.y, tz = tb2.x;
+      f2x acc[4] = {0ull, 0ull, 0ull, 0ull};
+      // (1) the leaf itself, masked
+      for (int j0 = 0; j0 < tn; j0 += P2P_TILE) {
+        const int n = min(P2P_TILE, tn - j0);
+        __syncwarp();
+        for (int j = lane; j < n; j += 32) st_src(sp, j, pos[tb + j0 + j]);
+        __syncwarp();
+        p2p_tile2<true>(sp, n, h, S, tx, ty, tz, acc);
+      }
+      // (2) every other source cell of the leaf's and its ancestors' P2P lists, concatenated
+      int fill = 0;
       for (int a = leaf; a >= 0; a = C.parent[a]) {
         const int off = Ls.off[2][a], ncell = Ls.cnt[2][a];
         for (int e = 0; e < ncell; ++e) {
           const int s = Ls.src[2][off + e];
-          const int sb = C.beg[s], sn = C.cnt[s];
-          const bool self = (s == leaf);
-          for (int j0 = 0; j0 < sn; j0 += P2P_TILE) {
-            const int nt = min(P2P_TILE, sn - j0);
-            __syncwarp();
-            for (int j = lane; j < nt; j += WARP) sp[j] = pos[sb + j0 + j];
-            __syncwarp();
-            if (self)
-              p2p_tile<true>(sp, nt, t, phi, gx, gy, gz);
-            else
-              p2p_tile<false>(sp, nt, t, phi, gx, gy, gz);
+          if (s == leaf) continue;
+          int sb = C.beg[s], sn = C.cnt[s];
+          while (sn > 0) {
+            const int take = min(sn, P2P_TILE - fill);
+            for (int j = lane; j < take; j += 32) st_src(sp, fill + j, pos[sb + j]);
+            fill += take;
+            sb += take;
+            sn -= take;
+            if (fill == P2P_TILE) {
+              __syncwarp();
+              p2p_tile2<false>(sp, fill, h, S, tx, ty, tz, acc);
+              __syncwarp();
+              fill = 0;
+            }
           }
         }
       }
-      if (valid) acc[i] = make_float4(phi, gx, gy, gz);
+      if (fill > 0) {
+        __syncwarp();
+        p2p_tile2<false>(sp, fill, h, S, tx, ty, tz, acc);
+      }
+      // reduce the S source slices (lanes grp, grp + G, ...), fixed butterfly order
+      float2 r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = upk(acc[k]);
+      for (int o = G; o < 32; o <<= 1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          r[k].x += __shfl_xor_sync(0xffffffffu, r[k].x, o);
+          r[k].y += __shfl_xor_sync(0xffffffffu, r[k].y, o);
+        }
+      }
+      if (h == 0) {
+        if (i0 < tn) acc_out[tb + i0] = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
+        if (i1 < tn) acc_out[tb + i1] = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
+      }
+      __syncwarp();
     }
   }
 }
 
-// FMM_DIRECT: all N targets against all N sources in caller order (no tree). Block of 256 targets,
-// source tiles of 256 staged by the whole block.
+// FMM_DIRECT: all N targets against all N sources in caller order (no tree). Block of 256
+// threads = 512 targets (2 per thread), source tiles of 512 staged by the whole block.
 __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__restrict__ pos,
                                                     float *__restrict__ phi_out,
-                                                    float *__restrict__ grad_out) {
-  __shared__ float4 sh[256];
-  for (int64_t base = (int64_t)blockIdx.x * 256; base < n; base += (int64_t)gridDim.x * 256) {
-    const int64_t i = base + threadIdx.x;
-    const bool valid = i < n;
-    const float4 t = valid ? pos[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    float phi = 0.f, gx = 0.f, gy = 0.f, gz = 0.f;
-    for (int64_t j0 = 0; j0 < n; j0 += 256) {
-      const int nt = (int)min((int64_t)256, n - j0);
+                                                    float *__restrict__ grad_out, float m1) {
+  __shared__ float4 sh[2 * 512];
+  __shared__ float4 tq[2 * 256];
+  for (int64_t base = (int64_t)blockIdx.x * 512; base < n; base += (int64_t)gridDim.x * 512) {
+    const int64_t i0 = base + 2 * threadIdx.x, i1 = i0 + 1;
+    const float4 t0 = i0 < n ? pos[i0] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 t1 = i1 < n ? pos[i1] : t0;
+    __syncthreads();
+    tq[2 * threadIdx.x] = make_float4(m1 * t0.x, m1 * t1.x, m1 * t0.y, m1 * t1.y);
+    tq[2 * threadIdx.x + 1] = make_float4(m1 * t0.z, m1 * t1.z, 0.f, 0.f);
+    const ulonglong2 ta = *reinterpret_cast<const ulonglong2 *>(&tq[2 * threadIdx.x]);
+    const ulonglong2 tb2 = *reinterpret_cast<const ulonglong2 *>(&tq[2 * threadIdx.x + 1]);
+    const f2x tx = ta.x, ty = ta.y, tz = tb2.x;
+    f2x acc[4] = {0ull, 0ull, 0ull, 0ull};
+    for (int64_t j0 = 0; j0 < n; j0 += 512) {
+      const int nt = (int)min((int64_t)512, n - j0);
       __syncthreads();
-      if (threadIdx.x < nt) sh[threadIdx.x] = pos[j0 + threadIdx.x];
+      for (int j = threadIdx.x; j < nt; j += 256) st_src(sh, j, pos[j0 + j]);
       __syncthreads();
-      p2p_tile<true>(sh, nt, t, phi, gx, gy, gz);
+      p2p_tile2<true>(sh, nt, 0, 1, tx, ty, tz, acc);
     }
-    if (valid) {
-      phi_out[i] = phi;
-      grad_out[3 * i + 0] = gx;
-      grad_out[3 * i + 1] = gy;
-      grad_out[3 * i + 2] = gz;
+    float2 r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r[k] = upk(acc[k]);
+    if (i0 < n) {
+      phi_out[i0] = r[0].x;
+      grad_out[3 * i0 + 0] = r[1].x;
+      grad_out[3 * i0 + 1] = r[2].x;
+      grad_out[3 * i0 + 2] = r[3].x;
+    }
+    if (i1 < n) {
+      phi_out[i1] = r[0].y;
+      grad_out[3 * i1 + 0] = r[1].y;
+      grad_out[3 * i1 + 1] = r[2].y;
+      grad_out[3 * i1 + 2] = r[3].y;
     }
   }
 }
@@ -113,12 +251,12 @@ void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls
   int64_t b = (nleaves + P2P_WARPS - 1) / P2P_WARPS;
   if (b > 148 * 8) b = 148 * 8;
   if (b < 1) b = 1;
-  k_p2p_leaves<<<(int)b, P2P_WARPS * 32, 0, st>>>(leaves, nleaves, C, Ls, pos, acc);
+  k_p2p_leaves<<<(int)b, P2P_WARPS * 32, 0, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f);
 }
 
 void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cudaStream_t st) {
-  int64_t b = (n + 255) / 256;
+  int64_t b = (n + 511) / 512;
   if (b > 148 * 64) b = 148 * 64;
   if (b < 1) b = 1;
-  k_p2p_direct<<<(int)b, 256, 0, st>>>(n, pos, phi, grad);
+  k_p2p_direct<<<(int)b, 256, 0, st>>>(n, pos, phi, grad, -1.0f);
 }
