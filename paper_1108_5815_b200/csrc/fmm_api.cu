@@ -399,7 +399,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(h->m2l_flag.ensure(np));
     CK(h->m2l_cid.ensure(np));
     CK(h->m2l_cstart.ensure((size_t)np + 1));
-    CK(h->m2l_counters.ensure(4));
+    CK(h->m2l_counters.ensure(8));
     CK(h->m2l_items.ensure((size_t)np + 1));
     CK(h->m2l_small.ensure(np));
     CK(h->m2l_Y.ensure((size_t)np * m2l_y_stride(p)));
@@ -444,7 +444,8 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   }
   record(h, EV_M2L);
   // a12 P2P (writes acc), a11 M2P (adds)
-  launch_p2p_leaves(h->leaves.p, h->nleaves, h->cells(), h->lists(), h->pos.p, h->acc.p, st);
+  launch_p2p_leaves(h->leaves.p, h->nleaves, h->cells(), h->lists(), h->pos.p, h->acc.p,
+                    h->d_small + 12, st);
   CKL();
   record(h, EV_P2P);
   if (h->ntask[FMM_KIND_M2P] > 0) {

@@ -95,7 +95,7 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
 
 // ---- p2p.cu ----
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                       const float4 *pos, float4 *acc, cudaStream_t st);
+                       const float4 *pos, float4 *acc, int *counter, cudaStream_t st);
 void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cudaStream_t st);
 
 // ---- synthetic batches for the kernel pre-calculation (autotune.cu) ----

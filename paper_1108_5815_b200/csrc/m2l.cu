@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
                                                      const unsigned *__restrict__ ssrc,
                                                      const float *__restrict__ Tg,
                                                      const float *__restrict__ M,
-                                                     float *__restrict__ Y) {
+                                                     float *__restrict__ Y, int *queue) {
   extern __shared__ __align__(128) float sh_gemm[];
   const int NC = nc_of(p), KR = 2 * NC;
   const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
   unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xs0 + 2 * M2L_XCH * XKS);
   unsigned long long *t_full = &bars[0], *t_empty = &bars[1];
   unsigned long long *x_full = &bars[2], *x_empty = &bars[4];  // [2] each
+  volatile int *item_slot = reinterpret_cast<volatile int *>(&bars[6]);  // [2]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned tbytes = (unsigned)(Kpad * Rpad * sizeof(float));
   const unsigned rbytes = (unsigned)(Kpad * sizeof(float));
@@ -306,7 +307,18 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
 
   if (warp == ncw) {  // ---------------- producer ----------------
     int g = 0, ii = 0;
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ii) {
+    for (;; ++ii) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(&queue[0], 1);  // dynamic item queue
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (lane == 0) item_slot[ii & 1] = it;         // hand the item index to the consumers
+      if (it >= nitems) {
+        if (lane == 0) {
+          fence_proxy_async();
+          mbar_expect_tx(t_full, 0);  // release the consumers with a sentinel phase
+        }
+        break;
+      }
       const int4 item = items[it];
       const int pos0 = item.x, cnt = item.y, gid = item.w;
       if (ii > 0) mbar_wait(t_empty, (ii - 1) & 1);
@@ -342,10 +354,12 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
   const int rg = tid >> 4, cg = tid & 15;
   const bool active = tid < ncons;
   int g = 0, ii = 0;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++ii) {
+  for (;; ++ii) {
+    mbar_wait(t_full, ii & 1);
+    const int it = item_slot[ii & 1];
+    if (it >= nitems) break;
     const int4 item = items[it];
     const int pos0 = item.x, cnt = item.y;
-    mbar_wait(t_full, ii & 1);
     for (int c0 = 0; c0 < cnt; c0 += M2L_XCH, ++g) {
       const int b = g & 1, use = g >> 1;
       const int ncol = min(M2L_XCH, cnt - c0);
@@ -544,8 +558,10 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
     const int KR = 2 * nc_of(p);
     const int nthr = (((KR + 11) / 12) * 16 + 31) / 32 * 32 + 32;  // consumer warps + producer
     const int per_sm = (int)((227 * 1024) / smem) < 2 ? 1 : 2;
+    cudaMemsetAsync(W.counters + 4, 0, sizeof(int), st);
     k_m2l_gemm<<<148 * per_sm, nthr, smem, st>>>(p, W.items, W.counters, W.sidx, W.ssrc, W.Tg,
-                                                  reinterpret_cast<const float *>(M), W.Y);
+                                                  reinterpret_cast<const float *>(M), W.Y,
+                                                  W.counters + 4);
   }
   {
     const int nI = (2 * p + 1) * (2 * p + 1), nM = (p + 1) * (p + 1);

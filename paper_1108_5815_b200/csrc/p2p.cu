@@ -3,7 +3,7 @@
 //
 //   phi_i  += sum_j q_j / r_ij          grad_i += sum_j q_j (x_j - x_i) / r_ij^3
 //
-// Target-parallel, one warp per (target leaf, chunk of <= 64 targets). Every lane holds TWO
+// Target-parallel, one warp per (target leaf, chunk of <= 32 targets). Every lane holds TWO
 // targets in packed float2 registers, so each source costs 13 packed FP32 instructions
 // (FADD2/FMUL2/FFMA2 with the source value as the broadcast operand) + 2 MUFU.RSQ for 2 pairs.
 // Small leaves use a 2-D lane mapping: G target groups x S = 32/G source slices (slice h takes
@@ -17,7 +17,7 @@
 #include "kernels.cuh"
 
 #define P2P_TILE 128
-#define P2P_WARPS 8
+#define P2P_WARPS 4
 
 __device__ __forceinline__ float rsqrt_approx(float x) {  // MUFU.RSQ, no denormal fix-up
   float y;
@@ -114,32 +114,92 @@ __device__ __forceinline__ void p2p_tile2(const float4 *__restrict__ sp, int ns,
   acc[3] = add2(acc[3], gz);
 }
 
-__global__ void __launch_bounds__(P2P_WARPS * 32, 2) k_p2p_leaves(const int *__restrict__ leaves,
+// raw-float4 tile variant: source value as the broadcast operand of the packed ops
+template <bool MASK>
+__device__ __forceinline__ void p2p_raw(const float4 sv, const f2x tx, const f2x ty, const f2x tz,
+                                        f2x &ph, f2x &gx, f2x &gy, f2x &gz) {
+  const f2x dx = add2(pk(sv.x, sv.x), tx);
+  const f2x dy = add2(pk(sv.y, sv.y), ty);
+  const f2x dz = add2(pk(sv.z, sv.z), tz);
+  f2x r2 = mul2(dx, dx);
+  r2 = fma2(dy, dy, r2);
+  r2 = fma2(dz, dz, r2);
+  const float2 r2f = upk(r2);
+  float rx = rsqrt_approx(r2f.x), ry = rsqrt_approx(r2f.y);
+  if (MASK) {
+    rx = r2f.x > 0.f ? rx : 0.f;
+    ry = r2f.y > 0.f ? ry : 0.f;
+  }
+  const f2x ri = pk(rx, ry);
+  const f2x qr = mul2(pk(sv.w, sv.w), ri);
+  ph = add2(ph, qr);
+  const f2x qr3 = mul2(qr, mul2(ri, ri));
+  gx = fma2(dx, qr3, gx);
+  gy = fma2(dy, qr3, gy);
+  gz = fma2(dz, qr3, gz);
+}
+
+template <bool MASK>
+__device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int ns, int h, int S,
+                                             f2x tx, f2x ty, f2x tz, f2x acc[4]) {
+  f2x ph = 0ull, gx = 0ull, gy = 0ull, gz = 0ull;
+  int j = h;
+  for (; j + 3 * S < ns; j += 4 * S) {
+    const float4 s0 = sp[j], s1 = sp[j + S], s2 = sp[j + 2 * S], s3 = sp[j + 3 * S];
+    p2p_raw<MASK>(s0, tx, ty, tz, ph, gx, gy, gz);
+    p2p_raw<MASK>(s1, tx, ty, tz, ph, gx, gy, gz);
+    p2p_raw<MASK>(s2, tx, ty, tz, ph, gx, gy, gz);
+    p2p_raw<MASK>(s3, tx, ty, tz, ph, gx, gy, gz);
+  }
+  for (; j < ns; j += S) p2p_raw<MASK>(sp[j], tx, ty, tz, ph, gx, gy, gz);
+  acc[0] = add2(acc[0], ph);
+  acc[1] = add2(acc[1], gx);
+  acc[2] = add2(acc[2], gy);
+  acc[3] = add2(acc[3], gz);
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+#define P2P_RANGES 512  // per-warp list of source particle ranges (processed in batches)
+
+__global__ void __launch_bounds__(P2P_WARPS * 32, 4) k_p2p_leaves(const int *__restrict__ leaves,
                                                                int nleaves, CellsView C,
                                                                ListsView Ls,
                                                                const float4 *__restrict__ pos,
                                                                float4 *__restrict__ acc_out,
-                                                               float m1) {
-  __shared__ float4 sh[P2P_WARPS][2 * P2P_TILE];
-  __shared__ float4 shq[P2P_WARPS][64];
+                                                               float m1, int *next_leaf) {
+  __shared__ __align__(16) float4 sh[P2P_WARPS][2][P2P_TILE];
+  __shared__ __align__(16) float4 shq[P2P_WARPS][64];  // 2 float4 per lane (target pairs)
+  __shared__ int2 shr[P2P_WARPS][P2P_RANGES];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float4 *sp = sh[wib];
   float4 *tq = shq[wib];
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int li = gw; li < nleaves; li += nw) {
+  int2 *rng = shr[wib];
+  for (;;) {
+    int li = 0;
+    if (lane == 0) li = atomicAdd(next_leaf, 1);  // dynamic leaf queue (load balance)
+    li = __shfl_sync(0xffffffffu, li, 0);
+    if (li >= nleaves) break;
     const int leaf = leaves[li];
     const int tb = C.beg[leaf], tn = C.cnt[leaf];
-    for (int c0 = 0; c0 < tn; c0 += 64) {
-      const int nt = min(64, tn - c0);
-      // G target groups (2 targets each) x S source slices
-      const int G = nt <= 8 ? 4 : nt <= 16 ? 8 : nt <= 32 ? 16 : 32;
+    // ancestors of the leaf (each may carry a P2P list)
+    int anc[FMM_LEVELS + 1], na = 0;
+    for (int a = leaf; a >= 0 && na <= FMM_LEVELS; a = C.parent[a]) anc[na++] = a;
+    for (int c0 = 0; c0 < tn; c0 += 32) {
+      const int nt = min(32, tn - c0);
+      const int G = nt <= 8 ? 4 : nt <= 16 ? 8 : 16;
       const int S = 32 / G;
       const int grp = lane % G, h = lane / G;
       const int i0 = c0 + 2 * grp, i1 = i0 + 1;
       const float4 t0 = i0 < tn ? pos[tb + i0] : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 t1 = i1 < tn ? pos[tb + i1] : t0;
-      // -x of the two targets as register pairs, round-tripped through shared memory so that
-      // they are loaded as 64-bit values (no per-use re-pairing MOVs)
       __syncwarp();
       tq[2 * lane] = make_float4(m1 * t0.x, m1 * t1.x, m1 * t0.y, m1 * t1.y);
       tq[2 * lane + 1] = make_float4(m1 * t0.z, m1 * t1.z, 0.f, 0.f);
@@ -148,40 +208,70 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, 2) k_p2p_leaves(const int *__r
       const ulonglong2 tb2 = *reinterpret_cast<const ulonglong2 *>(&tq[2 * lane + 1]);
       const f2x tx = ta.x, ty = ta.y, tz = tb2.x;
       f2x acc[4] = {0ull, 0ull, 0ull, 0ull};
-      // (1) the leaf itself, masked
+      // (1) the leaf itself, masked (r = 0 pairs)
       for (int j0 = 0; j0 < tn; j0 += P2P_TILE) {
         const int n = min(P2P_TILE, tn - j0);
         __syncwarp();
-        for (int j = lane; j < n; j += 32) st_src(sp, j, pos[tb + j0 + j]);
+        for (int j = lane; j < n; j += 32) sh[wib][0][j] = pos[tb + j0 + j];
         __syncwarp();
-        p2p_tile2<true>(sp, n, h, S, tx, ty, tz, acc);
+        p2p_tile_raw<true>(sh[wib][0], n, h, S, tx, ty, tz, acc);
       }
-      // (2) every other source cell of the leaf's and its ancestors' P2P lists, concatenated
-      int fill = 0;
-      for (int a = leaf; a >= 0; a = C.parent[a]) {
-        const int off = Ls.off[2][a], ncell = Ls.cnt[2][a];
-        for (int e = 0; e < ncell; ++e) {
-          const int s = Ls.src[2][off + e];
-          if (s == leaf) continue;
-          int sb = C.beg[s], sn = C.cnt[s];
-          while (sn > 0) {
-            const int take = min(sn, P2P_TILE - fill);
-            for (int j = lane; j < take; j += 32) st_src(sp, fill + j, pos[sb + j]);
+      // (2) all other source cells of the P2P lists of the leaf and its ancestors, as particle
+      // ranges collected into shared memory (batches of P2P_RANGES), streamed by cp.async into a
+      // double-buffered tile: tile k+1 is in flight while tile k is computed
+      int ai = 0, ae = 0;  // resume point: ancestor index, list position
+      while (ai < na) {
+        int nr = 0;
+        while (ai < na && nr + 32 <= P2P_RANGES) {
+          const int a = anc[ai];
+          const int off = Ls.off[2][a], ncell = Ls.cnt[2][a];
+          if (ae >= ncell) {
+            ++ai;
+            ae = 0;
+            continue;
+          }
+          const int e = ae + lane;
+          int2 r = make_int2(0, 0);
+          if (e < ncell) {
+            const int s = Ls.src[2][off + e];
+            if (s != leaf) r = make_int2(C.beg[s], C.cnt[s]);
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, r.y > 0);
+          if (r.y > 0) rng[nr + __popc(bal & ((1u << lane) - 1u))] = r;
+          nr += __popc(bal);
+          ae += 32;
+        }
+        __syncwarp();
+        // stream the ranges through the two tile buffers
+        int ri = 0, roff = 0, buf = 0;
+        auto issue = [&](int b) -> int {  // fill tile b from the range cursor; returns its size
+          int fill = 0;
+          while (ri < nr && fill < P2P_TILE) {
+            const int2 r = rng[ri];
+            const int take = min(r.y - roff, P2P_TILE - fill);
+            for (int j = lane; j < take; j += 32) cp_async16(&sh[wib][b][fill + j], &pos[r.x + roff + j]);
             fill += take;
-            sb += take;
-            sn -= take;
-            if (fill == P2P_TILE) {
-              __syncwarp();
-              p2p_tile2<false>(sp, fill, h, S, tx, ty, tz, acc);
-              __syncwarp();
-              fill = 0;
+            roff += take;
+            if (roff == r.y) {
+              ++ri;
+              roff = 0;
             }
           }
+          cp_async_commit();
+          return fill;
+        };
+        int cur = issue(0);
+        while (cur > 0) {
+          const int nxt = issue(buf ^ 1);
+          cp_async_wait1();  // tile `buf` has landed
+          __syncwarp();
+          p2p_tile_raw<false>(sh[wib][buf], cur, h, S, tx, ty, tz, acc);
+          __syncwarp();
+          buf ^= 1;
+          cur = nxt;
         }
-      }
-      if (fill > 0) {
+        cp_async_wait0();
         __syncwarp();
-        p2p_tile2<false>(sp, fill, h, S, tx, ty, tz, acc);
       }
       // reduce the S source slices (lanes grp, grp + G, ...), fixed butterfly order
       float2 r[4];
@@ -247,11 +337,20 @@ __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__r
 }
 
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                       const float4 *pos, float4 *acc, cudaStream_t st) {
-  int64_t b = (nleaves + P2P_WARPS - 1) / P2P_WARPS;
-  if (b > 148 * 8) b = 148 * 8;
-  if (b < 1) b = 1;
-  k_p2p_leaves<<<(int)b, P2P_WARPS * 32, 0, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f);
+                       const float4 *pos, float4 *acc, int *counter, cudaStream_t st) {
+  static int resident = 0;
+  if (!resident) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p2p_leaves, P2P_WARPS * 32, 0);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    resident = (per_sm > 0 ? per_sm : 1) * nsm;
+  }
+  const int need = (nleaves + P2P_WARPS - 1) / P2P_WARPS;
+  const int b = need < resident ? (need > 0 ? need : 1) : resident;
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  k_p2p_leaves<<<b, P2P_WARPS * 32, 0, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f, counter);
 }
 
 void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cudaStream_t st) {
