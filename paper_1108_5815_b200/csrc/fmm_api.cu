@@ -80,6 +80,7 @@ struct fmm_ctx {
   DBuf<unsigned> idx_in, perm;
   DBuf<float4> pos, acc;
   DBuf<char> cub_tmp;
+  DBuf<float> host_stage;
   // small device structs
   RootInfo *d_root = nullptr;
   unsigned *d_mm = nullptr;
@@ -92,7 +93,7 @@ struct fmm_ctx {
   DBuf<int4> cgrid;
   DBuf<float4> cgeo;
   DBuf<uint64_t> cprefix;
-  DBuf<int> nch, excl, leafflag, leaves;
+  DBuf<int> nch, excl, leafflag, leaves, bnd;
   DBuf<int2> crange;
   std::vector<int> level_off, level_cnt;
   int ncells = 0, nleaves = 0, depth = 0;
@@ -236,8 +237,10 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
     CK(h->nch.ensure(nl));
     CK(h->excl.ensure(nl));
     CK(h->crange.ensure((size_t)8 * nl));
+    CK(h->bnd.ensure((size_t)8 * nl));
     launch_split(c0, nl, level, h->ncrit, h->keys.p, h->cells(), h->cprefix.p, h->nch.p,
-                 h->crange.p, st);
+                 h->crange.p, h->bnd.p, st);
+    h->stats.launches += 1;
     CKL();
     if (int rc = cub_scan(h, h->nch.p, h->excl.p, nl)) return rc;
     launch_level_total(h->nch.p, h->excl.p, nl, h->d_small, st);
@@ -622,10 +625,10 @@ int fmm_destroy(fmm_t h) {
   if (!h) return FMM_OK;
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->keys_in.release(); h->keys.release(); h->idx_in.release(); h->perm.release();
-  h->pos.release(); h->acc.release(); h->cub_tmp.release();
+  h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release();
-  h->nch.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
+  h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
@@ -674,8 +677,8 @@ int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, 
   if (n < 0) return fail(h, FMM_E_INVALID, "n < 0");
   if (n == 0) return FMM_OK;
   if (!h_xyz || !h_q || !h_phi || !h_grad) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
-  float *d = nullptr;
-  CK(cudaMallocAsync(&d, sizeof(float) * 8 * (size_t)n, h->stream));
+  CK(h->host_stage.ensure(8 * (size_t)n));  // grow-only device staging (no per-call malloc)
+  float *d = h->host_stage.p;
   float *xyz = d, *q = d + 3 * n, *phi = d + 4 * n, *grad = d + 5 * n;
   int rc = FMM_OK;
   cudaError_t e = cudaMemcpyAsync(xyz, h_xyz, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, h->stream);
@@ -688,8 +691,6 @@ int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, 
     if (!e) e = cudaStreamSynchronize(h->stream);
     if (e) rc = fail(h, FMM_E_CUDA, "D2H: %s", cudaGetErrorString(e));
   }
-  cudaFreeAsync(d, h->stream);
-  cudaStreamSynchronize(h->stream);
   return rc;
 }
 

@@ -19,7 +19,7 @@ cudaError_t exclusive_scan(void *tmp, size_t &tmp_bytes, const int *in, int *out
 void launch_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64_t *prefix,
                       cudaStream_t st);
 void launch_split(int c0, int nl, int level, int ncrit, const uint64_t *keys, CellsView C,
-                  const uint64_t *prefix, int *nch, int2 *crange, cudaStream_t st);
+                  const uint64_t *prefix, int *nch, int2 *crange, int *bnd, cudaStream_t st);
 void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int *excl,
                  const int2 *crange, const RootInfo *root, CellsView C, uint64_t *prefix,
                  cudaStream_t st);

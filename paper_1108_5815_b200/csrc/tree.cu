@@ -49,13 +49,31 @@ __global__ void __launch_bounds__(256) k_bbox(const float *__restrict__ xyz,
     }
   }
   bad = __any_sync(0xffffffffu, bad);
-  if ((threadIdx.x & 31) == 0) {
+  // block reduction, then one atomic per block and value (not per warp: contention)
+  __shared__ unsigned slo[3][8], shi[3][8], sbad[8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      atomicMin(&mm[a], lo[a]);
-      atomicMax(&mm[3 + a], hi[a]);
+      slo[a][w] = lo[a];
+      shi[a][w] = hi[a];
     }
-    if (bad) atomicOr(&root->nonfinite, 1u);
+    sbad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int a = threadIdx.x;
+    unsigned l = slo[a][0], h = shi[a][0];
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      l = min(l, slo[a][k]);
+      h = max(h, shi[a][k]);
+    }
+    atomicMin(&mm[a], l);
+    atomicMax(&mm[3 + a], h);
+  } else if (threadIdx.x == 3) {
+    unsigned b = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b |= sbad[k];
+    if (b) atomicOr(&root->nonfinite, 1u);
   }
 }
 
@@ -159,31 +177,47 @@ __global__ void k_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64
 }
 
 // For each cell of level `level` (ids [c0, c0 + nl)): child sub-ranges by binary search on the
-// sorted keys. A cell is split iff count > ncrit and level < 21.
+// sorted keys. A cell is split iff count > ncrit and level < 21. One thread
+// per (cell, octant o): bnd[8k + o] = first index of the cell whose child prefix is >= base + o
+// (8 independent searches instead of 8 sequential ones per cell: short latency chains at the top
+// levels where there are few cells and long ranges).
 __global__ void __launch_bounds__(256) k_split(int c0, int nl, int level, int ncrit,
                                                const uint64_t *__restrict__ keys, CellsView C,
                                                const uint64_t *__restrict__ prefix,
-                                               int *__restrict__ nch, int2 *__restrict__ crange) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nl) return;
+                                               int *__restrict__ bnd) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= 8 * nl) return;
+  const int k = id >> 3, o = id & 7;
   const int c = c0 + k;
   const int b = C.beg[c], n = C.cnt[c];
+  if (!(n > ncrit && level < FMM_LEVELS)) {
+    bnd[id] = -1;
+    return;
+  }
+  const int shift = 3 * (FMM_LEVELS - (level + 1));
+  const uint64_t tgt = prefix[c] * 8 + (uint64_t)o;
+  int l = b, r = b + n;
+  while (l < r) {
+    const int m = (l + r) >> 1;
+    if ((keys[m] >> shift) < tgt) l = m + 1;
+    else r = m;
+  }
+  bnd[id] = l;
+}
+
+// child ranges from the 8 boundaries of each cell (non-empty octants, Morton order)
+__global__ void __launch_bounds__(256) k_split_ranges(int c0, int nl, CellsView C,
+                                                      const int *__restrict__ bnd,
+                                                      int *__restrict__ nch,
+                                                      int2 *__restrict__ crange) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nl) return;
   int cnt = 0;
-  if (n > ncrit && level < FMM_LEVELS) {
-    const int shift = 3 * (FMM_LEVELS - (level + 1));
-    const uint64_t base = prefix[c] * 8;
-    int lo = b;
+  if (bnd[8 * k] >= 0) {
+    const int c = c0 + k, end = C.beg[c] + C.cnt[c];
     for (int o = 0; o < 8; ++o) {
-      // first index >= lo whose child prefix exceeds base + o
-      int l = lo, r = b + n;
-      const uint64_t tgt = base + (uint64_t)o;
-      while (l < r) {
-        const int m = (l + r) >> 1;
-        if ((keys[m] >> shift) <= tgt) l = m + 1;
-        else r = m;
-      }
-      if (l > lo) crange[8 * k + cnt++] = make_int2(lo, (l - lo) | (o << 28));
-      lo = l;
+      const int lo = bnd[8 * k + o], hi = o < 7 ? bnd[8 * k + o + 1] : end;
+      if (hi > lo) crange[8 * k + cnt++] = make_int2(lo, (hi - lo) | (o << 28));
     }
   }
   nch[k] = cnt;
@@ -269,8 +303,9 @@ void launch_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64_t *pr
   k_root_cell<<<1, 1, 0, st>>>(n, root, C, prefix);
 }
 void launch_split(int c0, int nl, int level, int ncrit, const uint64_t *keys, CellsView C,
-                  const uint64_t *prefix, int *nch, int2 *crange, cudaStream_t st) {
-  k_split<<<(nl + 255) / 256, 256, 0, st>>>(c0, nl, level, ncrit, keys, C, prefix, nch, crange);
+                  const uint64_t *prefix, int *nch, int2 *crange, int *bnd, cudaStream_t st) {
+  k_split<<<(8 * nl + 255) / 256, 256, 0, st>>>(c0, nl, level, ncrit, keys, C, prefix, bnd);
+  k_split_ranges<<<(nl + 255) / 256, 256, 0, st>>>(c0, nl, C, bnd, nch, crange);
 }
 void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int *excl,
                  const int2 *crange, const RootInfo *root, CellsView C, uint64_t *prefix,
