@@ -313,10 +313,11 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
       it = __shfl_sync(0xffffffffu, it, 0);
       if (lane == 0) item_slot[ii & 1] = it;         // hand the item index to the consumers
       if (it >= nitems) {
-        if (lane == 0) {
-          fence_proxy_async();
-          mbar_expect_tx(t_full, 0);  // release the consumers with a sentinel phase
-        }
+        // release the consumers with a sentinel phase; first make sure the previous phase of
+        // t_full has completed (the consumers finished the previous item), otherwise this arrival
+        // would land in the still-pending phase
+        if (ii > 0) mbar_wait(t_empty, (ii - 1) & 1);
+        if (lane == 0) mbar_expect_tx(t_full, 0);
         break;
       }
       const int4 item = items[it];

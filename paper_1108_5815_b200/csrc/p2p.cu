@@ -139,23 +139,36 @@ __device__ __forceinline__ void p2p_raw(const float4 sv, const f2x tx, const f2x
   gz = fma2(dz, qr3, gz);
 }
 
-template <bool MASK>
-__device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int ns, int h, int S,
-                                             f2x tx, f2x ty, f2x tz, f2x acc[4]) {
+// S (source slices) is a compile-time constant so the four LDS.128 of an unrolled step use
+// immediate offsets (no IMAD address arithmetic on the FMA pipe)
+template <bool MASK, int S>
+__device__ __forceinline__ void p2p_tile_rawS(const float4 *__restrict__ sp, int ns, int h,
+                                              f2x tx, f2x ty, f2x tz, f2x acc[4]) {
   f2x ph = 0ull, gx = 0ull, gy = 0ull, gz = 0ull;
-  int j = h;
-  for (; j + 3 * S < ns; j += 4 * S) {
-    const float4 s0 = sp[j], s1 = sp[j + S], s2 = sp[j + 2 * S], s3 = sp[j + 3 * S];
+  const float4 *q = sp + h;
+  const float4 *end4 = sp + ns - 3 * S;  // q + 3S < sp + ns
+  for (; q < end4; q += 4 * S) {
+    const float4 s0 = q[0], s1 = q[S], s2 = q[2 * S], s3 = q[3 * S];
     p2p_raw<MASK>(s0, tx, ty, tz, ph, gx, gy, gz);
     p2p_raw<MASK>(s1, tx, ty, tz, ph, gx, gy, gz);
     p2p_raw<MASK>(s2, tx, ty, tz, ph, gx, gy, gz);
     p2p_raw<MASK>(s3, tx, ty, tz, ph, gx, gy, gz);
   }
-  for (; j < ns; j += S) p2p_raw<MASK>(sp[j], tx, ty, tz, ph, gx, gy, gz);
+  for (; q < sp + ns; q += S) p2p_raw<MASK>(q[0], tx, ty, tz, ph, gx, gy, gz);
   acc[0] = add2(acc[0], ph);
   acc[1] = add2(acc[1], gx);
   acc[2] = add2(acc[2], gy);
   acc[3] = add2(acc[3], gz);
+}
+template <bool MASK>
+__device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int ns, int h, int S,
+                                             f2x tx, f2x ty, f2x tz, f2x acc[4]) {
+  switch (S) {
+    case 1: p2p_tile_rawS<MASK, 1>(sp, ns, h, tx, ty, tz, acc); break;
+    case 2: p2p_tile_rawS<MASK, 2>(sp, ns, h, tx, ty, tz, acc); break;
+    case 4: p2p_tile_rawS<MASK, 4>(sp, ns, h, tx, ty, tz, acc); break;
+    default: p2p_tile_rawS<MASK, 8>(sp, ns, h, tx, ty, tz, acc); break;
+  }
 }
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {

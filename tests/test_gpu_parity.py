@@ -146,3 +146,18 @@ def test_host_entry_point(O, handles):
     phi, grad = f.evaluate_host(xyz, q)
     ref = O.fmm(xyz, q, 6, 0.5, 24, O.HYBRID, cost=COST)
     assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
+
+
+def test_repeated_evaluations_stable(handles):
+    # many evaluations of varying size through the same handle (pipelined M2L GEMM item queue,
+    # P2P leaf queue, grow-only buffers): results must stay bit-identical
+    f = handles(10, 0.4, 64, "fmm")
+    ref = {}
+    for it in range(3):
+        for n, dist in [(200_000, "uniform"), (50_000, "plummer"), (300_000, "mixed")]:
+            xyz, q = make_particles(n, dist, 21)
+            out = run(f, xyz, q)
+            if it == 0:
+                ref[n] = out
+            else:
+                assert np.array_equal(out[0], ref[n][0]) and np.array_equal(out[1], ref[n][1])
