@@ -127,6 +127,18 @@ int fmm_export_lists(fmm_t h, int64_t cap, int32_t *h_kind, int32_t *h_tlevel, u
 int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, double *h_origin3,
                     double *h_L);
 
+/* Multi-GPU building block (PAPER.md:89 spatial domain decomposition). With a
+ * partition set, fmm_evaluate builds the tree and the upward sweep over all n particles it is
+ * given but evaluates only the targets of Morton part `part` of `nparts`: the leaves whose first
+ * sorted particle index b satisfies floor(b * nparts / n) == part. Only those particles' entries of
+ * d_phi / d_grad are written. fmm_get_partition returns that part's sorted-order particle range
+ * [lo, hi) of the last evaluation; fmm_partition_indices writes the caller indices of those
+ * particles (int64, DEVICE buffer d_out of cap entries) so results can be routed to their owners.
+ * nparts = 1 (default) restores whole evaluation. Errors: FMM_E_INVALID, FMM_E_STATE. */
+int fmm_set_partition(fmm_t h, int nparts, int part);
+int fmm_get_partition(fmm_t h, int64_t *lo, int64_t *hi);
+int fmm_partition_indices(fmm_t h, int64_t *d_out, int64_t cap, int64_t *count_out);
+
 const char *fmm_strerror(int code);
 const char *fmm_last_error(fmm_t h);
 

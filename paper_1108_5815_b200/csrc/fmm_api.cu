@@ -97,6 +97,10 @@ struct fmm_ctx {
   DBuf<int2> crange;
   std::vector<int> level_off, level_cnt;
   int ncells = 0, nleaves = 0, depth = 0;
+  // Morton partition of the targets (multi-GPU); nparts = 1: everything
+  int nparts = 1, part = 0;
+  int tleaves_n = 0, part_lo = 0, part_hi = 0;
+  DBuf<int> tleaves;
   // expansions
   DBuf<float2> M, L;
   // M2L class batching
@@ -273,6 +277,26 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
   CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   h->nleaves = h->h_small[0];
+  // target leaves of this handle's partition
+  h->part_lo = 0;
+  h->part_hi = (int)n;
+  h->tleaves_n = h->nleaves;
+  if (h->nparts > 1) {
+    CK(h->tleaves.ensure(total));
+    launch_part_flags(total, h->cells(), n, h->nparts, h->part, h->leafflag.p, h->d_small + 8, st);
+    h->stats.launches += 1;
+    CKL();
+    if (int rc = cub_scan(h, h->leafflag.p, h->excl.p, total)) return rc;
+    launch_leaf_scatter(total, h->leafflag.p, h->excl.p, h->tleaves.p, st);
+    CKL();
+    launch_level_total(h->leafflag.p, h->excl.p, total, h->d_small, st);
+    CKL();
+    CK(cudaMemcpyAsync(h->h_small, h->d_small, 10 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h->tleaves_n = h->h_small[0];
+    h->part_lo = h->tleaves_n ? h->h_small[8] : 0;
+    h->part_hi = h->tleaves_n ? h->h_small[9] : 0;
+  }
   return FMM_OK;
 }
 
@@ -310,6 +334,8 @@ restart:
     A.mode = h->mode;
     A.stack_cap = h->stack_cap;
     A.grid_blocks = std::min(grid_blocks, (nt + warps_per_block - 1) / warps_per_block);
+    A.tlo = h->part_lo;
+    A.thi = h->part_hi;
     A.theta = h->theta;
     A.t_pp = h->cost.t_pp;
     A.t_mp = h->cost.t_mp;
@@ -447,12 +473,14 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   }
   record(h, EV_M2L);
   // a12 P2P (writes acc), a11 M2P (adds)
-  launch_p2p_leaves(h->leaves.p, h->nleaves, h->cells(), h->lists(), h->pos.p, h->acc.p,
+  const int *tl = h->nparts > 1 ? h->tleaves.p : h->leaves.p;
+  const int ntl = h->tleaves_n;
+  launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p,
                     h->d_small + 12, st);
   CKL();
   record(h, EV_P2P);
   if (h->ntask[FMM_KIND_M2P] > 0) {
-    launch_m2p(p, h->leaves.p, h->nleaves, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, st);
+    launch_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, st);
     CKL();
   }
   record(h, EV_M2P);
@@ -463,7 +491,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
       CKL();
     }
   }
-  launch_l2p(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, phi,
+  launch_l2p(p, tl, ntl, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, phi,
              grad, far_local ? 1 : 0, st);
   CKL();
   record(h, EV_DOWN);
@@ -628,6 +656,7 @@ int fmm_destroy(fmm_t h) {
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release();
+  h->tleaves.release();
   h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
@@ -804,6 +833,38 @@ int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, dou
   if (h_keys) CK(cudaMemcpy(h_keys, h->keys.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   if (h_origin3) for (int a = 0; a < 3; ++a) h_origin3[a] = h->h_root.origin[a];
   if (h_L) *h_L = h->h_root.L;
+  return FMM_OK;
+}
+
+int fmm_set_partition(fmm_t h, int nparts, int part) {
+  if (!h) return FMM_E_INVALID;
+  if (nparts < 1 || part < 0 || part >= nparts)
+    return fail(h, FMM_E_INVALID, "bad partition %d of %d", part, nparts);
+  h->nparts = nparts;
+  h->part = part;
+  return FMM_OK;
+}
+
+int fmm_get_partition(fmm_t h, int64_t *lo, int64_t *hi) {
+  if (!h || !lo || !hi) return FMM_E_INVALID;
+  if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
+  *lo = h->part_lo;
+  *hi = h->part_hi;
+  return FMM_OK;
+}
+
+int fmm_partition_indices(fmm_t h, int64_t *d_out, int64_t cap, int64_t *count_out) {
+  if (!h || !count_out) return FMM_E_INVALID;
+  if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
+  const int cnt = h->part_hi - h->part_lo;
+  *count_out = cnt;
+  if (cap < cnt) return fail(h, FMM_E_INVALID, "cap too small");
+  if (cnt > 0) {
+    if (int rc = check_device_ptr(h, d_out, "out")) return rc;
+    launch_part_indices(h->part_lo, cnt, h->perm.p, d_out, h->stream);
+    CKL();
+    CK(cudaStreamSynchronize(h->stream));
+  }
   return FMM_OK;
 }
 

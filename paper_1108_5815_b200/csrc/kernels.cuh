@@ -25,6 +25,9 @@ void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int
                  cudaStream_t st);
 void launch_level_total(const int *nch, const int *excl, int nl, int *total, cudaStream_t st);
 void launch_leaf_flags(int ncells, const int *nchild, int *flag, cudaStream_t st);
+void launch_part_flags(int ncells, CellsView C, int64_t n, int nparts, int part, int *flag,
+                       int *lohi, cudaStream_t st);
+void launch_part_indices(int lo, int cnt, const unsigned *perm, int64_t *out, cudaStream_t st);
 void launch_leaf_scatter(int ncells, const int *flag, const int *excl, int *leaves,
                          cudaStream_t st);
 
@@ -32,6 +35,7 @@ void launch_leaf_scatter(int ncells, const int *flag, const int *excl, int *leav
 struct TravArgs {
   CellsView C;
   int t0, nt, level, mode, stack_cap, grid_blocks;
+  int tlo, thi;  // targets restricted to cells intersecting sorted particle range [tlo, thi)
   double theta, t_pp, t_mp, t_ml;
   const unsigned *in_src;
   const int *in_off, *in_cnt;

@@ -50,6 +50,21 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
     const int t = A.t0 + k;
     const int4 gt = C.grid[t];
     const int tcnt = C.cnt[t];
+    if (!(C.beg[t] < A.thi && C.beg[t] + tcnt > A.tlo)) {  // outside this rank's target partition
+      if (lane == 0) {
+        if (WRITE) {
+          for (int c = 0; c < 3; ++c) {
+            A.loff[c][t] = 0;
+            A.lcnt[c][t] = 0;
+          }
+          A.out_off[t] = 0;
+          A.out_cnt[t] = 0;
+        } else {
+          for (int c = 0; c < 4; ++c) A.cnt4[c * A.nt + k] = 0;
+        }
+      }
+      continue;
+    }
     const bool tleaf = C.nchild[t] == 0;
     int n[4] = {0, 0, 0, 0};
     unsigned *dst[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -269,6 +269,35 @@ __global__ void __launch_bounds__(256) k_leaf_scatter(int ncells, const int *__r
   if (c < ncells && flag[c]) leaves[excl[c]] = c;
 }
 
+// Morton partition of the targets (multi-GPU): a leaf belongs to part floor(begin * nparts / n).
+// flag = leaf of part `part`; the part's sorted particle range [lo, hi) via atomics into lohi.
+__global__ void __launch_bounds__(256) k_part_flags(int ncells, CellsView C, int64_t n,
+                                                    int nparts, int part, int *__restrict__ flag,
+                                                    int *__restrict__ lohi) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  int f = 0;
+  if (C.nchild[c] == 0) {
+    const int b = C.beg[c];
+    f = (int)(((int64_t)b * nparts) / n) == part;
+    if (f) {
+      atomicMin(&lohi[0], b);
+      atomicMax(&lohi[1], b + C.cnt[c]);
+    }
+  }
+  flag[c] = f;
+}
+__global__ void k_part_init(int *lohi, int n) {
+  lohi[0] = n;
+  lohi[1] = 0;
+}
+__global__ void __launch_bounds__(256) k_part_indices(int lo, int cnt,
+                                                      const unsigned *__restrict__ perm,
+                                                      int64_t *__restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    out[i] = perm[lo + i];
+}
+
 // ---- host launchers --------------------------------------------------------------------------
 static int grid_for(int64_t n, int bs) {
   int64_t g = (n + bs - 1) / bs;
@@ -315,6 +344,15 @@ void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int
 }
 void launch_level_total(const int *nch, const int *excl, int nl, int *total, cudaStream_t st) {
   k_level_total<<<1, 1, 0, st>>>(nch, excl, nl, total);
+}
+void launch_part_flags(int ncells, CellsView C, int64_t n, int nparts, int part, int *flag,
+                       int *lohi, cudaStream_t st) {
+  k_part_init<<<1, 1, 0, st>>>(lohi, (int)n);
+  k_part_flags<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, C, n, nparts, part, flag, lohi);
+}
+void launch_part_indices(int lo, int cnt, const unsigned *perm, int64_t *out, cudaStream_t st) {
+  const int b = (cnt + 255) / 256 < 148 * 8 ? (cnt + 255) / 256 : 148 * 8;
+  k_part_indices<<<b > 0 ? b : 1, 256, 0, st>>>(lo, cnt, perm, out);
 }
 void launch_leaf_flags(int ncells, const int *nchild, int *flag, cudaStream_t st) {
   k_leaf_flags<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, nchild, flag);

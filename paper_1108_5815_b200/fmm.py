@@ -14,7 +14,8 @@ MODES = {"hybrid": HYBRID, "fmm": FMM_MODE, "treecode": TREECODE, "direct": DIRE
 SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_host", "fmm_set_stream",
            "fmm_set_mode", "fmm_set_timing", "fmm_tune", "fmm_get_cost_model",
            "fmm_set_cost_model", "fmm_get_stats", "fmm_export_tree", "fmm_export_lists",
-           "fmm_export_perm", "fmm_strerror", "fmm_last_error"]
+           "fmm_export_perm", "fmm_set_partition", "fmm_get_partition", "fmm_partition_indices",
+           "fmm_strerror", "fmm_last_error"]
 
 
 class FmmError(RuntimeError):
@@ -72,6 +73,9 @@ def load_library():
     L.fmm_export_tree.argtypes = [vp, i64, vp, vp, vp, vp, P(i64)]
     L.fmm_export_lists.argtypes = [vp, i64, vp, vp, vp, vp, vp, P(i64)]
     L.fmm_export_perm.argtypes = [vp, i64, vp, vp, vp, vp]
+    L.fmm_set_partition.argtypes = [vp, C.c_int, C.c_int]
+    L.fmm_get_partition.argtypes = [vp, P(i64), P(i64)]
+    L.fmm_partition_indices.argtypes = [vp, vp, i64, P(i64)]
     L.fmm_strerror.argtypes = [C.c_int]
     L.fmm_strerror.restype = C.c_char_p
     L.fmm_last_error.argtypes = [vp]
@@ -175,6 +179,25 @@ class FMM:
         self._check(self.L.fmm_evaluate_host(self.h, _ptr(xyz), _ptr(q), n, _ptr(phi), _ptr(grad)),
                     "fmm_evaluate_host")
         return phi, grad
+
+    def set_partition(self, nparts: int, part: int):
+        self._check(self.L.fmm_set_partition(self.h, int(nparts), int(part)), "fmm_set_partition")
+
+    def partition_range(self):
+        lo, hi = C.c_int64(), C.c_int64()
+        self._check(self.L.fmm_get_partition(self.h, C.byref(lo), C.byref(hi)), "fmm_get_partition")
+        return lo.value, hi.value
+
+    def partition_indices(self, device=None):
+        """Caller indices (int64 CUDA tensor) of the particles evaluated by this partition."""
+        import torch
+
+        lo, hi = self.partition_range()
+        out = torch.empty(max(hi - lo, 1), dtype=torch.int64, device=device or "cuda")
+        cnt = C.c_int64()
+        self._check(self.L.fmm_partition_indices(self.h, out.data_ptr(), out.numel(), C.byref(cnt)),
+                    "fmm_partition_indices")
+        return out[: cnt.value]
 
     def export_tree(self) -> dict:
         cnt = C.c_int64()
