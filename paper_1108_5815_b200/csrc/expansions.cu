@@ -57,11 +57,12 @@ __device__ void regular_table(float x, float y, float z, int P, float2 *tab, int
 
 // ---------------------------------------------------------------------------------------------
 // P2M: warp per leaf; lanes = particles; each coefficient reduced with a fixed butterfly.
-__global__ void __launch_bounds__(128) k_p2m(int p, const int *__restrict__ leaves, int nleaves,
+template <int p>
+__global__ void __launch_bounds__(128) k_p2m(const int *__restrict__ leaves, int nleaves,
                                              CellsView C, const float4 *__restrict__ pos,
                                              float2 *__restrict__ M) {
   extern __shared__ float2 sh_p2m[];
-  const int NC = nc_of(p), NCS = nc_stride(p);
+  constexpr int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *acc = sh_p2m + wib * NC;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -79,9 +80,11 @@ __global__ void __launch_bounds__(128) k_p2m(int p, const int *__restrict__ leav
       const float q = y.w;
       const float r2 = x * x + yy * yy + z * z;
       float2 Rmm = make_float2(1.f, 0.f);
+#pragma unroll
       for (int m = 0; m <= p; ++m) {
         if (m > 0) Rmm = cscale(cmul(Rmm, make_float2(x, yy)), -1.f / (2.f * m));
         float2 R2 = make_float2(0.f, 0.f), R1 = Rmm;
+#pragma unroll
         for (int n = m; n <= p; ++n) {
           float2 Rn;
           if (n == m) Rn = Rmm;
@@ -199,17 +202,21 @@ __global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
 
 // ---------------------------------------------------------------------------------------------
 // M2P: warp per leaf, lanes = target particles; sources = M2P lists of the leaf and its ancestors.
-__global__ void __launch_bounds__(128) k_m2p(int p, const int *__restrict__ leaves, int nleaves,
+template <int p>
+__global__ void __launch_bounds__(128) k_m2p(const int *__restrict__ leaves, int nleaves,
                                              CellsView C, ListsView Ls,
                                              const float4 *__restrict__ pos,
                                              const float2 *__restrict__ M,
-                                             float4 *__restrict__ acc) {
+                                             float4 *__restrict__ acc, int *next_leaf) {
   extern __shared__ float2 sh_m2p[];
-  const int NC = nc_of(p), NCS = nc_stride(p);
+  constexpr int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *Ms = sh_m2p + wib * NC;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int li = gw; li < nleaves; li += nw) {
+  for (;;) {
+    int li = 0;
+    if (lane == 0) li = atomicAdd(next_leaf, 1);  // dynamic leaf queue (load balance)
+    li = __shfl_sync(0xffffffffu, li, 0);
+    if (li >= nleaves) break;
     const int leaf = leaves[li];
     bool any = false;
     for (int a = leaf; a >= 0; a = C.parent[a]) any |= Ls.cnt[1][a] > 0;
@@ -234,10 +241,12 @@ __global__ void __launch_bounds__(128) k_m2p(int p, const int *__restrict__ leav
           float ph = 0.f, dz = 0.f;
           float2 dxy = make_float2(0.f, 0.f);
           float2 Imm = make_float2(sqrtf(ir2), 0.f);
+#pragma unroll
           for (int mm = 0; mm <= p + 1; ++mm) {
             if (mm > 0) Imm = cscale(cmul(Imm, make_float2(xx, yy)), -(2.f * mm - 1.f) * ir2);
             float2 I2 = make_float2(0.f, 0.f), I1 = Imm;
             const float w = mm ? 2.f : 1.f;
+#pragma unroll
             for (int a2 = mm; a2 <= p + 1; ++a2) {
               float2 Ia;
               if (a2 == mm) Ia = Imm;
@@ -292,7 +301,8 @@ __global__ void __launch_bounds__(128) k_m2p(int p, const int *__restrict__ leav
 // ---------------------------------------------------------------------------------------------
 // L2P + combine + un-permute: warp per leaf, lanes = particles. out = acc (+ L2P if use_local),
 // written to the caller's order: phi[perm[i]], grad[3 perm[i] + a].
-__global__ void __launch_bounds__(128) k_l2p(int p, const int *__restrict__ leaves, int nleaves,
+template <int p>
+__global__ void __launch_bounds__(128) k_l2p(const int *__restrict__ leaves, int nleaves,
                                              CellsView C, const float4 *__restrict__ pos,
                                              const float2 *__restrict__ L,
                                              const float4 *__restrict__ acc,
@@ -300,7 +310,7 @@ __global__ void __launch_bounds__(128) k_l2p(int p, const int *__restrict__ leav
                                              float *__restrict__ phi_out,
                                              float *__restrict__ grad_out, int use_local) {
   extern __shared__ float2 sh_l2p[];
-  const int NC = nc_of(p), NCS = nc_stride(p);
+  constexpr int NC = nc_of(p), NCS = nc_stride(p);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float2 *Ll = sh_l2p + wib * NC;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -325,10 +335,12 @@ __global__ void __launch_bounds__(128) k_l2p(int p, const int *__restrict__ leav
         float ph = 0.f, dz = 0.f;
         float2 dxy = make_float2(0.f, 0.f);
         float2 Rmm = make_float2(1.f, 0.f);
+#pragma unroll
         for (int mm = 0; mm <= p; ++mm) {
           if (mm > 0) Rmm = cscale(cmul(Rmm, make_float2(xx, yy)), -1.f / (2.f * mm));
           float2 R2 = make_float2(0.f, 0.f), R1 = Rmm;
           const float w = mm ? 2.f : 1.f;
+#pragma unroll
           for (int a2 = mm; a2 <= p; ++a2) {
             float2 Ra;
             if (a2 == mm) Ra = Rmm;
@@ -398,10 +410,31 @@ M2LTiles make_m2l_tiles(int p) {
   return T;
 }
 
+#define FMM_DISPATCH_P(p, CALL)                                                      \
+  switch (p) {                                                                       \
+    case 1: { constexpr int P_ = 1; CALL; } break;                                   \
+    case 2: { constexpr int P_ = 2; CALL; } break;                                   \
+    case 3: { constexpr int P_ = 3; CALL; } break;                                   \
+    case 4: { constexpr int P_ = 4; CALL; } break;                                   \
+    case 5: { constexpr int P_ = 5; CALL; } break;                                   \
+    case 6: { constexpr int P_ = 6; CALL; } break;                                   \
+    case 7: { constexpr int P_ = 7; CALL; } break;                                   \
+    case 8: { constexpr int P_ = 8; CALL; } break;                                   \
+    case 9: { constexpr int P_ = 9; CALL; } break;                                   \
+    case 10: { constexpr int P_ = 10; CALL; } break;                                 \
+    case 11: { constexpr int P_ = 11; CALL; } break;                                 \
+    case 12: { constexpr int P_ = 12; CALL; } break;                                 \
+    case 13: { constexpr int P_ = 13; CALL; } break;                                 \
+    case 14: { constexpr int P_ = 14; CALL; } break;                                 \
+    case 15: { constexpr int P_ = 15; CALL; } break;                                 \
+    default: { constexpr int P_ = 16; CALL; } break;                                 \
+  }
+
 void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos, float2 *M,
                 cudaStream_t st) {
   ensure_nm_table();
-  k_p2m<<<warp_grid(nleaves, 4), 128, 4 * nc_of(p) * sizeof(float2), st>>>(p, leaves, nleaves, C, pos, M);
+  FMM_DISPATCH_P(p, (k_p2m<P_><<<warp_grid(nleaves, 4), 128, 4 * nc_of(P_) * sizeof(float2), st>>>(
+                        leaves, nleaves, C, pos, M)));
 }
 void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st) {
   ensure_nm_table();
@@ -412,13 +445,16 @@ void launch_l2l(int p, int c0, int nl, CellsView C, float2 *L, cudaStream_t st) 
   k_l2l<<<warp_grid(nl, 4), 128, 4 * 2 * nc_of(p) * sizeof(float2), st>>>(p, c0, nl, C, L);
 }
 void launch_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                const float4 *pos, const float2 *M, float4 *acc, cudaStream_t st) {
+                const float4 *pos, const float2 *M, float4 *acc, int *counter, cudaStream_t st) {
   ensure_nm_table();
-  k_m2p<<<warp_grid(nleaves, 4), 128, 4 * nc_of(p) * sizeof(float2), st>>>(p, leaves, nleaves, C, Ls, pos, M, acc);
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  FMM_DISPATCH_P(p, (k_m2p<P_><<<148 * 8, 128, 4 * nc_of(P_) * sizeof(float2), st>>>(
+                        leaves, nleaves, C, Ls, pos, M, acc, counter)));
 }
 void launch_l2p(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos,
                 const float2 *L, const float4 *acc, const unsigned *perm, float *phi, float *grad,
                 int use_local, cudaStream_t st) {
   ensure_nm_table();
-  k_l2p<<<warp_grid(nleaves, 4), 128, 4 * nc_of(p) * sizeof(float2), st>>>(p, leaves, nleaves, C, pos, L, acc, perm, phi, grad, use_local);
+  FMM_DISPATCH_P(p, (k_l2p<P_><<<warp_grid(nleaves, 4), 128, 4 * nc_of(P_) * sizeof(float2), st>>>(
+                        leaves, nleaves, C, pos, L, acc, perm, phi, grad, use_local)));
 }

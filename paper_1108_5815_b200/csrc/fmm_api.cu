@@ -480,7 +480,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   CKL();
   record(h, EV_P2P);
   if (h->ntask[FMM_KIND_M2P] > 0) {
-    launch_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, st);
+    launch_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, h->d_small + 13, st);
     CKL();
   }
   record(h, EV_M2P);

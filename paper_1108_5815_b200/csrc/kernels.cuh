@@ -62,7 +62,7 @@ void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4
 void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st);
 void launch_l2l(int p, int c0, int nl, CellsView C, float2 *L, cudaStream_t st);
 void launch_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                const float4 *pos, const float2 *M, float4 *acc, cudaStream_t st);
+                const float4 *pos, const float2 *M, float4 *acc, int *counter, cudaStream_t st);
 void launch_l2p(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos,
                 const float2 *L, const float4 *acc, const unsigned *perm, float *phi, float *grad,
                 int use_local, cudaStream_t st);
