@@ -117,71 +117,66 @@ __global__ void __launch_bounds__(128) k_p2m(const int *__restrict__ leaves, int
 }
 
 // ---------------------------------------------------------------------------------------------
-// M2M: warp per parent cell of one level. b/r_P = (+-1/2, +-1/2, +-1/2) exactly.
-__global__ void __launch_bounds__(128) k_m2m(int p, int c0, int nl, CellsView C,
-                                             float2 *__restrict__ M) {
-  extern __shared__ float2 sh_m2m[];
-  const int NC = nc_of(p), NCS = nc_stride(p);
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float2 *Mc = sh_m2m + wib * 2 * NC, *Rb = Mc + NC;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int k = gw; k < nl; k += nw) {
+// M2M: one CTA of 8 warps per parent cell of one level; warp w shifts child w (b/r_P is exactly
+// (+-1/2, +-1/2, +-1/2)) and the 8 contributions are summed in child order in shared memory
+// (deterministic). Eight warps per parent keep the few-parent top levels from being latency-bound.
+template <int p>
+__global__ void __launch_bounds__(256) k_m2m(int c0, int nl, CellsView C, float2 *__restrict__ M) {
+  constexpr int NC = nc_of(p), NCS = nc_stride(p);
+  __shared__ float2 Mc[8][NC], Rb[8][NC], part[8][NC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = blockIdx.x; k < nl; k += gridDim.x) {
     const int P = c0 + k;
     const int nch = C.nchild[P];
-    if (nch == 0) continue;
-    const int4 gp = C.grid[P];
-    const float rP = (float)(1 << (FMM_LEVELS - gp.w));
-    float2 acc[5];
-#pragma unroll
-    for (int s = 0; s < 5; ++s) acc[s] = make_float2(0.f, 0.f);
-    for (int ch = 0; ch < nch; ++ch) {
-      const int Cc = C.child0[P] + ch;
+    if (nch == 0) continue;  // block-uniform
+    if (w < nch) {
+      const int4 gp = C.grid[P];
+      const float rP = (float)(1 << (FMM_LEVELS - gp.w));
+      const int Cc = C.child0[P] + w;
       const int4 gc = C.grid[Cc];
-      for (int o = lane; o < NC; o += WARP) Mc[o] = M[(size_t)Cc * NCS + o];
-      regular_table((gc.x - gp.x) / rP, (gc.y - gp.y) / rP, (gc.z - gp.z) / rP, p, Rb, lane);
+      for (int o = lane; o < NC; o += WARP) Mc[w][o] = M[(size_t)Cc * NCS + o];
+      regular_table((gc.x - gp.x) / rP, (gc.y - gp.y) / rP, (gc.z - gp.z) / rP, p, Rb[w], lane);
       __syncwarp();
-#pragma unroll
-      for (int s = 0; s < 5; ++s) {
-        const int o = lane + s * WARP;
-        if (o >= NC) break;
+      for (int o = lane; o < NC; o += WARP) {
         const int n = c_nm[o].x, m = c_nm[o].y;
         float2 a = make_float2(0.f, 0.f);
         float sc = 1.f;
         for (int j = 0; j <= n; ++j, sc *= 0.5f) {
           const int klo = max(-j, m - (n - j)), khi = min(j, m + (n - j));
-          float2 part = make_float2(0.f, 0.f);
-          for (int kk = klo; kk <= khi; ++kk) {
-            const float2 mv = sget(Mc, j, kk), rv = cconj(sget(Rb, n - j, m - kk));
-            part = cadd(part, cmul(mv, rv));
-          }
-          a = cadd(a, cscale(part, sc));
+          float2 pa = make_float2(0.f, 0.f);
+          for (int kk = klo; kk <= khi; ++kk)
+            pa = cadd(pa, cmul(sget(Mc[w], j, kk), cconj(sget(Rb[w], n - j, m - kk))));
+          a = cadd(a, cscale(pa, sc));
         }
-        acc[s] = cadd(acc[s], a);
+        part[w][o] = a;
       }
-      __syncwarp();
     }
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-      const int o = lane + s * WARP;
-      if (o < NC) M[(size_t)P * NCS + o] = acc[s];
+    __syncthreads();
+    for (int o = threadIdx.x; o < NC; o += blockDim.x) {
+      float2 acc = part[0][o];
+      for (int c = 1; c < nch; ++c) acc = cadd(acc, part[c][o]);
+      M[(size_t)P * NCS + o] = acc;
     }
+    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// L2L: warp per child cell of one level; adds the parent's local expansion.
-__global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
-                                             float2 *__restrict__ L) {
-  extern __shared__ float2 sh_l2l[];
-  const int NC = nc_of(p), NCS = nc_stride(p);
+// L2L: warp per child cell of one level; adds the parent's local expansion shifted by
+// e/r_P = (+-1/2, +-1/2, +-1/2).
+template <int p>
+__global__ void __launch_bounds__(128) k_l2l(int c0, int nl, CellsView C, float2 *__restrict__ L) {
+  constexpr int NC = nc_of(p), NCS = nc_stride(p);
+  __shared__ float2 sh[4][2][NC];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float2 *Lp = sh_l2l + wib * 2 * NC, *Re = Lp + NC;
+  float2 *Lp = sh[wib][0], *Re = sh[wib][1];
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int k = gw; k < nl; k += nw) {
     const int Cc = c0 + k;
     const int P = C.parent[Cc];
     const int4 gp = C.grid[P], gc = C.grid[Cc];
     const float rP = (float)(1 << (FMM_LEVELS - gp.w));
+    __syncwarp();
     for (int o = lane; o < NC; o += WARP) Lp[o] = L[(size_t)P * NCS + o];
     regular_table((gc.x - gp.x) / rP, (gc.y - gp.y) / rP, (gc.z - gp.z) / rP, p, Re, lane);
     __syncwarp();
@@ -196,7 +191,6 @@ __global__ void __launch_bounds__(128) k_l2l(int p, int c0, int nl, CellsView C,
       const float2 old = L[(size_t)Cc * NCS + o];
       L[(size_t)Cc * NCS + o] = make_float2(old.x + sc * a.x, old.y + sc * a.y);
     }
-    __syncwarp();
   }
 }
 
@@ -438,11 +432,12 @@ void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4
 }
 void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st) {
   ensure_nm_table();
-  k_m2m<<<warp_grid(nl, 4), 128, 4 * 2 * nc_of(p) * sizeof(float2), st>>>(p, c0, nl, C, M);
+  const int blocks = nl < 148 * 8 ? (nl > 0 ? nl : 1) : 148 * 8;
+  FMM_DISPATCH_P(p, (k_m2m<P_><<<blocks, 256, 0, st>>>(c0, nl, C, M)));
 }
 void launch_l2l(int p, int c0, int nl, CellsView C, float2 *L, cudaStream_t st) {
   ensure_nm_table();
-  k_l2l<<<warp_grid(nl, 4), 128, 4 * 2 * nc_of(p) * sizeof(float2), st>>>(p, c0, nl, C, L);
+  FMM_DISPATCH_P(p, (k_l2l<P_><<<warp_grid(nl, 4), 128, 0, st>>>(c0, nl, C, L)));
 }
 void launch_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
                 const float4 *pos, const float2 *M, float4 *acc, int *counter, cudaStream_t st) {

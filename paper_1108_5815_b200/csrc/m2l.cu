@@ -16,6 +16,7 @@
 // Rare classes (< M2L_SMALL pairs) and orders p > 12 (T too large for shared memory) use
 // k_m2l_pairs: one warp per pair evaluating the double loop directly.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -271,7 +272,8 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restrict__ items,
+template <int p>
+__global__ void __launch_bounds__(288, 2) k_m2l_gemm(const int4 *__restrict__ items,
                                                      const int *__restrict__ counters,
                                                      const unsigned *__restrict__ sidx,
                                                      const unsigned *__restrict__ ssrc,
@@ -279,11 +281,11 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
                                                      const float *__restrict__ M,
                                                      float *__restrict__ Y, int *queue) {
   extern __shared__ __align__(128) float sh_gemm[];
-  const int NC = nc_of(p), KR = 2 * NC;
-  const int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
-  const int XKS = ((Kpad >> 2) & 1) ? Kpad : Kpad + 4;  // X row stride: odd number of 16-B slots
-  const int ncons = (Rpad / 12) * 16;                    // consumer threads
-  const int ncw = (ncons + 31) / 32;                     // consumer warps; the next warp produces
+  constexpr int NC = nc_of(p), KR = 2 * NC;
+  constexpr int Kpad = (KR + 3) & ~3, Rpad = ((KR + 11) / 12) * 12;
+  constexpr int XKS = ((Kpad >> 2) & 1) ? Kpad : Kpad + 4;  // X row stride: odd # of 16-B slots
+  constexpr int ncons = (Rpad / 12) * 16;                    // consumer threads
+  constexpr int ncw = (ncons + 31) / 32;                     // consumer warps; the next produces
   float *Ts = sh_gemm;
   float *Xs0 = Ts + Kpad * Rpad;  // double buffer: Xs0 + b * M2L_XCH * XKS
   unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xs0 + 2 * M2L_XCH * XKS);
@@ -330,9 +332,11 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
       }
       for (int c0 = 0; c0 < cnt; c0 += M2L_XCH, ++g) {
         const int b = g & 1, use = g >> 1;
-        if (use > 0) mbar_wait(&x_empty[b], (use - 1) & 1);
         const int ncol = min(M2L_XCH, cnt - c0);
-        const int s = lane < ncol ? (int)ssrc[pos0 + c0 + lane] : 0;
+        // source ids are loaded before waiting for the buffer (the asm wait is a memory fence
+        // for the compiler, so the load would otherwise sit on the critical path)
+        const int s = lane < ncol ? (int)__ldg(&ssrc[pos0 + c0 + lane]) : 0;
+        if (use > 0) mbar_wait(&x_empty[b], (use - 1) & 1);
         const int s0 = __shfl_sync(0xffffffffu, s, 0), sl = __shfl_sync(0xffffffffu, s, ncol - 1);
         const bool contiguous = (XKS == Kpad) && (sl - s0 == ncol - 1) &&
                                 __all_sync(0xffffffffu, lane >= ncol || s == s0 + lane);
@@ -375,6 +379,7 @@ __global__ void __launch_bounds__(288, 2) k_m2l_gemm(int p, const int4 *__restri
         const float *Tp = Ts + rg * 12;
         const float *Xb = Xs0 + b * M2L_XCH * XKS;
         const float *x0p = Xb + cg * XKS, *x1p = Xb + (cg + 16) * XKS;
+#pragma unroll 3
         for (int k = 0; k < Kpad; k += 4) {
           const float4 xa = *reinterpret_cast<const float4 *>(x0p + k);
           const float4 xb = *reinterpret_cast<const float4 *>(x1p + k);
@@ -551,18 +556,28 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
                         float2 *L, cudaStream_t st) {
   if (!W.direct_all) {
     const size_t smem = m2l_gemm_smem(p);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      cudaFuncSetAttribute(k_m2l_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      configured = smem;
-    }
     const int KR = 2 * nc_of(p);
     const int nthr = (((KR + 11) / 12) * 16 + 31) / 32 * 32 + 32;  // consumer warps + producer
     const int per_sm = (int)((227 * 1024) / smem) < 2 ? 1 : 2;
     cudaMemsetAsync(W.counters + 4, 0, sizeof(int), st);
-    k_m2l_gemm<<<148 * per_sm, nthr, smem, st>>>(p, W.items, W.counters, W.sidx, W.ssrc, W.Tg,
-                                                  reinterpret_cast<const float *>(M), W.Y,
-                                                  W.counters + 4);
+#define M2L_GEMM_CASE(PP)                                                                    \
+  case PP: {                                                                               \
+    static bool cfg = false;                                                               \
+    if (!cfg && smem > 48 * 1024) {                                                        \
+      cudaFuncSetAttribute(k_m2l_gemm<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      cfg = true;                                                                          \
+    }                                                                                      \
+    k_m2l_gemm<PP><<<148 * per_sm, nthr, smem, st>>>(W.items, W.counters, W.sidx, W.ssrc, W.Tg, \
+                                                    reinterpret_cast<const float *>(M), W.Y, \
+                                                    W.counters + 4);                     \
+  } break;
+    switch (p) {
+      M2L_GEMM_CASE(1) M2L_GEMM_CASE(2) M2L_GEMM_CASE(3) M2L_GEMM_CASE(4) M2L_GEMM_CASE(5)
+      M2L_GEMM_CASE(6) M2L_GEMM_CASE(7) M2L_GEMM_CASE(8) M2L_GEMM_CASE(9) M2L_GEMM_CASE(10)
+      M2L_GEMM_CASE(11) M2L_GEMM_CASE(12)
+      default: break;
+    }
+#undef M2L_GEMM_CASE
   }
   {
     const int nI = (2 * p + 1) * (2 * p + 1), nM = (p + 1) * (p + 1);
