@@ -193,3 +193,26 @@ def test_virtual_rank_partition_union(handles, mode):
     # fewer than M2L_SMALL pairs differs (direct loop vs class GEMM): FP32 rounding level
     from oracle.oracle import rel_l2
     assert rel_l2(phi_u, full_phi) < 1e-6 and rel_l2(grad_u, full_grad) < 1e-6
+
+
+@pytest.mark.parametrize("cfg_name", ["C2", "C3"])
+def test_full_size_sampled_parity(O, cfg_name):
+    """BASELINE configs at full size in the bench's launch configuration (auto-tuned hybrid):
+    sampled targets against the oracle's sampled-target mode (exact for those targets, same tree,
+    lists and imported cost model) within 1e-5, and against the direct sum within 1e-4 (p=10)."""
+    from fmm_inputs import CONFIGS
+
+    cfg = CONFIGS[cfg_name]
+    xyz, q = make_particles(cfg["n"], cfg["dist"], cfg["seed"])
+    f = FMM(p=cfg["p"], theta=cfg["theta"], ncrit=cfg["ncrit"], mode="hybrid", tune=True)
+    try:
+        phi, grad = run(f, xyz, q)
+        cost = f.cost_model()
+    finally:
+        f.close()
+    s = np.random.default_rng(7).choice(len(q), 2048, replace=False)
+    ref = O.fmm(xyz, q, cfg["p"], cfg["theta"], cfg["ncrit"], O.HYBRID, cost=cost, sample=s,
+                want_structure=False)
+    assert O.rel_l2(phi[s], ref.phi) < 1e-5 and O.rel_l2(grad[s], ref.grad) < 1e-5
+    d = O.direct(xyz, q, s)
+    assert O.rel_l2(phi[s], d[0]) < 1e-4 and O.rel_l2(grad[s], d[1]) < 1e-3
