@@ -44,6 +44,7 @@ struct ListsView {
   int *off[3];       // per target cell, per kind (M2L, M2P, P2P)
   int *cnt[3];
   unsigned *src[3];  // source cell ids
+  int2 *p2p_rng;     // (begin, count) of every P2P source cell, parallel to src[2]
 };
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {

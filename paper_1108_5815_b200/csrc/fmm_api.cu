@@ -113,6 +113,7 @@ struct fmm_ctx {
   // lists
   DBuf<int> loff[3], lcnt[3];
   DBuf<unsigned> lsrc[3];
+  DBuf<int2> p2p_rng;
   DBuf<int> out_off, out_cnt, cnt4, excl4;
   DBuf<unsigned> outA, outB, stack;
   int stack_cap = 2048;
@@ -139,6 +140,7 @@ struct fmm_ctx {
       Ls.cnt[k] = lcnt[k].p;
       Ls.src[k] = lsrc[k].p;
     }
+    Ls.p2p_rng = p2p_rng.p;
     return Ls;
   }
 };
@@ -375,6 +377,8 @@ restart:
       A.lcnt[k] = h->lcnt[k].p;
       A.base[k] = (int)base[k];
     }
+    CK(h->p2p_rng.ensure_keep((size_t)(base[2] + tot[2]) + 1, (size_t)base[2], st));
+    A.p2p_rng = h->p2p_rng.p;
     DBuf<unsigned> *ob = outbuf[level & 1];
     CK(ob->ensure((size_t)tot[3] + 1));
     A.out_src = ob->p;
@@ -664,7 +668,7 @@ int fmm_destroy(fmm_t h) {
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
   h->m2l_Y.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
-  h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
+  h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();
   if (h->d_root) cudaFree(h->d_root);
   if (h->d_mm) cudaFree(h->d_mm);

@@ -47,6 +47,7 @@ struct TravArgs {
   int *loff[3], *lcnt[3];
   unsigned *out_src;
   int *out_off, *out_cnt;
+  int2 *p2p_rng;  // WRITE pass: (begin, count) of each P2P source cell, parallel to lsrc[2]
   unsigned long long *stats;  // [0] P2P particle pairs, [1] M2P target evaluations
 };
 void launch_traverse(const TravArgs &A, bool write, cudaStream_t st);

@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, 4) k_p2p_leaves(const int *__r
           const int e = ae + lane;
           int2 r = make_int2(0, 0);
           if (e < ncell) {
-            const int s = Ls.src[2][off + e];
-            if (s != leaf) r = make_int2(C.beg[s], C.cnt[s]);
+            r = Ls.p2p_rng[off + e];   // (begin, count) stored by the traversal: one load
+            if (r.x == tb) r.y = 0;     // the leaf itself is done separately (masked)
           }
           const unsigned bal = __ballot_sync(0xffffffffu, r.y > 0);
           if (r.y > 0) rng[nr + __popc(bal & ((1u << lane) - 1u))] = r;

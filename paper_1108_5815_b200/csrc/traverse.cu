@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
           top += __popc(b);
           if (top > A.stack_cap) overflow = true;
         } else {
-          if (WRITE && cat == c) dst[c][n[c] + pos] = s;
+          if (WRITE && cat == c) {
+            dst[c][n[c] + pos] = s;
+            if (c == CAT_P2P) A.p2p_rng[(dst[c] - A.lsrc[2]) + n[c] + pos] = make_int2(C.beg[s], C.cnt[s]);
+          }
           n[c] += __popc(b);
         }
       }
