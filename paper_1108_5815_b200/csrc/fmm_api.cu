@@ -108,6 +108,8 @@ struct fmm_ctx {
   DBuf<unsigned long long> m2l_keys_in, m2l_keys;
   DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep, m2l_ssrc;
   DBuf<float> m2l_T;
+  DBuf<unsigned> m2l_Ttc;
+  bool m2l_tc_used = false;
   DBuf<int4> m2l_items;
   DBuf<float> m2l_Y;
   // lists
@@ -467,13 +469,26 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(cudaMemcpyAsync(h->h_small, h->m2l_counters.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int ngclass = h->h_small[3];
-    CK(h->m2l_T.ensure((size_t)std::max(1, ngclass) * m2l_T_floats(p)));
-    W.Tg = h->m2l_T.p;
-    CK(m2l_build_T(p, W, ngclass, st));
+    // class GEMMs on the tensor cores (tcgen05, 3xTF32) unless disabled / unsupported
+    const char *cc = getenv("FMM_M2L_CUDA_CORES");
+    const bool use_tc = !W.direct_all && m2l_tc_supported(p) && !(cc && cc[0] && cc[0] != '0');
+    if (use_tc) {
+      CK(h->m2l_Ttc.ensure((size_t)std::max(1, ngclass) * m2l_tc_T_words(p)));
+      CK(m2l_tc_build_T(p, W, ngclass, h->m2l_Ttc.p, st));
+    } else {
+      CK(h->m2l_T.ensure((size_t)std::max(1, ngclass) * m2l_T_floats(p)));
+      W.Tg = h->m2l_T.p;
+      CK(m2l_build_T(p, W, ngclass, st));
+    }
     h->stats.launches += 1;
     record(h, EV_M2L_PREP);
-    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st));
-    h->stats.launches += 3;
+    if (use_tc) {
+      CK(m2l_tc_gemm(p, W, h->m2l_Ttc.p, h->M.p, st));
+      h->stats.launches += 1;
+    }
+    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st, use_tc));
+    h->stats.launches += 2;
+    h->m2l_tc_used = use_tc;
   }
   record(h, EV_M2L);
   // a12 P2P (writes acc), a11 M2P (adds)
@@ -666,7 +681,7 @@ int fmm_destroy(fmm_t h) {
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
-  h->m2l_Y.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_T.release();
+  h->m2l_Y.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();

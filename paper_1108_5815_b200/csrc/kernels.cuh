@@ -96,7 +96,14 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
 size_t m2l_T_floats(int p);
 cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st);
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
-                        float2 *L, cudaStream_t st);
+                        float2 *L, cudaStream_t st, bool gemm_done = false);
+
+// ---- m2l_tc.cu (tcgen05 3xTF32 class GEMM) ----
+bool m2l_tc_supported(int p);
+size_t m2l_tc_T_words(int p);
+cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg, cudaStream_t st);
+cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
+                        cudaStream_t st);
 
 // ---- p2p.cu ----
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,

@@ -553,8 +553,8 @@ cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st) {
 }
 
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
-                        float2 *L, cudaStream_t st) {
-  if (!W.direct_all) {
+                        float2 *L, cudaStream_t st, bool gemm_done) {
+  if (!W.direct_all && !gemm_done) {
     const size_t smem = m2l_gemm_smem(p);
     const int KR = 2 * nc_of(p);
     const int nthr = (((KR + 11) / 12) * 16 + 31) / 32 * 32 + 32;  // consumer warps + producer

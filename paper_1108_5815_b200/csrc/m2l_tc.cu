@@ -1,0 +1,416 @@
+// m2l_tc.cu — M2L class GEMMs on the 5th-generation tensor cores (tcgen05, sm_100a).
+//
+// After class batching (m2l.cu) the translations of one class are a dense product
+//     D[pair][out] = sum_k X[pair][k] * T[out][k]
+// over the real degrees of freedom of a real field: d = 0..(p+1)^2-1 enumerates
+// (n, m=0, Re), (n, m>0, Re), (n, m>0, Im) of every coefficient (the Im part of m = 0 is zero).
+// At p = 10 that is 121 -> padded to K = N = 128. FP32 accuracy comes from 3xTF32 splitting:
+//     X = Xh + Xl, T = Th + Tl (each part TF32), D = Xh Th + Xh Tl + Xl Th
+// (the dropped Xl Tl term is ~2^-22 relative), accumulated in FP32 in TMEM.
+//
+// One CTA per SM (persistent, dynamic item queue), 4 warps = 128 threads:
+//   * A operand (X tile, 128 pairs x K) lives in TMEM: thread i = TMEM lane i = pair i loads its
+//     source multipole row, splits it and writes Xh, Xl with tcgen05.st;
+//   * B operand (class matrix, N x K, hi and lo) is one TMA bulk copy of a pre-arranged K-major
+//     core-matrix image into shared memory (built once per class by k_m2l_build_T_tc);
+//   * one elected thread issues 3 * K/8 tcgen05.mma.kind::tf32 (M = 128, N = K, K = 8 each);
+//     tcgen05.commit signals an mbarrier;
+//   * D (128 lanes x N columns FP32) is read back with tcgen05.ld and written to the pair slots
+//     Y[pair] in the same layout as the CUDA-core path, so k_m2l_reduce is shared.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+__host__ __device__ constexpr int dof_of(int p) { return (p + 1) * (p + 1); }
+__host__ __device__ constexpr int tc_dim(int p) { return (dof_of(p) + 15) & ~15; }  // K = N
+
+// real degree of freedom d -> float index inside an (m >= 0, complex) expansion row.
+// Order of the dofs: for n = 0..p: (n,0,Re), then for m = 1..n: (n,m,Re), (n,m,Im).
+__host__ __device__ constexpr int dof_to_float(int d) {
+  int n = 0;
+  while ((n + 1) * (n + 1) <= d) ++n;
+  const int r = d - n * n;                      // 0 .. 2n
+  if (r == 0) return 2 * (n * (n + 1) / 2);     // Re of (n, 0)
+  const int m = (r + 1) / 2, im = (r + 1) & 1;  // r = 2m-1 -> Re, r = 2m -> Im
+  return 2 * (n * (n + 1) / 2 + m) + im;
+}
+// float index f -> dof, or -1 for the (zero) Im part of an m = 0 coefficient
+__host__ __device__ constexpr int float_to_dof(int f) {
+  const int c = f / 2, part = f & 1;
+  int n = 0;
+  while ((n + 1) * (n + 2) / 2 <= c) ++n;
+  const int m = c - n * (n + 1) / 2;
+  if (m == 0) return part ? -1 : n * n;
+  return n * n + 2 * m - 1 + part;
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init_tc(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx_tc(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_tc(unsigned long long *bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_TC:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE_TC;\n bra WAIT_TC;\n DONE_TC:\n }" ::"r"(smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_tc(void *dst, const void *src, unsigned bytes,
+                                            unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ unsigned f32_to_tf32(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// tcgen05 wrappers -------------------------------------------------------------------------------
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_st32(unsigned taddr, const unsigned (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld32(unsigned taddr, unsigned (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::tf32, cta_group::1
+__device__ __forceinline__ void tc_mma_ts(unsigned d_tmem, unsigned a_tmem, unsigned long long bdesc,
+                                          unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(unsigned long long *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_addr(bar))
+               : "memory");
+}
+
+// K-major, no-swizzle ("interleaved") shared-memory operand: element (row, k) of an NR-row
+// operand at byte (k/4)*(NR*16) + row*16 + (k%4)*4, i.e. 8x16-byte core matrices; the two
+// 16-byte k-chunks of one K=8 MMA are LBO = NR*16 apart, 8-row groups SBO = 128 B apart.
+__device__ __forceinline__ unsigned long long make_bdesc(unsigned saddr, int nrows) {
+  unsigned long long d = 0;
+  d |= (unsigned long long)((saddr >> 4) & 0x3fff);                  // start address
+  d |= (unsigned long long)(((nrows * 16) >> 4) & 0x3fff) << 16;     // leading byte offset
+  d |= (unsigned long long)((128 >> 4) & 0x3fff) << 32;              // stride byte offset
+  d |= 1ull << 46;                                                   // version (sm_100)
+  // base offset 0, lbo mode 0, layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
+}  // namespace
+
+// per class: Th | Tl images (N x K each, N = K = tc_dim(p)) in the core-matrix layout above,
+// from the same translation formula as the CUDA-core k_m2l_build_T (m2l.cu header)
+__global__ void __launch_bounds__(256) k_m2l_build_T_tc(int p, const int *__restrict__ counters,
+                                                        const unsigned *__restrict__ class_rep,
+                                                        const int *__restrict__ pair_t,
+                                                        const unsigned *__restrict__ src,
+                                                        CellsView C, unsigned *__restrict__ Timg) {
+  extern __shared__ float2 itab_tc[];
+  const int KD = dof_of(p), NT = tc_dim(p);
+  const int ng = counters[3];
+  for (int gid = blockIdx.x; gid < ng; gid += gridDim.x) {
+    const int rep = class_rep[gid];
+    const int4 gt = C.grid[pair_t[rep]], gs = C.grid[src[rep]];
+    const float rt_inv = 1.f / (float)(1 << (FMM_LEVELS - gt.w));
+    const int dl = gt.w - gs.w;
+    float ux = (gt.x - gs.x) * rt_inv, uy = (gt.y - gs.y) * rt_inv, uz = (gt.z - gs.z) * rt_inv;
+    const bool vform = dl > 0;
+    if (vform) {
+      const float ir = ldexpf(1.f, -dl);
+      ux *= ir;
+      uy *= ir;
+      uz *= ir;
+    }
+    __syncthreads();
+    // irregular harmonics I_a^b(u), a <= 2p, signed b (same recurrences as m2l.cu)
+    {
+      const float r2 = ux * ux + uy * uy + uz * uz, ir2 = 1.f / r2;
+      for (int mm = threadIdx.x; mm <= 2 * p; mm += blockDim.x) {
+        float2 Imm = make_float2(rsqrtf(r2), 0.f);
+        for (int k = 1; k <= mm; ++k) {
+          const float tx = Imm.x * ux - Imm.y * uy, ty = Imm.x * uy + Imm.y * ux;
+          const float s = -(2.f * k - 1.f) * ir2;
+          Imm = make_float2(tx * s, ty * s);
+        }
+        float2 I2 = make_float2(0.f, 0.f), I1 = Imm;
+        const float sg = (mm & 1) ? -1.f : 1.f;
+        for (int a = mm; a <= 2 * p; ++a) {
+          float2 Ia;
+          if (a == mm) Ia = Imm;
+          else if (a == mm + 1) {
+            const float s = (2.f * mm + 1.f) * uz * ir2;
+            Ia = make_float2(Imm.x * s, Imm.y * s);
+          } else {
+            const float c1 = (2.f * a - 1.f) * uz, c2 = (float)(a + mm - 1) * (float)(a - mm - 1);
+            Ia = make_float2((c1 * I1.x - c2 * I2.x) * ir2, (c1 * I1.y - c2 * I2.y) * ir2);
+          }
+          if (a > mm) {
+            I2 = I1;
+            I1 = Ia;
+          }
+          itab_tc[a * a + a + mm] = Ia;
+          itab_tc[a * a + a - mm] = make_float2(sg * Ia.x, -sg * Ia.y);
+        }
+      }
+    }
+    __syncthreads();
+    unsigned *hi = Timg + (size_t)gid * 2 * NT * NT, *lo = hi + (size_t)NT * NT;
+    for (int id = threadIdx.x; id < NT * NT; id += blockDim.x) {
+      const int row = id / NT, kd = id - row * NT;  // row = output dof, kd = input dof
+      float v = 0.f;
+      if (row < KD && kd < KD) {
+        // output dof -> (j, k_out, re/im); input dof -> (n, m, re/im)
+        int j = 0;
+        while ((j + 1) * (j + 1) <= row) ++j;
+        const int ro = row - j * j, ko = (ro + 1) / 2, rim = ro ? ((ro + 1) & 1) : 0;
+        int n = 0;
+        while ((n + 1) * (n + 1) <= kd) ++n;
+        const int ri = kd - n * n, m = (ri + 1) / 2, cim = ri ? ((ri + 1) & 1) : 0;
+        const float sgn = ((j + ko) & 1) ? -1.f : 1.f;
+        const float sc = sgn * (vform ? ldexpf(1.f, -dl * (j + 1)) : ldexpf(1.f, n * dl));
+        const int a = n + j;
+        const float2 Cp = itab_tc[a * a + a + (m - ko)];
+        if (m == 0) {
+          v = sc * (rim ? Cp.y : Cp.x);
+        } else {
+          const float2 Cm = itab_tc[a * a + a + (-m - ko)];
+          const float sm = (m & 1) ? -1.f : 1.f;
+          if (!cim)
+            v = sc * (rim ? (Cp.y + sm * Cm.y) : (Cp.x + sm * Cm.x));
+          else
+            v = sc * (rim ? (Cp.x - sm * Cm.x) : -(Cp.y - sm * Cm.y));
+        }
+      }
+      const unsigned vh = f32_to_tf32(v);
+      const unsigned vl = f32_to_tf32(v - __uint_as_float(vh));
+      const int off = (kd >> 2) * (NT * 4) + row * 4 + (kd & 3);  // core-matrix image (32-bit units)
+      hi[off] = vh;
+      lo[off] = vl;
+    }
+  }
+}
+
+template <int p>
+__global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ items,
+                                                   const int *__restrict__ counters,
+                                                   const unsigned *__restrict__ sidx,
+                                                   const unsigned *__restrict__ ssrc,
+                                                   const unsigned *__restrict__ Timg,
+                                                   const float *__restrict__ M,
+                                                   float *__restrict__ Y, int *queue) {
+  constexpr int KD = dof_of(p), NT = tc_dim(p);
+  constexpr int NC = nc_of(p), KR = 2 * NC, YS = (KR + 3) & ~3, MROW = 2 * nc_stride(p);
+  constexpr unsigned TBYTES = 2u * NT * NT * 4u;
+  // TMEM columns: Xh [0, NT), Xl [NT, 2NT), D [2NT, 3NT)
+  constexpr int TCOLS = 3 * NT <= 32 ? 32 : 3 * NT <= 64 ? 64 : 3 * NT <= 128 ? 128 : 3 * NT <= 256 ? 256 : 512;
+  static_assert(3 * NT <= 512, "TMEM budget");
+  extern __shared__ __align__(1024) unsigned char sh_tc[];
+  unsigned *Bimg = reinterpret_cast<unsigned *>(sh_tc);  // Th | Tl
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(sh_tc + TBYTES);
+  unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 4);
+  volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 5);
+  unsigned long long *t_full = &bars[0], *mma_done = &bars[1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_base_slot)),
+                 "n"(TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init_tc(t_full, 1);
+    mbar_init_tc(mma_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem = *tmem_base_slot;
+  const unsigned lane_base = (unsigned)(warp * 32) << 16;  // this warp's TMEM lane quarter
+  const unsigned tXh = tmem, tXl = tmem + NT, tD = tmem + 2 * NT;
+  // instruction descriptor: D F32, A/B TF32, K-major A and B, N = NT, M = 128
+  constexpr unsigned IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(NT >> 3) << 17) | (8u << 24);
+  const unsigned bh_addr = smem_addr(Bimg), bl_addr = bh_addr + (unsigned)(NT * NT * 4);
+
+  unsigned ph_t = 0, ph_m = 0;
+  const int nitems = counters[1];
+  for (;;) {
+    if (tid == 0) item_sh[0] = atomicAdd(queue, 1);
+    __syncthreads();
+    const int it = item_sh[0];
+    if (it >= nitems) break;
+    const int4 item = items[it];
+    const int pos0 = item.x, cnt = item.y, gid = item.w;
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx_tc(t_full, TBYTES);
+      bulk_g2s_tc(Bimg, Timg + (size_t)gid * 2 * NT * NT, TBYTES, t_full);
+    }
+    for (int c0 = 0; c0 < cnt; c0 += 128) {
+      const int row = c0 + tid;
+      const bool valid = row < cnt;
+      const float *Mr = M + (size_t)(valid ? ssrc[pos0 + row] : 0) * MROW;
+      // A operand: this pair's multipole row (16-byte loads), split into TF32 hi/lo in dof order,
+      // stored into TMEM lane `tid` (one row per thread)
+      float xf[MROW];
+#pragma unroll
+      for (int q = 0; q < MROW / 4; ++q) {
+        const float4 v4 = valid ? __ldg(reinterpret_cast<const float4 *>(Mr) + q)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        xf[4 * q] = v4.x;
+        xf[4 * q + 1] = v4.y;
+        xf[4 * q + 2] = v4.z;
+        xf[4 * q + 3] = v4.w;
+      }
+#pragma unroll
+      for (int cb = 0; cb < NT / 32; ++cb) {
+        unsigned vh[32], vl[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int d = cb * 32 + q;
+          const float x = d < KD ? xf[dof_to_float(d)] : 0.f;
+          vh[q] = f32_to_tf32(x);
+          vl[q] = f32_to_tf32(x - __uint_as_float(vh[q]));
+        }
+        tc_st32(tXh + lane_base + cb * 32, vh);
+        tc_st32(tXl + lane_base + cb * 32, vl);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncthreads();
+      if (c0 == 0) mbar_wait_tc(t_full, ph_t);  // class matrix landed (first tile of the item)
+      if (tid == 0) {
+        tc_fence_after();
+        for (int ks = 0; ks < NT / 8; ++ks) {
+          const unsigned long long bh = make_bdesc(bh_addr + ks * 2 * NT * 16, NT);
+          const unsigned long long bl = make_bdesc(bl_addr + ks * 2 * NT * 16, NT);
+          tc_mma_ts(tD, tXh + ks * 8, bh, IDESC, ks > 0 ? 1u : 0u);
+          tc_mma_ts(tD, tXh + ks * 8, bl, IDESC, 1u);
+          tc_mma_ts(tD, tXl + ks * 8, bh, IDESC, 1u);
+        }
+        tc_commit(mma_done);
+      }
+      mbar_wait_tc(mma_done, ph_m);
+      ph_m ^= 1;
+      tc_fence_after();
+      // epilogue: D row `tid` -> Y[pair], expanded back to the (m >= 0 complex) float layout and
+      // written as 16-byte stores (the Im part of every k = 0 output is zero by construction)
+      unsigned dv[NT];
+#pragma unroll
+      for (int cb = 0; cb < NT / 32; ++cb) {
+        unsigned v[32];
+        tc_ld32(tD + lane_base + cb * 32, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) dv[cb * 32 + q] = v[q];
+      }
+      tc_wait_ld();
+      if (valid) {
+        float4 *yr = reinterpret_cast<float4 *>(Y + (size_t)sidx[pos0 + row] * YS);
+#pragma unroll
+        for (int q = 0; q < YS / 4; ++q) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int f = 4 * q + e;
+            const int d = f < KR ? float_to_dof(f) : -1;
+            o[e] = d >= 0 ? __uint_as_float(dv[d]) : 0.f;
+          }
+          yr[q] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+      }
+      tc_fence_before();
+      __syncthreads();  // TMEM A / D are reused by the next tile
+    }
+    ph_t ^= 1;
+    __syncthreads();  // Bimg is reused by the next item
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS)
+                 : "memory");
+}
+
+// ---- host side ----------------------------------------------------------------------------------
+bool m2l_tc_supported(int p) { return p >= 1 && p <= 11; }
+size_t m2l_tc_T_words(int p) { return (size_t)2 * tc_dim(p) * tc_dim(p); }
+
+cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg, cudaStream_t st) {
+  if (ngclass <= 0) return cudaSuccess;
+  const size_t smem = (size_t)(2 * p + 1) * (2 * p + 1) * sizeof(float2);
+  k_m2l_build_T_tc<<<ngclass < 148 * 4 ? ngclass : 148 * 4, 256, smem, st>>>(
+      p, W.counters, W.class_rep, W.pair_t, W.src, W.C, Timg);
+  return cudaGetLastError();
+}
+
+cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
+                        cudaStream_t st) {
+  cudaMemsetAsync(W.counters + 4, 0, sizeof(int), st);
+#define M2L_TC_CASE(PP)                                                                        \
+  case PP: {                                                                                 \
+    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + 64;                        \
+    static bool cfg = false;                                                                 \
+    if (!cfg) {                                                                              \
+      cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      cfg = true;                                                                            \
+    }                                                                                        \
+    k_m2l_tc<PP><<<148, 128, smem, st>>>(W.items, W.counters, W.sidx, W.ssrc, Timg,           \
+                                        reinterpret_cast<const float *>(M), W.Y, W.counters + 4); \
+  } break;
+  switch (p) {
+    M2L_TC_CASE(1) M2L_TC_CASE(2) M2L_TC_CASE(3) M2L_TC_CASE(4) M2L_TC_CASE(5) M2L_TC_CASE(6)
+    M2L_TC_CASE(7) M2L_TC_CASE(8) M2L_TC_CASE(9) M2L_TC_CASE(10) M2L_TC_CASE(11)
+    default: break;
+  }
+#undef M2L_TC_CASE
+  return cudaGetLastError();
+}
