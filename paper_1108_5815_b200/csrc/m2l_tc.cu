@@ -4,7 +4,7 @@
 //     D[pair][out] = sum_k X[pair][k] * T[out][k]
 // over the real degrees of freedom of a real field: d = 0..(p+1)^2-1 enumerates
 // (n, m=0, Re), (n, m>0, Re), (n, m>0, Im) of every coefficient (the Im part of m = 0 is zero).
-// At p = 10 that is 121 -> padded to K = N = 128. FP32 accuracy comes from 3xTF32 splitting:
+// At p = 10 that is 121 -> padded to K = N = 128 (multiples of 32: TMEM is moved in 32-column chunks). FP32 accuracy comes from 3xTF32 splitting:
 //     X = Xh + Xl, T = Th + Tl (each part TF32), D = Xh Th + Xh Tl + Xl Th
 // (the dropped Xl Tl term is ~2^-22 relative), accumulated in FP32 in TMEM.
 //
@@ -25,7 +25,7 @@
 namespace {
 
 __host__ __device__ constexpr int dof_of(int p) { return (p + 1) * (p + 1); }
-__host__ __device__ constexpr int tc_dim(int p) { return (dof_of(p) + 15) & ~15; }  // K = N
+__host__ __device__ constexpr int tc_dim(int p) { return (dof_of(p) + 31) & ~31; }  // K = N, 32-column TMEM chunks
 
 // real degree of freedom d -> float index inside an (m >= 0, complex) expansion row.
 // Order of the dofs: for n = 0..p: (n,0,Re), then for m = 1..n: (n,m,Re), (n,m,Im).
