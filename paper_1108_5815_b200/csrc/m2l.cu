@@ -21,7 +21,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
-#define M2L_ITEM 1024
+#define M2L_ITEM 2048
 #define M2L_PREF 12  // float4 per thread staged for the next chunk (= max over p <= 12 of ceil(Kpad/4*64/threads))
 #define M2L_CHUNK 64
 #define M2L_SMALL 16

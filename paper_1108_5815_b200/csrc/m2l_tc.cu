@@ -237,6 +237,17 @@ __global__ void __launch_bounds__(256) k_m2l_build_T_tc(int p, const int *__rest
   }
 }
 
+__device__ __forceinline__ void cp_async16_tc(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_tc() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all_tc() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Pipelined per CTA (4 warps; thread i = TMEM lane i = pair i of the tile):
+//   X(i+1) rows stream into shared memory by cp.async while MMA(i) runs; after MMA(i) completes,
+//   X(i+1) is split into TF32 hi/lo and stored to TMEM, MMA(i+1) is issued into the other D
+//   buffer, and the epilogue of tile i (tcgen05.ld -> Y) overlaps MMA(i+1).
+// TMEM columns: Xh [0,NT) | Xl [NT,2NT) | D0 [2NT,3NT) | D1 [3NT,4NT)  (4 NT <= 512 -> p <= 10)
 template <int p>
 __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ items,
                                                    const int *__restrict__ counters,
@@ -248,21 +259,20 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   constexpr int KD = dof_of(p), NT = tc_dim(p);
   constexpr int NC = nc_of(p), KR = 2 * NC, YS = (KR + 3) & ~3, MROW = 2 * nc_stride(p);
   constexpr unsigned TBYTES = 2u * NT * NT * 4u;
-  // TMEM columns: Xh [0, NT), Xl [NT, 2NT), D [2NT, 3NT)
-  constexpr int TCOLS = 3 * NT <= 32 ? 32 : 3 * NT <= 64 ? 64 : 3 * NT <= 128 ? 128 : 3 * NT <= 256 ? 256 : 512;
-  static_assert(3 * NT <= 512, "TMEM budget");
+  static_assert(4 * NT <= 512, "TMEM budget");
   extern __shared__ __align__(1024) unsigned char sh_tc[];
-  unsigned *Bimg = reinterpret_cast<unsigned *>(sh_tc);  // Th | Tl
-  unsigned long long *bars = reinterpret_cast<unsigned long long *>(sh_tc + TBYTES);
+  unsigned *Bimg = reinterpret_cast<unsigned *>(sh_tc);                      // Th | Tl
+  float *Xst = reinterpret_cast<float *>(sh_tc + TBYTES);                     // [128][MROW]
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xst + 128 * MROW);
   unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 4);
   volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 5);
   unsigned long long *t_full = &bars[0], *mma_done = &bars[1];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(tmem_base_slot)),
-                 "n"(TCOLS)
+                 "n"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -275,11 +285,86 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   __syncthreads();
   tc_fence_after();
   const unsigned tmem = *tmem_base_slot;
-  const unsigned lane_base = (unsigned)(warp * 32) << 16;  // this warp's TMEM lane quarter
-  const unsigned tXh = tmem, tXl = tmem + NT, tD = tmem + 2 * NT;
-  // instruction descriptor: D F32, A/B TF32, K-major A and B, N = NT, M = 128
+  const unsigned lane_base = (unsigned)(warp * 32) << 16;
+  const unsigned tXh = tmem, tXl = tmem + NT;
   constexpr unsigned IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(NT >> 3) << 17) | (8u << 24);
   const unsigned bh_addr = smem_addr(Bimg), bl_addr = bh_addr + (unsigned)(NT * NT * 4);
+  float *myrow = Xst + tid * MROW;
+
+  // stage this thread's pair row of tile starting at c0 (zeros past the end)
+  auto stage = [&](int pos0, int cnt, int c0) {
+    const int row = c0 + tid;
+    if (row < cnt) {
+      const float *Mr = M + (size_t)ssrc[pos0 + row] * MROW;
+#pragma unroll
+      for (int q = 0; q < MROW / 4; ++q) cp_async16_tc(myrow + 4 * q, Mr + 4 * q);
+    }
+    cp_async_commit_tc();
+  };
+  // split the staged row into hi/lo and store it as TMEM lane `tid` of the A operand
+  auto load_A = [&](bool valid) {
+    cp_async_wait_all_tc();
+    float xf[MROW];  // the staged row, read with conflict-free 16-byte loads (odd # of slots)
+#pragma unroll
+    for (int q = 0; q < MROW / 4; ++q) {
+      const float4 v4 = reinterpret_cast<const float4 *>(myrow)[q];
+      xf[4 * q] = v4.x;
+      xf[4 * q + 1] = v4.y;
+      xf[4 * q + 2] = v4.z;
+      xf[4 * q + 3] = v4.w;
+    }
+#pragma unroll
+    for (int cb = 0; cb < NT / 32; ++cb) {
+      unsigned vh[32], vl[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int d = cb * 32 + q;
+        const float x = (d < KD && valid) ? xf[dof_to_float(d)] : 0.f;
+        vh[q] = f32_to_tf32(x);
+        vl[q] = f32_to_tf32(x - __uint_as_float(vh[q]));
+      }
+      tc_st32(tXh + lane_base + cb * 32, vh);
+      tc_st32(tXl + lane_base + cb * 32, vl);
+    }
+    tc_wait_st();
+  };
+  auto issue_mma = [&](unsigned tD) {  // one elected thread
+    tc_fence_after();
+    for (int ks = 0; ks < NT / 8; ++ks) {
+      const unsigned long long bh = make_bdesc(bh_addr + ks * 2 * NT * 16, NT);
+      const unsigned long long bl = make_bdesc(bl_addr + ks * 2 * NT * 16, NT);
+      tc_mma_ts(tD, tXh + ks * 8, bh, IDESC, ks > 0 ? 1u : 0u);
+      tc_mma_ts(tD, tXh + ks * 8, bl, IDESC, 1u);
+      tc_mma_ts(tD, tXl + ks * 8, bh, IDESC, 1u);
+    }
+    tc_commit(mma_done);
+  };
+  auto epilogue = [&](unsigned tD, int pos0, int cnt, int c0) {
+    const int row = c0 + tid;
+    unsigned dv[NT];
+#pragma unroll
+    for (int cb = 0; cb < NT / 32; ++cb) {
+      unsigned v[32];
+      tc_ld32(tD + lane_base + cb * 32, v);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) dv[cb * 32 + q] = v[q];
+    }
+    tc_wait_ld();
+    if (row < cnt) {
+      float4 *yr = reinterpret_cast<float4 *>(Y + (size_t)sidx[pos0 + row] * YS);
+#pragma unroll
+      for (int q = 0; q < YS / 4; ++q) {
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int f = 4 * q + e;
+          const int d = f < KR ? float_to_dof(f) : -1;
+          o[e] = d >= 0 ? __uint_as_float(dv[d]) : 0.f;
+        }
+        yr[q] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  };
 
   unsigned ph_t = 0, ph_m = 0;
   const int nitems = counters[1];
@@ -290,98 +375,47 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
     if (it >= nitems) break;
     const int4 item = items[it];
     const int pos0 = item.x, cnt = item.y, gid = item.w;
+    const int ntile = (cnt + 127) / 128;
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx_tc(t_full, TBYTES);
       bulk_g2s_tc(Bimg, Timg + (size_t)gid * 2 * NT * NT, TBYTES, t_full);
     }
-    for (int c0 = 0; c0 < cnt; c0 += 128) {
-      const int row = c0 + tid;
-      const bool valid = row < cnt;
-      const float *Mr = M + (size_t)(valid ? ssrc[pos0 + row] : 0) * MROW;
-      // A operand: this pair's multipole row (16-byte loads), split into TF32 hi/lo in dof order,
-      // stored into TMEM lane `tid` (one row per thread)
-      float xf[MROW];
-#pragma unroll
-      for (int q = 0; q < MROW / 4; ++q) {
-        const float4 v4 = valid ? __ldg(reinterpret_cast<const float4 *>(Mr) + q)
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-        xf[4 * q] = v4.x;
-        xf[4 * q + 1] = v4.y;
-        xf[4 * q + 2] = v4.z;
-        xf[4 * q + 3] = v4.w;
-      }
-#pragma unroll
-      for (int cb = 0; cb < NT / 32; ++cb) {
-        unsigned vh[32], vl[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const int d = cb * 32 + q;
-          const float x = d < KD ? xf[dof_to_float(d)] : 0.f;
-          vh[q] = f32_to_tf32(x);
-          vl[q] = f32_to_tf32(x - __uint_as_float(vh[q]));
-        }
-        tc_st32(tXh + lane_base + cb * 32, vh);
-        tc_st32(tXl + lane_base + cb * 32, vl);
-      }
-      tc_wait_st();
-      tc_fence_before();
-      __syncthreads();
-      if (c0 == 0) mbar_wait_tc(t_full, ph_t);  // class matrix landed (first tile of the item)
-      if (tid == 0) {
-        tc_fence_after();
-        for (int ks = 0; ks < NT / 8; ++ks) {
-          const unsigned long long bh = make_bdesc(bh_addr + ks * 2 * NT * 16, NT);
-          const unsigned long long bl = make_bdesc(bl_addr + ks * 2 * NT * 16, NT);
-          tc_mma_ts(tD, tXh + ks * 8, bh, IDESC, ks > 0 ? 1u : 0u);
-          tc_mma_ts(tD, tXh + ks * 8, bl, IDESC, 1u);
-          tc_mma_ts(tD, tXl + ks * 8, bh, IDESC, 1u);
-        }
-        tc_commit(mma_done);
-      }
-      mbar_wait_tc(mma_done, ph_m);
+    // prologue: tile 0
+    stage(pos0, cnt, 0);
+    load_A(tid < cnt);
+    tc_fence_before();
+    __syncthreads();
+    mbar_wait_tc(t_full, ph_t);
+    ph_t ^= 1;
+    if (tid == 0) issue_mma(tmem + 2 * NT);
+    for (int i = 0; i < ntile; ++i) {
+      const unsigned tDi = tmem + (2 + (i & 1)) * NT;
+      const bool more = i + 1 < ntile;
+      if (more) stage(pos0, cnt, (i + 1) * 128);  // streams in while MMA(i) runs
+      mbar_wait_tc(mma_done, ph_m);                // MMA(i) done: A free, D(i) ready
       ph_m ^= 1;
       tc_fence_after();
-      // epilogue: D row `tid` -> Y[pair], expanded back to the (m >= 0 complex) float layout and
-      // written as 16-byte stores (the Im part of every k = 0 output is zero by construction)
-      unsigned dv[NT];
-#pragma unroll
-      for (int cb = 0; cb < NT / 32; ++cb) {
-        unsigned v[32];
-        tc_ld32(tD + lane_base + cb * 32, v);
-#pragma unroll
-        for (int q = 0; q < 32; ++q) dv[cb * 32 + q] = v[q];
+      if (more) {
+        load_A((i + 1) * 128 + tid < cnt);
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) issue_mma(tmem + (2 + ((i + 1) & 1)) * NT);
       }
-      tc_wait_ld();
-      if (valid) {
-        float4 *yr = reinterpret_cast<float4 *>(Y + (size_t)sidx[pos0 + row] * YS);
-#pragma unroll
-        for (int q = 0; q < YS / 4; ++q) {
-          float o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int f = 4 * q + e;
-            const int d = f < KR ? float_to_dof(f) : -1;
-            o[e] = d >= 0 ? __uint_as_float(dv[d]) : 0.f;
-          }
-          yr[q] = make_float4(o[0], o[1], o[2], o[3]);
-        }
-      }
+      epilogue(tDi, pos0, cnt, i * 128);  // overlaps MMA(i+1)
       tc_fence_before();
-      __syncthreads();  // TMEM A / D are reused by the next tile
+      __syncthreads();
     }
-    ph_t ^= 1;
-    __syncthreads();  // Bimg is reused by the next item
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512)
                  : "memory");
 }
 
 // ---- host side ----------------------------------------------------------------------------------
-bool m2l_tc_supported(int p) { return p >= 1 && p <= 11; }
+bool m2l_tc_supported(int p) { return p >= 1 && p <= 10; }
 size_t m2l_tc_T_words(int p) { return (size_t)2 * tc_dim(p) * tc_dim(p); }
 
 cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg, cudaStream_t st) {
@@ -397,7 +431,7 @@ cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const flo
   cudaMemsetAsync(W.counters + 4, 0, sizeof(int), st);
 #define M2L_TC_CASE(PP)                                                                        \
   case PP: {                                                                                 \
-    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + 64;                        \
+    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + 64; \
     static bool cfg = false;                                                                 \
     if (!cfg) {                                                                              \
       cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
@@ -408,7 +442,7 @@ cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const flo
   } break;
   switch (p) {
     M2L_TC_CASE(1) M2L_TC_CASE(2) M2L_TC_CASE(3) M2L_TC_CASE(4) M2L_TC_CASE(5) M2L_TC_CASE(6)
-    M2L_TC_CASE(7) M2L_TC_CASE(8) M2L_TC_CASE(9) M2L_TC_CASE(10) M2L_TC_CASE(11)
+    M2L_TC_CASE(7) M2L_TC_CASE(8) M2L_TC_CASE(9) M2L_TC_CASE(10)
     default: break;
   }
 #undef M2L_TC_CASE
