@@ -477,17 +477,37 @@ __global__ void __launch_bounds__(128) k_m2l_pairs(int p, const unsigned *__rest
 }
 
 // ---- per-target sum of the pair slots, in list order -------------------------------------------
-__global__ void __launch_bounds__(128) k_m2l_reduce(int p, int ncells, const int *__restrict__ off,
+// warp per target; lane l sums float4 chunk l (and 32 + l) of the target's consecutive Y rows
+__global__ void __launch_bounds__(256) k_m2l_reduce(int p, int ncells, const int *__restrict__ off,
                                                     const int *__restrict__ cnt,
                                                     const float *__restrict__ Y,
                                                     float *__restrict__ L) {
-  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3;
-  for (int t = blockIdx.x; t < ncells; t += gridDim.x) {
+  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3, NQ = YS / 4;
+  const int LS = 2 * nc_stride(p);  // L row stride (floats), multiple of 4
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const float4 *Y4 = reinterpret_cast<const float4 *>(Y);
+  for (int t = gw; t < ncells; t += nw) {
     const int o = off[t], c = cnt[t];
-    for (int r = threadIdx.x; r < KR; r += blockDim.x) {
-      float s = 0.f;
-      for (int e = 0; e < c; ++e) s += Y[(size_t)(o + e) * YS + r];
-      L[(size_t)t * YS + r] = s;
+    for (int q0 = 0; q0 < NQ; q0 += 32) {
+      const int q = q0 + lane;
+      if (q >= NQ) break;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int e = 0; e < c; ++e) {
+        const float4 v = __ldg(&Y4[(size_t)(o + e) * NQ + q]);
+        s.x += v.x;
+        s.y += v.y;
+        s.z += v.z;
+        s.w += v.w;
+      }
+      float *lr = L + (size_t)t * LS + 4 * q;
+      if (4 * q + 3 < KR) {
+        *reinterpret_cast<float4 *>(lr) = s;
+      } else {
+        if (4 * q + 0 < KR) lr[0] = s.x;
+        if (4 * q + 1 < KR) lr[1] = s.y;
+        if (4 * q + 2 < KR) lr[2] = s.z;
+      }
     }
   }
 }
@@ -589,7 +609,10 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
     }
     k_m2l_pairs<<<148 * 4, 128, smem, st>>>(p, W.small, W.counters, W.pair_t, W.src, W.C, M, W.Y);
   }
-  k_m2l_reduce<<<ncells < 148 * 16 ? (ncells > 0 ? ncells : 1) : 148 * 16, 128, 0, st>>>(
-      p, ncells, W.off, W.cnt, W.Y, reinterpret_cast<float *>(L));
+  {
+    int b = (ncells + 7) / 8;
+    b = b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
+    k_m2l_reduce<<<b, 256, 0, st>>>(p, ncells, W.off, W.cnt, W.Y, reinterpret_cast<float *>(L));
+  }
   return cudaGetLastError();
 }

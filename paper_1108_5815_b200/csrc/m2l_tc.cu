@@ -266,8 +266,9 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xst + 128 * MROW);
   unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 4);
   volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 5);
-  unsigned long long *t_full = &bars[0], *mma_done = &bars[1];
+  unsigned long long *t_full = &bars[0], *mma_done = &bars[1], *x_full = &bars[2];
   const int tid = threadIdx.x, warp = tid >> 5;
+  unsigned ph_x = 0;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   if (tid == 0) {
     mbar_init_tc(t_full, 1);
     mbar_init_tc(mma_done, 1);
+    mbar_init_tc(x_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -291,19 +293,17 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   const unsigned bh_addr = smem_addr(Bimg), bl_addr = bh_addr + (unsigned)(NT * NT * 4);
   float *myrow = Xst + tid * MROW;
 
-  // stage this thread's pair row of tile starting at c0 (zeros past the end)
-  auto stage = [&](int pos0, int cnt, int c0) {
-    const int row = c0 + tid;
-    if (row < cnt) {
-      const float *Mr = M + (size_t)ssrc[pos0 + row] * MROW;
-#pragma unroll
-      for (int q = 0; q < MROW / 4; ++q) cp_async16_tc(myrow + 4 * q, Mr + 4 * q);
-    }
-    cp_async_commit_tc();
+  // stage this thread's pair row of the tile starting at c0: one TMA bulk copy per row (x_full
+  // counts the bytes); `s` is the row's source cell, fetched one tile ahead
+  auto stage = [&](int cnt, int c0, int s) {
+    const int nrows = min(128, cnt - c0);
+    if (tid == 0) mbar_expect_tx_tc(x_full, (unsigned)nrows * (unsigned)(MROW * 4));
+    if (c0 + tid < cnt) bulk_g2s_tc(myrow, M + (size_t)s * MROW, MROW * 4, x_full);
   };
   // split the staged row into hi/lo and store it as TMEM lane `tid` of the A operand
   auto load_A = [&](bool valid) {
-    cp_async_wait_all_tc();
+    mbar_wait_tc(x_full, ph_x);
+    ph_x ^= 1;
     float xf[MROW];  // the staged row, read with conflict-free 16-byte loads (odd # of slots)
 #pragma unroll
     for (int q = 0; q < MROW / 4; ++q) {
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
     }
     tc_commit(mma_done);
   };
-  auto epilogue = [&](unsigned tD, int pos0, int cnt, int c0) {
+  auto epilogue = [&](unsigned tD, int cnt, int c0, unsigned yslot) {
     const int row = c0 + tid;
     unsigned dv[NT];
 #pragma unroll
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
     }
     tc_wait_ld();
     if (row < cnt) {
-      float4 *yr = reinterpret_cast<float4 *>(Y + (size_t)sidx[pos0 + row] * YS);
+      float4 *yr = reinterpret_cast<float4 *>(Y + (size_t)yslot * YS);
 #pragma unroll
       for (int q = 0; q < YS / 4; ++q) {
         float o[4];
@@ -381,8 +381,11 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
       mbar_expect_tx_tc(t_full, TBYTES);
       bulk_g2s_tc(Bimg, Timg + (size_t)gid * 2 * NT * NT, TBYTES, t_full);
     }
-    // prologue: tile 0
-    stage(pos0, cnt, 0);
+    // prologue: tile 0 (source ids / output slots are fetched one tile ahead)
+    int s_cur = tid < cnt ? (int)ssrc[pos0 + tid] : 0;
+    int s_nxt = 128 + tid < cnt ? (int)ssrc[pos0 + 128 + tid] : 0;
+    unsigned y_cur = tid < cnt ? sidx[pos0 + tid] : 0u;
+    stage(cnt, 0, s_cur);
     load_A(tid < cnt);
     tc_fence_before();
     __syncthreads();
@@ -392,19 +395,26 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
     for (int i = 0; i < ntile; ++i) {
       const unsigned tDi = tmem + (2 + (i & 1)) * NT;
       const bool more = i + 1 < ntile;
-      if (more) stage(pos0, cnt, (i + 1) * 128);  // streams in while MMA(i) runs
-      mbar_wait_tc(mma_done, ph_m);                // MMA(i) done: A free, D(i) ready
+      // X(i+1) streams in while MMA(i) runs: the staging buffer was consumed by load_A(i)
+      if (more) stage(cnt, (i + 1) * 128, s_nxt);
+      const int r2 = (i + 2) * 128 + tid;
+      const int s_after = r2 < cnt ? (int)ssrc[pos0 + r2] : 0;
+      const int r1 = (i + 1) * 128 + tid;
+      const unsigned y_nxt = r1 < cnt ? sidx[pos0 + r1] : 0u;
+      mbar_wait_tc(mma_done, ph_m);  // MMA(i) done: A free, D(i) ready
       ph_m ^= 1;
       tc_fence_after();
       if (more) {
-        load_A((i + 1) * 128 + tid < cnt);
+        load_A(r1 < cnt);
         tc_fence_before();
         __syncthreads();
         if (tid == 0) issue_mma(tmem + (2 + ((i + 1) & 1)) * NT);
       }
-      epilogue(tDi, pos0, cnt, i * 128);  // overlaps MMA(i+1)
+      epilogue(tDi, cnt, i * 128, y_cur);  // overlaps MMA(i+1)
       tc_fence_before();
       __syncthreads();
+      s_nxt = s_after;
+      y_cur = y_nxt;
     }
   }
   tc_fence_before();
