@@ -265,23 +265,35 @@ def run_ours(args):
     m2l_gflops = stats["n_m2l"] * m2l_flops(p) / (m2l_ms * 1e-3) / 1e9 if m2l_ms > 0 else 0.0
     p2p_gflops = stats["p2p_pairs"] * P2P_FLOP_PER_PAIR / (p2p_ms * 1e-3) / 1e9 if p2p_ms > 0 else 0.0
     peak_gflops = N_SM * FP32_LANES_PER_SM * 2 * 1.965  # GFLOP/s at clocks.max.sm (B200_PROFILING)
-    if m2l_ms >= p2p_ms:
-        dom, ach, traffic_note = "m2l", m2l_gflops, "k_m2l"
-    else:
-        dom, ach, traffic_note = "p2p", p2p_gflops, "k_p2p_leaves"
-    traffic = None
+    # M2L runs on the tcgen05 tensor cores (3xTF32) for p <= 10: its roofline is the TF32 tensor
+    # peak = measured bf16 burst (MEASURED_PEAKS.json) x nominal tf32/bf16 ratio (1.1/2.25 PF)
+    tc_dim = ((p + 1) ** 2 + 31) // 32 * 32
+    m2l_tc_flops = 3 * 2 * tc_dim * tc_dim  # three TF32 MMAs per pair (hi.hi, hi.lo, lo.hi)
+    try:
+        bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+        tf32_src = "MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (nominal tf32/bf16)"
+    except (OSError, ValueError, KeyError):
+        bf16, tf32_src = 1590.0, "B200_PROFILING fallback 1.59 PF bf16 x 1.1/2.25"
+    tf32_peak = bf16 * 1.1 / 2.25
+    m2l_tensor_tflops = stats["n_m2l"] * m2l_tc_flops / (m2l_ms * 1e-3) / 1e12 if m2l_ms > 0 else 0.0
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(traffic_note)
-        except (OSError, ValueError):
-            traffic = None
-    roofline = {"bound": "alu", "kernel": dom, "achieved": ach / 1e3, "peak": peak_gflops / 1e3,
-                "unit": "TFLOP/s", "frac": ach / peak_gflops, "traffic": traffic,
-                "peak_source": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING nominal; "
-                               "tools/peak_fp32 measured 74.1 TFLOP/s FFMA2)",
-                "m2l_tflops": m2l_gflops / 1e3, "p2p_tflops": p2p_gflops / 1e3,
-                "m2l_flop_per_pair": m2l_flops(p), "p2p_flop_per_pair": P2P_FLOP_PER_PAIR}
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    p2p_line = {"bound": "alu", "kernel": "k_p2p_leaves", "achieved": p2p_gflops / 1e3,
+                "peak": peak_gflops / 1e3, "unit": "TFLOP/s", "frac": p2p_gflops / peak_gflops,
+                "traffic": traffic.get("k_p2p_leaves"),
+                "peak_source": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING unit counts x "
+                               "max clock); tools/peak_fp32 measured 74.0 TFLOP/s FFMA2",
+                "flop_per_pair": P2P_FLOP_PER_PAIR}
+    m2l_line = {"bound": "tensor", "kernel": "k_m2l_tc", "achieved": m2l_tensor_tflops,
+                "peak": tf32_peak, "unit": "TFLOP/s", "frac": m2l_tensor_tflops / tf32_peak,
+                "traffic": traffic.get("k_m2l_tc"), "peak_source": tf32_src,
+                "tf32_flop_per_pair": m2l_tc_flops, "fp32_equiv_tflops": m2l_gflops / 1e3,
+                "fp32_equiv_flop_per_pair": m2l_flops(p),
+                "note": "time includes the per-target reduction of the pair slots"}
+    if p2p_ms >= m2l_ms:
+        roofline = dict(p2p_line, secondary=m2l_line)
+    else:
+        roofline = dict(m2l_line, secondary=p2p_line)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
@@ -315,7 +327,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
