@@ -56,26 +56,29 @@ __device__ void regular_table(float x, float y, float z, int P, float2 *tab, int
 }
 
 // ---------------------------------------------------------------------------------------------
-// P2M: warp per leaf; lanes = particles; each coefficient reduced with a fixed butterfly.
+// P2M: warp per leaf; lane = particle. Each lane accumulates q conj(R(xi)) of its particles in
+// registers (all NC coefficients, templated p), then the warp sums the 32 lane vectors through a
+// padded shared-memory transpose (fixed order: deterministic).
 template <int p>
 __global__ void __launch_bounds__(128) k_p2m(const int *__restrict__ leaves, int nleaves,
                                              CellsView C, const float4 *__restrict__ pos,
                                              float2 *__restrict__ M) {
-  extern __shared__ float2 sh_p2m[];
-  constexpr int NC = nc_of(p), NCS = nc_stride(p);
+  constexpr int NC = nc_of(p), NCS = nc_stride(p), RS = 2 * NC + 1;  // odd row stride
+  extern __shared__ float sh_p2m[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float2 *acc = sh_p2m + wib * NC;
+  float *red = sh_p2m + wib * 32 * RS;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (int li = gw; li < nleaves; li += nw) {
     const int leaf = leaves[li];
     const float4 g = C.geo[leaf];
     const float rinv = 1.f / g.w;
     const int b = C.beg[leaf], cnt = C.cnt[leaf];
-    for (int o = lane; o < NC; o += WARP) acc[o] = make_float2(0.f, 0.f);
-    __syncwarp();
+    float acc[2 * NC];
+#pragma unroll
+    for (int o = 0; o < 2 * NC; ++o) acc[o] = 0.f;
     for (int c0 = 0; c0 < cnt; c0 += WARP) {
       const bool valid = c0 + lane < cnt;
-      float4 y = valid ? pos[b + c0 + lane] : make_float4(g.x, g.y, g.z, 0.f);
+      const float4 y = valid ? pos[b + c0 + lane] : make_float4(g.x, g.y, g.z, 0.f);
       const float x = (y.x - g.x) * rinv, yy = (y.y - g.y) * rinv, z = (y.z - g.z) * rinv;
       const float q = y.w;
       const float r2 = x * x + yy * yy + z * z;
@@ -98,20 +101,20 @@ __global__ void __launch_bounds__(128) k_p2m(const int *__restrict__ leaves, int
             R2 = R1;
             R1 = Rn;
           }
-          float vr = q * Rn.x, vi = -q * Rn.y;  // q conj(R)
-          for (int s = 16; s > 0; s >>= 1) {
-            vr += __shfl_xor_sync(0xffffffffu, vr, s);
-            vi += __shfl_xor_sync(0xffffffffu, vi, s);
-          }
-          if (lane == 0) {
-            float2 a = acc[cidx(n, m)];
-            acc[cidx(n, m)] = make_float2(a.x + vr, a.y + vi);
-          }
+          acc[2 * cidx(n, m)] += q * Rn.x;       // q conj(R)
+          acc[2 * cidx(n, m) + 1] -= q * Rn.y;
         }
       }
     }
     __syncwarp();
-    for (int o = lane; o < NC; o += WARP) M[(size_t)leaf * NCS + o] = acc[o];
+#pragma unroll
+    for (int o = 0; o < 2 * NC; ++o) red[lane * RS + o] = acc[o];
+    __syncwarp();
+    for (int o = lane; o < 2 * NC; o += WARP) {
+      float s = 0.f;
+      for (int l = 0; l < 32; ++l) s += red[l * RS + o];
+      reinterpret_cast<float *>(M + (size_t)leaf * NCS)[o] = s;
+    }
     __syncwarp();
   }
 }
@@ -427,8 +430,15 @@ M2LTiles make_m2l_tiles(int p) {
 void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos, float2 *M,
                 cudaStream_t st) {
   ensure_nm_table();
-  FMM_DISPATCH_P(p, (k_p2m<P_><<<warp_grid(nleaves, 4), 128, 4 * nc_of(P_) * sizeof(float2), st>>>(
-                        leaves, nleaves, C, pos, M)));
+  FMM_DISPATCH_P(p, ({
+    const size_t smem = 4 * 32 * (2 * nc_of(P_) + 1) * sizeof(float);
+    static bool cfg = false;
+    if (!cfg) {
+      cudaFuncSetAttribute(k_p2m<P_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cfg = true;
+    }
+    k_p2m<P_><<<warp_grid(nleaves, 4), 128, smem, st>>>(leaves, nleaves, C, pos, M);
+  }));
 }
 void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st) {
   ensure_nm_table();

@@ -153,8 +153,15 @@ __global__ void __launch_bounds__(256) k_m2l_build_T_tc(int p, const int *__rest
                                                         const unsigned *__restrict__ src,
                                                         CellsView C, unsigned *__restrict__ Timg) {
   extern __shared__ float2 itab_tc[];
+  __shared__ int dec[512];  // dof -> n | m << 6 | part << 12
   const int KD = dof_of(p), NT = tc_dim(p);
   const int ng = counters[3];
+  for (int d = threadIdx.x; d < KD; d += blockDim.x) {
+    int n = 0;
+    while ((n + 1) * (n + 1) <= d) ++n;
+    const int r = d - n * n, m = (r + 1) / 2, part = r ? ((r + 1) & 1) : 0;
+    dec[d] = n | (m << 6) | (part << 12);
+  }
   for (int gid = blockIdx.x; gid < ng; gid += gridDim.x) {
     const int rep = class_rep[gid];
     const int4 gt = C.grid[pair_t[rep]], gs = C.grid[src[rep]];
@@ -202,17 +209,15 @@ __global__ void __launch_bounds__(256) k_m2l_build_T_tc(int p, const int *__rest
     }
     __syncthreads();
     unsigned *hi = Timg + (size_t)gid * 2 * NT * NT, *lo = hi + (size_t)NT * NT;
-    for (int id = threadIdx.x; id < NT * NT; id += blockDim.x) {
-      const int row = id / NT, kd = id - row * NT;  // row = output dof, kd = input dof
+    // walk the image in memory order (coalesced stores); dof decodes come from the smem table
+    for (int off = threadIdx.x; off < NT * NT; off += blockDim.x) {
+      const int kq = off / (NT * 4), rem = off - kq * NT * 4;
+      const int row = rem >> 2, kd = kq * 4 + (rem & 3);  // row = output dof, kd = input dof
       float v = 0.f;
       if (row < KD && kd < KD) {
-        // output dof -> (j, k_out, re/im); input dof -> (n, m, re/im)
-        int j = 0;
-        while ((j + 1) * (j + 1) <= row) ++j;
-        const int ro = row - j * j, ko = (ro + 1) / 2, rim = ro ? ((ro + 1) & 1) : 0;
-        int n = 0;
-        while ((n + 1) * (n + 1) <= kd) ++n;
-        const int ri = kd - n * n, m = (ri + 1) / 2, cim = ri ? ((ri + 1) & 1) : 0;
+        const int dr = dec[row], dk = dec[kd];  // (n, m, part) packed
+        const int j = dr & 63, ko = (dr >> 6) & 63, rim = dr >> 12;
+        const int n = dk & 63, m = (dk >> 6) & 63, cim = dk >> 12;
         const float sgn = ((j + ko) & 1) ? -1.f : 1.f;
         const float sc = sgn * (vform ? ldexpf(1.f, -dl * (j + 1)) : ldexpf(1.f, n * dl));
         const int a = n + j;
@@ -229,10 +234,8 @@ __global__ void __launch_bounds__(256) k_m2l_build_T_tc(int p, const int *__rest
         }
       }
       const unsigned vh = f32_to_tf32(v);
-      const unsigned vl = f32_to_tf32(v - __uint_as_float(vh));
-      const int off = (kd >> 2) * (NT * 4) + row * 4 + (kd & 3);  // core-matrix image (32-bit units)
       hi[off] = vh;
-      lo[off] = vl;
+      lo[off] = f32_to_tf32(v - __uint_as_float(vh));
     }
   }
 }
