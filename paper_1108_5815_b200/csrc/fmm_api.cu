@@ -111,7 +111,12 @@ struct fmm_ctx {
   DBuf<unsigned> m2l_Ttc;
   bool m2l_tc_used = false;
   DBuf<int4> m2l_items;
-  DBuf<float> m2l_Y;
+  DBuf<float> m2l_Y;  // also the per-cell slots of the tensor-core M2M / L2L
+  // M2M / L2L as octant-class GEMMs on the tensor cores
+  DBuf<unsigned> sh_keys_in, sh_keys, sh_vals_in, sh_cells, sh_src, sh_T;
+  DBuf<int4> sh_items;
+  DBuf<int> sh_counters;
+  int sh_T_p = -1;
   // lists
   DBuf<int> loff[3], lcnt[3];
   DBuf<unsigned> lsrc[3];
@@ -412,10 +417,54 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   CK(h->M.ensure((size_t)h->ncells * NCS));
   CK(h->L.ensure((size_t)h->ncells * NCS));
   if (NCS != NC) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
+  // M2M / L2L: octant-class GEMMs on the tensor cores (p <= 10) unless disabled
+  const char *scc = getenv("FMM_SHIFT_CUDA_CORES");
+  const bool shift_tc = m2l_tc_supported(p) && h->ncells > 1 && !(scc && scc[0] && scc[0] != '0');
+  TcShiftWork S{};
+  if (shift_tc) {
+    const size_t tw = m2l_tc_T_words(p);
+    if (h->sh_T_p != p) {
+      CK(h->sh_T.ensure(16 * tw));
+      CK(tc_shift_build_ops(p, h->sh_T.p, h->sh_T.p + 8 * tw, st));
+      h->stats.launches += 1;
+      h->sh_T_p = p;
+    }
+    const int ns = h->ncells - 1;
+    S.items_per_level = 16 + h->ncells / 2048;
+    CK(h->sh_keys_in.ensure(ns));
+    CK(h->sh_keys.ensure(ns));
+    CK(h->sh_vals_in.ensure(ns));
+    CK(h->sh_cells.ensure(ns));
+    CK(h->sh_src.ensure(ns));
+    CK(h->sh_items.ensure((size_t)(FMM_LEVELS + 2) * S.items_per_level));
+    CK(h->sh_counters.ensure((size_t)(FMM_LEVELS + 2) * 8));
+    CK(h->cub_tmp.ensure(tc_shift_sort_bytes(ns)));
+    CK(h->m2l_Y.ensure((size_t)h->ncells * m2l_y_stride(p)));
+    S.keys_in = h->sh_keys_in.p;
+    S.keys = h->sh_keys.p;
+    S.vals_in = h->sh_vals_in.p;
+    S.cells = h->sh_cells.p;
+    S.src_l2l = h->sh_src.p;
+    S.items = h->sh_items.p;
+    S.lvl_counters = h->sh_counters.p;
+    S.Tm2m = h->sh_T.p;
+    S.Tl2l = h->sh_T.p + 8 * tw;
+    S.tmp = h->cub_tmp.p;
+    S.tmp_bytes = h->cub_tmp.cap;
+    CK(tc_shift_prepare(h->ncells, h->depth, S, h->cells(), st));
+    h->stats.launches += 3;
+    h->stats.cub_calls += 1;
+  }
   launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, st);
   CKL();
   for (int level = h->depth - 1; level >= 0; --level) {
-    launch_m2m(p, h->level_off[level], h->level_cnt[level], h->cells(), h->M.p, st);
+    if (shift_tc) {
+      CK(tc_shift_m2m_level(p, level, h->level_off[level], h->level_cnt[level], h->cells(), S,
+                            h->M.p, h->m2l_Y.p, st));
+      h->stats.launches += 2;
+    } else {
+      launch_m2m(p, h->level_off[level], h->level_cnt[level], h->cells(), h->M.p, st);
+    }
     CKL();
   }
   record(h, EV_UP);
@@ -506,7 +555,13 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   // a13 L2L top-down, a14/a15 L2P + combine + un-permute
   if (far_local) {
     for (int level = 1; level <= h->depth; ++level) {
-      launch_l2l(p, h->level_off[level], h->level_cnt[level], h->cells(), h->L.p, st);
+      if (shift_tc) {
+        CK(tc_shift_l2l_level(p, level, h->level_off[level], h->level_cnt[level], S, h->L.p,
+                              h->m2l_Y.p, st));
+        h->stats.launches += 2;
+      } else {
+        launch_l2l(p, h->level_off[level], h->level_cnt[level], h->cells(), h->L.p, st);
+      }
       CKL();
     }
   }
@@ -681,6 +736,8 @@ int fmm_destroy(fmm_t h) {
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
+  h->sh_keys_in.release(); h->sh_keys.release(); h->sh_vals_in.release(); h->sh_cells.release();
+  h->sh_src.release(); h->sh_T.release(); h->sh_items.release(); h->sh_counters.release();
   h->m2l_Y.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();

@@ -105,6 +105,28 @@ cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg,
 cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
                         cudaStream_t st);
 
+struct TcShiftWork {
+  unsigned *keys_in, *keys, *vals_in, *cells;  // (level<<3 | octant) sort of all non-root cells
+  unsigned *src_l2l;                           // per sorted position: L2L source (the parent)
+  int4 *items;                                 // [level][items_per_level]
+  int *lvl_counters;                           // [level][8]: [1] = #items, [4] = queue
+  int items_per_level;
+  unsigned *Tm2m, *Tl2l;                       // 8 octant operators each (tf32 hi/lo images)
+  void *tmp;
+  size_t tmp_bytes;
+};
+cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *queue,
+                          const unsigned *sidx, const unsigned *ssrc, const unsigned *Timg,
+                          const float2 *M, float *Y, int grid, cudaStream_t st);
+cudaError_t tc_shift_build_ops(int p, unsigned *Tm2m, unsigned *Tl2l, cudaStream_t st);
+size_t tc_shift_sort_bytes(int ncells);
+cudaError_t tc_shift_prepare(int ncells, int depth, const TcShiftWork &S, CellsView C,
+                             cudaStream_t st);
+cudaError_t tc_shift_m2m_level(int p, int level, int c0, int nl, CellsView C,
+                               const TcShiftWork &S, float2 *M, float *Y, cudaStream_t st);
+cudaError_t tc_shift_l2l_level(int p, int level, int c0, int nl, const TcShiftWork &S, float2 *L,
+                               float *Y, cudaStream_t st);
+
 // ---- p2p.cu ----
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
                        const float4 *pos, float4 *acc, int *counter, cudaStream_t st);

@@ -439,9 +439,10 @@ cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg,
   return cudaGetLastError();
 }
 
-cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
-                        cudaStream_t st) {
-  cudaMemsetAsync(W.counters + 4, 0, sizeof(int), st);
+cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *queue,
+                          const unsigned *sidx, const unsigned *ssrc, const unsigned *Timg,
+                          const float2 *M, float *Y, int grid, cudaStream_t st) {
+  cudaMemsetAsync(queue, 0, sizeof(int), st);
 #define M2L_TC_CASE(PP)                                                                        \
   case PP: {                                                                                 \
     const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + 64; \
@@ -450,8 +451,8 @@ cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const flo
       cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       cfg = true;                                                                            \
     }                                                                                        \
-    k_m2l_tc<PP><<<148, 128, smem, st>>>(W.items, W.counters, W.sidx, W.ssrc, Timg,           \
-                                        reinterpret_cast<const float *>(M), W.Y, W.counters + 4); \
+    k_m2l_tc<PP><<<grid, 128, smem, st>>>(items, counters, sidx, ssrc, Timg,                 \
+                                         reinterpret_cast<const float *>(M), Y, queue);      \
   } break;
   switch (p) {
     M2L_TC_CASE(1) M2L_TC_CASE(2) M2L_TC_CASE(3) M2L_TC_CASE(4) M2L_TC_CASE(5) M2L_TC_CASE(6)
@@ -459,5 +460,234 @@ cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const flo
     default: break;
   }
 #undef M2L_TC_CASE
+  return cudaGetLastError();
+}
+
+cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
+                        cudaStream_t st) {
+  return tc_class_gemm(p, W.items, W.counters, W.counters + 4, W.sidx, W.ssrc, Timg, M, W.Y, 148,
+                       st);
+}
+
+// ================================================================================================
+// M2M / L2L on the tensor cores. In the scaled form both shifts depend only on the octant of the
+// child (b/r_P = (+-1/2, +-1/2, +-1/2)), so each level is a class GEMM with 8 classes:
+//   M2M:  Y[child] = T^M2M_oct(child) Mhat[child];  Mhat[parent] = sum over its children of Y
+//   L2L:  Y[child] = T^L2L_oct(child) Lhat[parent]; Lhat[child] += Y[child]
+// The 16 operators are built once per handle by applying the shift formulas (expansions.cu
+// header) to the unit vectors of the real degrees of freedom.
+__device__ float2 sget_unit(int d, int n, int m) {  // unit vector e_d of the dofs, signed access
+  int nd = 0;
+  while ((nd + 1) * (nd + 1) <= d) ++nd;
+  const int r = d - nd * nd, md = (r + 1) / 2, im = r ? ((r + 1) & 1) : 0;
+  const int am = m < 0 ? -m : m;
+  if (n != nd || am != md) return make_float2(0.f, 0.f);
+  float2 v = im ? make_float2(0.f, 1.f) : make_float2(1.f, 0.f);
+  if (m < 0) v = (am & 1) ? make_float2(-v.x, v.y) : make_float2(v.x, -v.y);  // (-1)^m conj
+  return v;
+}
+
+// grid (8 octants, KD input dofs, 2 ops); block 128 threads over output coefficients
+__global__ void k_shift_basis(int p, unsigned *__restrict__ Tm2m, unsigned *__restrict__ Tl2l) {
+  const int o = blockIdx.x, d = blockIdx.y, op = blockIdx.z;
+  const int NC = nc_of(p), KD = dof_of(p), NT = tc_dim(p);
+  __shared__ float2 Rt[nc_of(FMM_PMAX)];
+  const float bx = ((o >> 2) & 1) ? 0.5f : -0.5f, by = ((o >> 1) & 1) ? 0.5f : -0.5f,
+              bz = (o & 1) ? 0.5f : -0.5f;
+  // regular harmonics R_n^m(b), m >= 0 (same recurrences as expansions.cu)
+  if (threadIdx.x <= p) {
+    const int m = threadIdx.x;
+    const float r2 = bx * bx + by * by + bz * bz;
+    float2 Rmm = make_float2(1.f, 0.f);
+    for (int k = 1; k <= m; ++k) {
+      const float tx = Rmm.x * bx - Rmm.y * by, ty = Rmm.x * by + Rmm.y * bx;
+      Rmm = make_float2(-tx / (2.f * k), -ty / (2.f * k));
+    }
+    Rt[cidx(m, m)] = Rmm;
+    float2 R2 = make_float2(0.f, 0.f), R1 = Rmm;
+    for (int n = m + 1; n <= p; ++n) {
+      float2 Rn;
+      if (n == m + 1) Rn = make_float2(Rmm.x * bz, Rmm.y * bz);
+      else {
+        const float inv = 1.f / ((float)(n - m) * (float)(n + m));
+        Rn = make_float2(((2 * n - 1) * bz * R1.x - r2 * R2.x) * inv, ((2 * n - 1) * bz * R1.y - r2 * R2.y) * inv);
+      }
+      Rt[cidx(n, m)] = Rn;
+      R2 = R1;
+      R1 = Rn;
+    }
+  }
+  __syncthreads();
+  unsigned *img = (op == 0 ? Tm2m : Tl2l) + (size_t)o * 2 * NT * NT;
+  for (int c = threadIdx.x; c < NC; c += blockDim.x) {
+    int n = 0;
+    while ((n + 1) * (n + 2) / 2 <= c) ++n;
+    const int m = c - n * (n + 1) / 2;
+    float2 a = make_float2(0.f, 0.f);
+    if (op == 0) {  // M2M: sum_{j<=n,k} e_d(j,k) 2^-j conj(R_{n-j}^{m-k})
+      float sc = 1.f;
+      for (int j = 0; j <= n; ++j, sc *= 0.5f) {
+        const int klo = max(-j, m - (n - j)), khi = min(j, m + (n - j));
+        for (int k = klo; k <= khi; ++k) {
+          const float2 e = sget_unit(d, j, k);
+          if (e.x == 0.f && e.y == 0.f) continue;
+          const float2 r = sget(Rt, n - j, m - k);
+          const float2 rc = make_float2(r.x, -r.y);
+          a.x += sc * (e.x * rc.x - e.y * rc.y);
+          a.y += sc * (e.x * rc.y + e.y * rc.x);
+        }
+      }
+    } else {  // L2L: 2^-(n+1) sum_{j>=n,k} e_d(j,k) R_{j-n}^{k-m}
+      for (int j = n; j <= p; ++j) {
+        const int klo = max(-j, m - (j - n)), khi = min(j, m + (j - n));
+        for (int k = klo; k <= khi; ++k) {
+          const float2 e = sget_unit(d, j, k);
+          if (e.x == 0.f && e.y == 0.f) continue;
+          const float2 r = sget(Rt, j - n, k - m);
+          a.x += e.x * r.x - e.y * r.y;
+          a.y += e.x * r.y + e.y * r.x;
+        }
+      }
+      const float sc = ldexpf(1.f, -(n + 1));
+      a.x *= sc;
+      a.y *= sc;
+    }
+    // output dofs of coefficient (n, m): Re -> row n^2 (m = 0) or n^2 + 2m - 1, Im -> n^2 + 2m
+    const int rows[2] = {m == 0 ? n * n : n * n + 2 * m - 1, m == 0 ? -1 : n * n + 2 * m};
+    const float vals[2] = {a.x, a.y};
+    for (int t = 0; t < 2; ++t) {
+      if (rows[t] < 0) continue;
+      const int off = (d >> 2) * (NT * 4) + rows[t] * 4 + (d & 3);
+      const unsigned vh = f32_to_tf32(vals[t]);
+      img[off] = vh;
+      img[(size_t)NT * NT + off] = f32_to_tf32(vals[t] - __uint_as_float(vh));
+    }
+  }
+  (void)KD;
+}
+
+// octant segments: the non-root cells sorted by (level << 3 | octant) give per level 8 contiguous
+// segments; a level's items are chunks of TC_SHIFT_ITEM cells of one segment (class = octant).
+// Output slots are the cell ids themselves (Y holds one row per cell).
+#define TC_SHIFT_ITEM 2048
+__global__ void k_shift_keys(int ncells, CellsView C, unsigned *keys, unsigned *vals) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells - 1) return;
+  const int cell = c + 1;  // the root has no parent
+  const int4 g = C.grid[cell], gp = C.grid[C.parent[cell]];
+  const unsigned oct = ((g.x > gp.x) << 2) | ((g.y > gp.y) << 1) | (g.z > gp.z);
+  keys[c] = ((unsigned)g.w << 3) | oct;
+  vals[c] = (unsigned)cell;
+}
+__global__ void k_shift_items(int nsorted, int depth, const unsigned *__restrict__ skeys,
+                              const unsigned *__restrict__ scell, const int *__restrict__ parent,
+                              int4 *__restrict__ items, int *__restrict__ lvl_counters,
+                              unsigned *__restrict__ src_l2l, int items_per_level) {
+  __shared__ int seg[(FMM_LEVELS + 2) * 8 + 1];
+  for (int k = threadIdx.x; k <= (FMM_LEVELS + 2) * 8; k += blockDim.x) {
+    int l = 0, r = nsorted;  // first sorted position with key >= k
+    while (l < r) {
+      const int mid = (l + r) >> 1;
+      if ((int)skeys[mid] < k) l = mid + 1;
+      else r = mid;
+    }
+    seg[k] = l;
+  }
+  __syncthreads();
+  for (int lv = threadIdx.x; lv <= depth; lv += blockDim.x) {
+    int ni = 0;
+    int4 *it = items + (size_t)lv * items_per_level;
+    for (int o = 0; o < 8; ++o) {
+      const int b = seg[lv * 8 + o], e = seg[lv * 8 + o + 1];
+      for (int a = b; a < e; a += TC_SHIFT_ITEM) it[ni++] = make_int4(a, min(TC_SHIFT_ITEM, e - a), 0, o);
+    }
+    lvl_counters[lv * 8 + 1] = ni;
+  }
+  for (int i = threadIdx.x; i < nsorted; i += blockDim.x) src_l2l[i] = (unsigned)parent[scell[i]];
+}
+
+// M2M: parent = sum of its children's slots (child order); L2L: child += its slot
+__global__ void __launch_bounds__(256) k_shift_m2m_reduce(int p, int c0, int nl, int child_off,
+                                                          CellsView C, const float *__restrict__ Y,
+                                                          float *__restrict__ M) {
+  (void)child_off;
+  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3, LS = 2 * nc_stride(p);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl * KR; i += gridDim.x * blockDim.x) {
+    const int k = i / KR, r = i - k * KR;
+    const int P = c0 + k, nch = C.nchild[P];
+    if (nch == 0) continue;
+    const int ch0 = C.child0[P];
+    float s = 0.f;
+    for (int c = 0; c < nch; ++c) s += Y[(size_t)(ch0 + c) * YS + r];
+    M[(size_t)P * LS + r] = s;
+  }
+}
+__global__ void __launch_bounds__(256) k_shift_l2l_add(int p, int c0, int nl,
+                                                       const float *__restrict__ Y,
+                                                       float *__restrict__ L) {
+  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3, LS = 2 * nc_stride(p);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl * KR; i += gridDim.x * blockDim.x) {
+    const int k = i / KR, r = i - k * KR;
+    L[(size_t)(c0 + k) * LS + r] += Y[(size_t)(c0 + k) * YS + r];
+  }
+}
+
+cudaError_t tc_shift_build_ops(int p, unsigned *Tm2m, unsigned *Tl2l, cudaStream_t st) {
+  cudaMemsetAsync(Tm2m, 0, sizeof(unsigned) * 8 * m2l_tc_T_words(p), st);
+  cudaMemsetAsync(Tl2l, 0, sizeof(unsigned) * 8 * m2l_tc_T_words(p), st);
+  k_shift_basis<<<dim3(8, dof_of(p), 2), 128, 0, st>>>(p, Tm2m, Tl2l);
+  return cudaGetLastError();
+}
+
+cudaError_t tc_shift_prepare(int ncells, int depth, const TcShiftWork &S, CellsView C,
+                             cudaStream_t st) {
+  const int ns = ncells - 1;
+  cudaMemsetAsync(S.lvl_counters, 0, sizeof(int) * 8 * (FMM_LEVELS + 2), st);
+  if (ns <= 0) return cudaGetLastError();
+  k_shift_keys<<<(ns + 255) / 256, 256, 0, st>>>(ncells, C, S.keys_in, S.vals_in);
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, S.keys_in, S.keys, S.vals_in,
+                                                  S.cells, ns, 0, 8, st);
+  if (e) return e;
+  if (bytes > S.tmp_bytes) return cudaErrorMemoryAllocation;
+  e = cub::DeviceRadixSort::SortPairs(S.tmp, bytes, S.keys_in, S.keys, S.vals_in, S.cells, ns, 0, 8,
+                                      st);
+  if (e) return e;
+  k_shift_items<<<1, 1024, 0, st>>>(ns, depth, S.keys, S.cells, C.parent, S.items, S.lvl_counters,
+                                    S.src_l2l, S.items_per_level);
+  return cudaGetLastError();
+}
+
+size_t tc_shift_sort_bytes(int ncells) {
+  size_t a = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned *)nullptr, (unsigned *)nullptr,
+                                  (unsigned *)nullptr, (unsigned *)nullptr, ncells, 0, 8);
+  return a;
+}
+
+cudaError_t tc_shift_m2m_level(int p, int level, int c0, int nl, CellsView C,
+                               const TcShiftWork &S, float2 *M, float *Y, cudaStream_t st) {
+  // children of this level's parents live at level + 1
+  const int lv = level + 1;
+  cudaError_t e = tc_class_gemm(p, S.items + (size_t)lv * S.items_per_level, S.lvl_counters + lv * 8,
+                                S.lvl_counters + lv * 8 + 4, S.cells, S.cells, S.Tm2m, M, Y, 148, st);
+  if (e) return e;
+  const int KR = 2 * nc_of(p);
+  int b = (nl * KR + 255) / 256;
+  b = b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
+  k_shift_m2m_reduce<<<b, 256, 0, st>>>(p, c0, nl, 0, C, Y, reinterpret_cast<float *>(M));
+  return cudaGetLastError();
+}
+
+cudaError_t tc_shift_l2l_level(int p, int level, int c0, int nl, const TcShiftWork &S, float2 *L,
+                               float *Y, cudaStream_t st) {
+  cudaError_t e = tc_class_gemm(p, S.items + (size_t)level * S.items_per_level,
+                                S.lvl_counters + level * 8, S.lvl_counters + level * 8 + 4, S.cells,
+                                S.src_l2l, S.Tl2l, L, Y, 148, st);
+  if (e) return e;
+  const int KR = 2 * nc_of(p);
+  int b = (nl * KR + 255) / 256;
+  b = b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
+  k_shift_l2l_add<<<b, 256, 0, st>>>(p, c0, nl, Y, reinterpret_cast<float *>(L));
   return cudaGetLastError();
 }
