@@ -25,6 +25,29 @@ __host__ __device__ __forceinline__ constexpr int cidx(int n, int m) { return n 
 // every row starts 16-byte aligned (TMA bulk copies); the pad entry is kept at zero.
 __host__ __device__ __forceinline__ constexpr int nc_stride(int p) { return (nc_of(p) + 1) & ~1; }
 
+// Real degrees of freedom of an expansion (the tensor-core paths): (p+1)^2 of them, ordered for
+// n = 0..p as (n,0,Re), then for m = 1..n: (n,m,Re), (n,m,Im). The Im part of m = 0 is zero.
+__host__ __device__ constexpr int dof_of(int p) { return (p + 1) * (p + 1); }
+__host__ __device__ constexpr int dof_stride(int p) { return (dof_of(p) + 3) & ~3; }  // Y rows
+// dof d -> float index inside an (m >= 0, complex) expansion row
+__host__ __device__ constexpr int dof_to_float(int d) {
+  int n = 0;
+  while ((n + 1) * (n + 1) <= d) ++n;
+  const int r = d - n * n;                      // 0 .. 2n
+  if (r == 0) return 2 * (n * (n + 1) / 2);     // Re of (n, 0)
+  const int m = (r + 1) / 2, im = (r + 1) & 1;  // r = 2m-1 -> Re, r = 2m -> Im
+  return 2 * (n * (n + 1) / 2 + m) + im;
+}
+// float index f -> dof, or -1 for the (zero) Im part of an m = 0 coefficient
+__host__ __device__ constexpr int float_to_dof(int f) {
+  const int c = f / 2, part = f & 1;
+  int n = 0;
+  while ((n + 1) * (n + 2) / 2 <= c) ++n;
+  const int m = c - n * (n + 1) / 2;
+  if (m == 0) return part ? -1 : n * n;
+  return n * n + 2 * m - 1 + part;
+}
+
 struct RootInfo {
   double origin[3];
   double L;       // power-of-two side of the root cube

@@ -105,7 +105,7 @@ struct fmm_ctx {
   DBuf<float2> M, L;
   // M2L class batching
   DBuf<int> m2l_pair_t, m2l_flag, m2l_cid, m2l_cstart, m2l_counters;
-  DBuf<unsigned long long> m2l_keys_in, m2l_keys;
+  DBuf<unsigned> m2l_keys_in, m2l_keys;
   DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep, m2l_ssrc;
   DBuf<float> m2l_T;
   DBuf<unsigned> m2l_Ttc;

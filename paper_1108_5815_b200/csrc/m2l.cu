@@ -16,6 +16,7 @@
 // Rare classes (< M2L_SMALL pairs) and orders p > 12 (T too large for shared memory) use
 // k_m2l_pairs: one warp per pair evaluating the double loop directly.
 #include <cub/cub.cuh>
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -110,36 +111,36 @@ __global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
 // Class key = (level difference, integer offset in units of the smaller cell); the source cell
 // id fills the low bits so that, after the radix sort, each class lists its pairs in source
 // order (consecutive source cells -> contiguous multipole rows -> one bulk copy per chunk).
-#define M2L_SRC_BITS 25
+// class key (24 bits, so the radix sort takes 3 passes): level difference and the integer offset
+// of the two centres in units of the smaller cell. Pairs outside that range get the reserved key
+// M2L_KEY_OWN and form classes of their own (evaluated by the direct per-pair path).
+#define M2L_KEY_BITS 24
+#define M2L_KEY_OWN 0xFFFFFFu
 __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
                           const unsigned *__restrict__ src, CellsView C,
-                          unsigned long long *__restrict__ keys, unsigned *__restrict__ idx) {
+                          unsigned *__restrict__ keys, unsigned *__restrict__ idx) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
     const unsigned s = src[e];
     const int4 gt = C.grid[pair_t[e]], gs = C.grid[s];
     const int dl = gt.w - gs.w;
     const int sh = FMM_LEVELS - max(gt.w, gs.w);
     const int dx = (gt.x - gs.x) >> sh, dy = (gt.y - gs.y) >> sh, dz = (gt.z - gs.z) >> sh;
-    const int lim = 1 << 10;
-    unsigned long long key;
-    if (abs(dx) < lim && abs(dy) < lim && abs(dz) < lim && s < (1u << M2L_SRC_BITS))
-      key = ((unsigned long long)(dl + 16) << 58) | ((unsigned long long)(dx + lim) << 47) |
-            ((unsigned long long)(dy + lim) << 36) | ((unsigned long long)(dz + lim) << 25) |
-            (unsigned long long)s;
-    else
-      key = (1ull << 63) | (unsigned long long)e;  // out of key range: a class of its own
+    unsigned key = M2L_KEY_OWN;
+    if (abs(dx) < 63 && abs(dy) < 63 && abs(dz) < 63 && dl >= -4 && dl <= 3)  // never all ones
+      key = ((unsigned)(dl + 4) << 21) | ((unsigned)(dx + 64) << 14) | ((unsigned)(dy + 64) << 7) |
+            (unsigned)(dz + 64);
     keys[e] = key;
     idx[e] = (unsigned)e;
   }
 }
 
-__global__ void k_m2l_class_flags(int npairs, const unsigned long long *__restrict__ skeys,
+__global__ void k_m2l_class_flags(int npairs, const unsigned *__restrict__ skeys,
                                   const unsigned *__restrict__ sidx,
                                   const unsigned *__restrict__ src, int *__restrict__ flag,
                                   unsigned *__restrict__ ssrc) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
-    const unsigned long long ck = skeys[i] >> M2L_SRC_BITS;  // class part of the key
-    flag[i] = (i == 0 || ck != (skeys[i - 1] >> M2L_SRC_BITS) || (skeys[i] >> 63)) ? 1 : 0;
+    const unsigned k = skeys[i];
+    flag[i] = (i == 0 || k != skeys[i - 1] || k == M2L_KEY_OWN) ? 1 : 0;
     ssrc[i] = src[sidx[i]];  // source cell in class-sorted order (one coalesced load later)
   }
 }
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(128) k_m2l_pairs(int p, const unsigned *__rest
                                                    const int *__restrict__ pair_t,
                                                    const unsigned *__restrict__ src, CellsView C,
                                                    const float2 *__restrict__ M,
-                                                   float *__restrict__ Y) {
+                                                   float *__restrict__ Y, int ydof) {
   extern __shared__ float2 sh_pairs[];
   const int NC = nc_of(p), KR = 2 * NC, YS = (KR + 3) & ~3;
   const int P2 = 2 * p, nI = (P2 + 1) * (P2 + 1), nM = (p + 1) * (p + 1);
@@ -470,37 +471,55 @@ __global__ void __launch_bounds__(128) k_m2l_pairs(int p, const unsigned *__rest
       }
       const float sgn = ((j + k) & 1) ? -1.f : 1.f;
       const float sc = sgn * (g.vform ? ldexpf(1.f, -g.dl * (j + 1)) : 1.f);
-      Y[(size_t)e * YS + 2 * o] = sc * re;
-      Y[(size_t)e * YS + 2 * o + 1] = (k == 0) ? 0.f : sc * im;
+      if (ydof) {  // tensor-core layout: dof order, stride dof_stride(p)
+        const int d = j * j + (k == 0 ? 0 : 2 * k - 1);
+        Y[(size_t)e * dof_stride(p) + d] = sc * re;
+        if (k > 0) Y[(size_t)e * dof_stride(p) + d + 1] = sc * im;
+      } else {
+        Y[(size_t)e * YS + 2 * o] = sc * re;
+        Y[(size_t)e * YS + 2 * o + 1] = (k == 0) ? 0.f : sc * im;
+      }
     }
   }
 }
 
 // ---- per-target sum of the pair slots, in list order -------------------------------------------
-// warp per target; lane l sums float4 chunk l (and 32 + l) of the target's consecutive Y rows
+// thread per (target, float4 column q): consecutive threads cover a target's row, so every load of
+// a warp is a contiguous piece of one or two Y rows; each column is summed in list order.
+// ydof: Y rows in dof order (tensor-core path), scattered into the float-order L row here.
 __global__ void __launch_bounds__(256) k_m2l_reduce(int p, int ncells, const int *__restrict__ off,
                                                     const int *__restrict__ cnt,
                                                     const float *__restrict__ Y,
-                                                    float *__restrict__ L) {
-  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3, NQ = YS / 4;
+                                                    float *__restrict__ L, int ydof) {
+  const int KR = 2 * nc_of(p), KD = dof_of(p);
+  const int YSr = ydof ? dof_stride(p) : ((KR + 3) & ~3), NQ = YSr / 4;
   const int LS = 2 * nc_stride(p);  // L row stride (floats), multiple of 4
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const float4 *Y4 = reinterpret_cast<const float4 *>(Y);
-  for (int t = gw; t < ncells; t += nw) {
+  const long long total = (long long)ncells * NQ;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(i / NQ), q = (int)(i - (long long)t * NQ);
     const int o = off[t], c = cnt[t];
-    for (int q0 = 0; q0 < NQ; q0 += 32) {
-      const int q = q0 + lane;
-      if (q >= NQ) break;
-      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int e = 0; e < c; ++e) {
-        const float4 v = __ldg(&Y4[(size_t)(o + e) * NQ + q]);
-        s.x += v.x;
-        s.y += v.y;
-        s.z += v.z;
-        s.w += v.w;
-      }
-      float *lr = L + (size_t)t * LS + 4 * q;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 *y = Y4 + (size_t)o * NQ + q;
+#pragma unroll 4
+    for (int e = 0; e < c; ++e) {
+      const float4 v = __ldcs(y + (size_t)e * NQ);
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    float *lr = L + (size_t)t * LS;
+    if (ydof) {
+      const float sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < KD) lr[dof_to_float(4 * q + e)] = sv[e];
+      if (q == 0)
+        for (int n = 0; n <= p; ++n) lr[2 * cidx(n, 0) + 1] = 0.f;
+    } else {
+      lr += 4 * q;
       if (4 * q + 3 < KR) {
         *reinterpret_cast<float4 *>(lr) = s;
       } else {
@@ -535,11 +554,11 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.keys_in, W.idx_in);
   size_t bytes = 0;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, W.idx_in,
-                                                  W.sidx, npairs, 0, 64, st);
+                                                  W.sidx, npairs, 0, M2L_KEY_BITS, st);
   if (e) return e;
   if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
   e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
-                                      64, st);
+                                      M2L_KEY_BITS, st);
   if (e) return e;
   k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.src, W.flag, W.ssrc);
   bytes = 0;
@@ -557,9 +576,8 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
 
 size_t m2l_temp_bytes(int npairs) {
   size_t a = 0, b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long *)nullptr,
-                                  (unsigned long long *)nullptr, (unsigned *)nullptr,
-                                  (unsigned *)nullptr, npairs, 0, 64);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned *)nullptr, (unsigned *)nullptr,
+                                  (unsigned *)nullptr, (unsigned *)nullptr, npairs, 0, M2L_KEY_BITS);
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, npairs);
   return a > b ? a : b;
 }
@@ -607,12 +625,15 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
       cudaFuncSetAttribute(k_m2l_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       configured = smem;
     }
-    k_m2l_pairs<<<148 * 4, 128, smem, st>>>(p, W.small, W.counters, W.pair_t, W.src, W.C, M, W.Y);
+    k_m2l_pairs<<<148 * 4, 128, smem, st>>>(p, W.small, W.counters, W.pair_t, W.src, W.C, M, W.Y,
+                                            gemm_done ? 1 : 0);
   }
   {
-    int b = (ncells + 7) / 8;
-    b = b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
-    k_m2l_reduce<<<b, 256, 0, st>>>(p, ncells, W.off, W.cnt, W.Y, reinterpret_cast<float *>(L));
+    const long long nthr = (long long)ncells * ((gemm_done ? dof_stride(p) : m2l_y_stride(p)) / 4);
+    int b = (int)std::min<long long>((nthr + 255) / 256, 148 * 16);
+    b = b > 0 ? b : 1;
+    k_m2l_reduce<<<b, 256, 0, st>>>(p, ncells, W.off, W.cnt, W.Y, reinterpret_cast<float *>(L),
+                                    gemm_done ? 1 : 0);
   }
   return cudaGetLastError();
 }

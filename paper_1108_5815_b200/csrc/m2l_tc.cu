@@ -24,28 +24,7 @@
 
 namespace {
 
-__host__ __device__ constexpr int dof_of(int p) { return (p + 1) * (p + 1); }
 __host__ __device__ constexpr int tc_dim(int p) { return (dof_of(p) + 31) & ~31; }  // K = N, 32-column TMEM chunks
-
-// real degree of freedom d -> float index inside an (m >= 0, complex) expansion row.
-// Order of the dofs: for n = 0..p: (n,0,Re), then for m = 1..n: (n,m,Re), (n,m,Im).
-__host__ __device__ constexpr int dof_to_float(int d) {
-  int n = 0;
-  while ((n + 1) * (n + 1) <= d) ++n;
-  const int r = d - n * n;                      // 0 .. 2n
-  if (r == 0) return 2 * (n * (n + 1) / 2);     // Re of (n, 0)
-  const int m = (r + 1) / 2, im = (r + 1) & 1;  // r = 2m-1 -> Re, r = 2m -> Im
-  return 2 * (n * (n + 1) / 2 + m) + im;
-}
-// float index f -> dof, or -1 for the (zero) Im part of an m = 0 coefficient
-__host__ __device__ constexpr int float_to_dof(int f) {
-  const int c = f / 2, part = f & 1;
-  int n = 0;
-  while ((n + 1) * (n + 2) / 2 <= c) ++n;
-  const int m = c - n * (n + 1) / 2;
-  if (m == 0) return part ? -1 : n * n;
-  return n * n + 2 * m - 1 + part;
-}
 
 __device__ __forceinline__ unsigned smem_addr(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -260,13 +239,14 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
                                                    const float *__restrict__ M,
                                                    float *__restrict__ Y, int *queue) {
   constexpr int KD = dof_of(p), NT = tc_dim(p);
-  constexpr int NC = nc_of(p), KR = 2 * NC, YS = (KR + 3) & ~3, MROW = 2 * nc_stride(p);
+  constexpr int YSD = dof_stride(p), MROW = 2 * nc_stride(p);
   constexpr unsigned TBYTES = 2u * NT * NT * 4u;
   static_assert(4 * NT <= 512, "TMEM budget");
   extern __shared__ __align__(1024) unsigned char sh_tc[];
   unsigned *Bimg = reinterpret_cast<unsigned *>(sh_tc);                      // Th | Tl
   float *Xst = reinterpret_cast<float *>(sh_tc + TBYTES);                     // [128][MROW]
-  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Xst + 128 * MROW);
+  float *Ep = Xst + 128 * MROW;                                                // [4][32][36]
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Ep + 4 * 32 * 36);
   unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 4);
   volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 5);
   unsigned long long *t_full = &bars[0], *mma_done = &bars[1], *x_full = &bars[2];
@@ -283,7 +263,7 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   if (tid == 0) {
     mbar_init_tc(t_full, 1);
     mbar_init_tc(mma_done, 1);
-    mbar_init_tc(x_full, 1);
+    mbar_init_tc(x_full, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -296,15 +276,21 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   const unsigned bh_addr = smem_addr(Bimg), bl_addr = bh_addr + (unsigned)(NT * NT * 4);
   float *myrow = Xst + tid * MROW;
 
-  // stage this thread's pair row of the tile starting at c0: one TMA bulk copy per row (x_full
-  // counts the bytes); `s` is the row's source cell, fetched one tile ahead
+  // stage this thread's pair row of the tile starting at c0: one TMA bulk copy per row. Every
+  // thread arrives on x_full (count 128; with its row's bytes when it has a row), so a phase can
+  // only complete after all threads have passed the previous one; `s` is the row's source cell
   auto stage = [&](int cnt, int c0, int s) {
-    const int nrows = min(128, cnt - c0);
-    if (tid == 0) mbar_expect_tx_tc(x_full, (unsigned)nrows * (unsigned)(MROW * 4));
-    if (c0 + tid < cnt) bulk_g2s_tc(myrow, M + (size_t)s * MROW, MROW * 4, x_full);
+    if (c0 + tid < cnt) {
+      mbar_expect_tx_tc(x_full, (unsigned)(MROW * 4));
+      bulk_g2s_tc(myrow, M + (size_t)s * MROW, MROW * 4, x_full);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(x_full)) : "memory");
+    }
   };
-  // split the staged row into hi/lo and store it as TMEM lane `tid` of the A operand
-  auto load_A = [&](bool valid) {
+  // split the staged row into hi/lo and store it as TMEM lane `tid` of the A operand. As soon as
+  // the row is in registers the staging row is refilled with the row of the tile after (`refill`),
+  // so its gather latency overlaps this tile's conversion, the epilogue and the next MMA.
+  auto load_A = [&](bool valid, int cnt, int c_next, int s_next) {
     mbar_wait_tc(x_full, ph_x);
     ph_x ^= 1;
     float xf[MROW];  // the staged row, read with conflict-free 16-byte loads (odd # of slots)
@@ -315,6 +301,10 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
       xf[4 * q + 1] = v4.y;
       xf[4 * q + 2] = v4.z;
       xf[4 * q + 3] = v4.w;
+    }
+    if (c_next < cnt) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      stage(cnt, c_next, s_next);
     }
 #pragma unroll
     for (int cb = 0; cb < NT / 32; ++cb) {
@@ -342,30 +332,33 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
     }
     tc_commit(mma_done);
   };
+  // epilogue: D rows (dof order) -> Y rows (dof order, stride YSD). Each warp transposes its 32
+  // rows through shared memory in 32-column chunks so that every store instruction writes four
+  // contiguous 128-byte row pieces (a thread-per-row store would touch 32 rows per instruction).
+  float *ep = Ep + warp * 32 * 36;
   auto epilogue = [&](unsigned tD, int cnt, int c0, unsigned yslot) {
-    const int row = c0 + tid;
-    unsigned dv[NT];
+    const int lane = tid & 31;
 #pragma unroll
     for (int cb = 0; cb < NT / 32; ++cb) {
       unsigned v[32];
       tc_ld32(tD + lane_base + cb * 32, v);
+      tc_wait_ld();
+      float4 *dst = reinterpret_cast<float4 *>(ep + lane * 36);
 #pragma unroll
-      for (int q = 0; q < 32; ++q) dv[cb * 32 + q] = v[q];
-    }
-    tc_wait_ld();
-    if (row < cnt) {
-      float4 *yr = reinterpret_cast<float4 *>(Y + (size_t)yslot * YS);
+      for (int j = 0; j < 8; ++j)
+        dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+      __syncwarp();
 #pragma unroll
-      for (int q = 0; q < YS / 4; ++q) {
-        float o[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int f = 4 * q + e;
-          const int d = f < KR ? float_to_dof(f) : -1;
-          o[e] = d >= 0 ? __uint_as_float(dv[d]) : 0.f;
-        }
-        yr[q] = make_float4(o[0], o[1], o[2], o[3]);
+      for (int k = 0; k < 8; ++k) {
+        const int r = 4 * k + (lane >> 3), c4 = lane & 7;
+        const unsigned ys = __shfl_sync(0xffffffffu, yslot, r);
+        const int col = cb * 32 + c4 * 4;
+        if (c0 + warp * 32 + r < cnt && col < YSD)
+          __stcs(reinterpret_cast<float4 *>(Y + (size_t)ys * YSD + col),
+                 reinterpret_cast<const float4 *>(ep + r * 36)[c4]);  // streamed: keep M, T in L2
       }
+      __syncwarp();
     }
   };
 
@@ -384,12 +377,14 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
       mbar_expect_tx_tc(t_full, TBYTES);
       bulk_g2s_tc(Bimg, Timg + (size_t)gid * 2 * NT * NT, TBYTES, t_full);
     }
-    // prologue: tile 0 (source ids / output slots are fetched one tile ahead)
-    int s_cur = tid < cnt ? (int)ssrc[pos0 + tid] : 0;
-    int s_nxt = 128 + tid < cnt ? (int)ssrc[pos0 + 128 + tid] : 0;
+    // prologue: tile 0. X rows stream two tiles ahead, so their source ids are loaded three
+    // tiles ahead (a dependent global load must not sit on the critical path); output slots one.
+    auto src_of = [&](int r) { return r < cnt ? (int)ssrc[pos0 + r] : 0; };
+    const int s_cur = src_of(tid), s_nxt = src_of(128 + tid);
+    int s_pf = src_of(256 + tid);
     unsigned y_cur = tid < cnt ? sidx[pos0 + tid] : 0u;
     stage(cnt, 0, s_cur);
-    load_A(tid < cnt);
+    load_A(tid < cnt, cnt, 128, s_nxt);
     tc_fence_before();
     __syncthreads();
     mbar_wait_tc(t_full, ph_t);
@@ -398,17 +393,15 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
     for (int i = 0; i < ntile; ++i) {
       const unsigned tDi = tmem + (2 + (i & 1)) * NT;
       const bool more = i + 1 < ntile;
-      // X(i+1) streams in while MMA(i) runs: the staging buffer was consumed by load_A(i)
-      if (more) stage(cnt, (i + 1) * 128, s_nxt);
-      const int r2 = (i + 2) * 128 + tid;
-      const int s_after = r2 < cnt ? (int)ssrc[pos0 + r2] : 0;
+      const int s_after = s_pf;  // tile i + 2
+      s_pf = src_of((i + 3) * 128 + tid);
       const int r1 = (i + 1) * 128 + tid;
       const unsigned y_nxt = r1 < cnt ? sidx[pos0 + r1] : 0u;
       mbar_wait_tc(mma_done, ph_m);  // MMA(i) done: A free, D(i) ready
       ph_m ^= 1;
       tc_fence_after();
       if (more) {
-        load_A(r1 < cnt);
+        load_A(r1 < cnt, cnt, (i + 2) * 128, s_after);  // X(i+1) -> TMEM, X(i+2) starts streaming
         tc_fence_before();
         __syncthreads();
         if (tid == 0) issue_mma(tmem + (2 + ((i + 1) & 1)) * NT);
@@ -416,7 +409,6 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
       epilogue(tDi, cnt, i * 128, y_cur);  // overlaps MMA(i+1)
       tc_fence_before();
       __syncthreads();
-      s_nxt = s_after;
       y_cur = y_nxt;
     }
   }
@@ -445,7 +437,7 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
   cudaMemsetAsync(queue, 0, sizeof(int), st);
 #define M2L_TC_CASE(PP)                                                                        \
   case PP: {                                                                                 \
-    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + 64; \
+    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + 4 * 32 * 36 * 4 + 64; \
     static bool cfg = false;                                                                 \
     if (!cfg) {                                                                              \
       cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
@@ -606,29 +598,33 @@ __global__ void k_shift_items(int nsorted, int depth, const unsigned *__restrict
   for (int i = threadIdx.x; i < nsorted; i += blockDim.x) src_l2l[i] = (unsigned)parent[scell[i]];
 }
 
-// M2M: parent = sum of its children's slots (child order); L2L: child += its slot
-__global__ void __launch_bounds__(256) k_shift_m2m_reduce(int p, int c0, int nl, int child_off,
-                                                          CellsView C, const float *__restrict__ Y,
+// M2M: parent = sum of its children's slots (child order); L2L: child += its slot. Y rows are in
+// dof order (stride dof_stride(p)); expansion rows in float order with Im(n, 0) = 0.
+__global__ void __launch_bounds__(256) k_shift_m2m_reduce(int p, int c0, int nl, CellsView C,
+                                                          const float *__restrict__ Y,
                                                           float *__restrict__ M) {
-  (void)child_off;
-  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3, LS = 2 * nc_stride(p);
+  const int KR = 2 * nc_of(p), YSD = dof_stride(p), LS = 2 * nc_stride(p);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl * KR; i += gridDim.x * blockDim.x) {
-    const int k = i / KR, r = i - k * KR;
+    const int k = i / KR, f = i - k * KR;
     const int P = c0 + k, nch = C.nchild[P];
     if (nch == 0) continue;
-    const int ch0 = C.child0[P];
+    const int d = float_to_dof(f);
     float s = 0.f;
-    for (int c = 0; c < nch; ++c) s += Y[(size_t)(ch0 + c) * YS + r];
-    M[(size_t)P * LS + r] = s;
+    if (d >= 0) {
+      const int ch0 = C.child0[P];
+      for (int c = 0; c < nch; ++c) s += Y[(size_t)(ch0 + c) * YSD + d];
+    }
+    M[(size_t)P * LS + f] = s;
   }
 }
 __global__ void __launch_bounds__(256) k_shift_l2l_add(int p, int c0, int nl,
                                                        const float *__restrict__ Y,
                                                        float *__restrict__ L) {
-  const int KR = 2 * nc_of(p), YS = (KR + 3) & ~3, LS = 2 * nc_stride(p);
+  const int KR = 2 * nc_of(p), YSD = dof_stride(p), LS = 2 * nc_stride(p);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nl * KR; i += gridDim.x * blockDim.x) {
-    const int k = i / KR, r = i - k * KR;
-    L[(size_t)(c0 + k) * LS + r] += Y[(size_t)(c0 + k) * YS + r];
+    const int k = i / KR, f = i - k * KR;
+    const int d = float_to_dof(f);
+    if (d >= 0) L[(size_t)(c0 + k) * LS + f] += Y[(size_t)(c0 + k) * YSD + d];
   }
 }
 
@@ -675,7 +671,7 @@ cudaError_t tc_shift_m2m_level(int p, int level, int c0, int nl, CellsView C,
   const int KR = 2 * nc_of(p);
   int b = (nl * KR + 255) / 256;
   b = b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
-  k_shift_m2m_reduce<<<b, 256, 0, st>>>(p, c0, nl, 0, C, Y, reinterpret_cast<float *>(M));
+  k_shift_m2m_reduce<<<b, 256, 0, st>>>(p, c0, nl, C, Y, reinterpret_cast<float *>(M));
   return cudaGetLastError();
 }
 
