@@ -225,13 +225,19 @@ __device__ __forceinline__ void cp_async16_tc(void *dst, const void *src) {
 __device__ __forceinline__ void cp_async_commit_tc() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all_tc() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Pipelined per CTA (4 warps; thread i = TMEM lane i = pair i of the tile):
-//   X(i+1) rows stream into shared memory by cp.async while MMA(i) runs; after MMA(i) completes,
-//   X(i+1) is split into TF32 hi/lo and stored to TMEM, MMA(i+1) is issued into the other D
-//   buffer, and the epilogue of tile i (tcgen05.ld -> Y) overlaps MMA(i+1).
+// Warp-specialised per CTA (160 threads):
+//   warps 0-3 ("row warps", thread i = TMEM lane i = pair row i of a 128-pair tile): stage their
+//     own X row by a TMA bulk copy, split it into TF32 hi/lo and store it as the A operand in
+//     TMEM, then read the previous tile's accumulator back (tcgen05.ld) and write it to Y;
+//   warp 4 (issuer): loads the class operator T (hi|lo) into shared memory by one TMA bulk copy
+//     per item and issues the 3xTF32 MMAs of each tile as soon as its A operand is in TMEM.
+// Barriers: x_full (128 arrivals + bytes: X rows staged), a_full (128: A stored), mma_done
+// (tcgen05.commit), t_full (bytes: T loaded). The row warps never wait for the MMA issue and the
+// issuer never waits for the epilogue, so MMA(i+1) overlaps the epilogue of tile i and the X
+// gather of tile i+2.
 // TMEM columns: Xh [0,NT) | Xl [NT,2NT) | D0 [2NT,3NT) | D1 [3NT,4NT)  (4 NT <= 512 -> p <= 10)
 template <int p>
-__global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ items,
+__global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ items,
                                                    const int *__restrict__ counters,
                                                    const unsigned *__restrict__ sidx,
                                                    const unsigned *__restrict__ ssrc,
@@ -249,9 +255,9 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
   unsigned long long *bars = reinterpret_cast<unsigned long long *>(Ep + 4 * 32 * 36);
   unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 4);
   volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 5);
-  unsigned long long *t_full = &bars[0], *mma_done = &bars[1], *x_full = &bars[2];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  unsigned ph_x = 0;
+  unsigned long long *t_full = &bars[0], *mma_done = &bars[1], *x_full = &bars[2], *a_full = &bars[3];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool issuer = warp == 4;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -264,152 +270,161 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4 *__restrict__ item
     mbar_init_tc(t_full, 1);
     mbar_init_tc(mma_done, 1);
     mbar_init_tc(x_full, 128);
+    mbar_init_tc(a_full, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const unsigned tmem = *tmem_base_slot;
-  const unsigned lane_base = (unsigned)(warp * 32) << 16;
   const unsigned tXh = tmem, tXl = tmem + NT;
   constexpr unsigned IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(NT >> 3) << 17) | (8u << 24);
-  const unsigned bh_addr = smem_addr(Bimg), bl_addr = bh_addr + (unsigned)(NT * NT * 4);
-  float *myrow = Xst + tid * MROW;
-
-  // stage this thread's pair row of the tile starting at c0: one TMA bulk copy per row. Every
-  // thread arrives on x_full (count 128; with its row's bytes when it has a row), so a phase can
-  // only complete after all threads have passed the previous one; `s` is the row's source cell
-  auto stage = [&](int cnt, int c0, int s) {
-    if (c0 + tid < cnt) {
-      mbar_expect_tx_tc(x_full, (unsigned)(MROW * 4));
-      bulk_g2s_tc(myrow, M + (size_t)s * MROW, MROW * 4, x_full);
-    } else {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(x_full)) : "memory");
-    }
-  };
-  // split the staged row into hi/lo and store it as TMEM lane `tid` of the A operand. As soon as
-  // the row is in registers the staging row is refilled with the row of the tile after (`refill`),
-  // so its gather latency overlaps this tile's conversion, the epilogue and the next MMA.
-  auto load_A = [&](bool valid, int cnt, int c_next, int s_next) {
-    mbar_wait_tc(x_full, ph_x);
-    ph_x ^= 1;
-    float xf[MROW];  // the staged row, read with conflict-free 16-byte loads (odd # of slots)
-#pragma unroll
-    for (int q = 0; q < MROW / 4; ++q) {
-      const float4 v4 = reinterpret_cast<const float4 *>(myrow)[q];
-      xf[4 * q] = v4.x;
-      xf[4 * q + 1] = v4.y;
-      xf[4 * q + 2] = v4.z;
-      xf[4 * q + 3] = v4.w;
-    }
-    if (c_next < cnt) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      stage(cnt, c_next, s_next);
-    }
-#pragma unroll
-    for (int cb = 0; cb < NT / 32; ++cb) {
-      unsigned vh[32], vl[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const int d = cb * 32 + q;
-        const float x = (d < KD && valid) ? xf[dof_to_float(d)] : 0.f;
-        vh[q] = f32_to_tf32(x);
-        vl[q] = f32_to_tf32(x - __uint_as_float(vh[q]));
-      }
-      tc_st32(tXh + lane_base + cb * 32, vh);
-      tc_st32(tXl + lane_base + cb * 32, vl);
-    }
-    tc_wait_st();
-  };
-  auto issue_mma = [&](unsigned tD) {  // one elected thread
-    tc_fence_after();
-    for (int ks = 0; ks < NT / 8; ++ks) {
-      const unsigned long long bh = make_bdesc(bh_addr + ks * 2 * NT * 16, NT);
-      const unsigned long long bl = make_bdesc(bl_addr + ks * 2 * NT * 16, NT);
-      tc_mma_ts(tD, tXh + ks * 8, bh, IDESC, ks > 0 ? 1u : 0u);
-      tc_mma_ts(tD, tXh + ks * 8, bl, IDESC, 1u);
-      tc_mma_ts(tD, tXl + ks * 8, bh, IDESC, 1u);
-    }
-    tc_commit(mma_done);
-  };
-  // epilogue: D rows (dof order) -> Y rows (dof order, stride YSD). Each warp transposes its 32
-  // rows through shared memory in 32-column chunks so that every store instruction writes four
-  // contiguous 128-byte row pieces (a thread-per-row store would touch 32 rows per instruction).
-  float *ep = Ep + warp * 32 * 36;
-  auto epilogue = [&](unsigned tD, int cnt, int c0, unsigned yslot) {
-    const int lane = tid & 31;
-#pragma unroll
-    for (int cb = 0; cb < NT / 32; ++cb) {
-      unsigned v[32];
-      tc_ld32(tD + lane_base + cb * 32, v);
-      tc_wait_ld();
-      float4 *dst = reinterpret_cast<float4 *>(ep + lane * 36);
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                             __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = 4 * k + (lane >> 3), c4 = lane & 7;
-        const unsigned ys = __shfl_sync(0xffffffffu, yslot, r);
-        const int col = cb * 32 + c4 * 4;
-        if (c0 + warp * 32 + r < cnt && col < YSD)
-          __stcs(reinterpret_cast<float4 *>(Y + (size_t)ys * YSD + col),
-                 reinterpret_cast<const float4 *>(ep + r * 36)[c4]);  // streamed: keep M, T in L2
-      }
-      __syncwarp();
-    }
-  };
-
-  unsigned ph_t = 0, ph_m = 0;
+  unsigned ph_x = 0, ph_m = 0, ph_a = 0, ph_t = 0;
   const int nitems = counters[1];
-  for (;;) {
-    if (tid == 0) item_sh[0] = atomicAdd(queue, 1);
-    __syncthreads();
-    const int it = item_sh[0];
-    if (it >= nitems) break;
-    const int4 item = items[it];
-    const int pos0 = item.x, cnt = item.y, gid = item.w;
-    const int ntile = (cnt + 127) / 128;
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx_tc(t_full, TBYTES);
-      bulk_g2s_tc(Bimg, Timg + (size_t)gid * 2 * NT * NT, TBYTES, t_full);
+
+  if (issuer) {
+    // ---------------------------------------------------------------- MMA issuer (one lane)
+    const unsigned bh_addr = smem_addr(Bimg), bl_addr = bh_addr + (unsigned)(NT * NT * 4);
+    for (;;) {
+      if (tid == 128) item_sh[0] = atomicAdd(queue, 1);
+      __syncthreads();
+      const int it = item_sh[0];
+      __syncthreads();  // item_sh is rewritten for the next item only after everyone read it
+      if (it >= nitems) break;
+      const int4 item = items[it];
+      const int ntile = (item.y + 127) / 128;
+      if (lane == 0) {
+        // T of this item: every MMA of the previous item has completed (the row warps waited
+        // for its last commit before the item barrier above)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx_tc(t_full, TBYTES);
+        bulk_g2s_tc(Bimg, Timg + (size_t)item.w * 2 * NT * NT, TBYTES, t_full);
+        mbar_wait_tc(t_full, ph_t);
+        ph_t ^= 1;
+        for (int i = 0; i < ntile; ++i) {
+          mbar_wait_tc(a_full, ph_a);  // A(i) in TMEM, D(i & 1) drained by the epilogue
+          ph_a ^= 1;
+          tc_fence_after();
+          const unsigned tD = tmem + (2 + (i & 1)) * NT;
+#pragma unroll
+          for (int ks = 0; ks < NT / 8; ++ks) {
+            const unsigned long long bh = make_bdesc(bh_addr + ks * 2 * NT * 16, NT);
+            const unsigned long long bl = make_bdesc(bl_addr + ks * 2 * NT * 16, NT);
+            tc_mma_ts(tD, tXh + ks * 8, bh, IDESC, ks > 0 ? 1u : 0u);
+            tc_mma_ts(tD, tXh + ks * 8, bl, IDESC, 1u);
+            tc_mma_ts(tD, tXl + ks * 8, bh, IDESC, 1u);
+          }
+          tc_commit(mma_done);
+        }
+      }
+      __syncwarp();
     }
-    // prologue: tile 0. X rows stream two tiles ahead, so their source ids are loaded three
-    // tiles ahead (a dependent global load must not sit on the critical path); output slots one.
-    auto src_of = [&](int r) { return r < cnt ? (int)ssrc[pos0 + r] : 0; };
-    const int s_cur = src_of(tid), s_nxt = src_of(128 + tid);
-    int s_pf = src_of(256 + tid);
-    unsigned y_cur = tid < cnt ? sidx[pos0 + tid] : 0u;
-    stage(cnt, 0, s_cur);
-    load_A(tid < cnt, cnt, 128, s_nxt);
-    tc_fence_before();
-    __syncthreads();
-    mbar_wait_tc(t_full, ph_t);
-    ph_t ^= 1;
-    if (tid == 0) issue_mma(tmem + 2 * NT);
-    for (int i = 0; i < ntile; ++i) {
-      const unsigned tDi = tmem + (2 + (i & 1)) * NT;
-      const bool more = i + 1 < ntile;
-      const int s_after = s_pf;  // tile i + 2
-      s_pf = src_of((i + 3) * 128 + tid);
-      const int r1 = (i + 1) * 128 + tid;
-      const unsigned y_nxt = r1 < cnt ? sidx[pos0 + r1] : 0u;
-      mbar_wait_tc(mma_done, ph_m);  // MMA(i) done: A free, D(i) ready
+  } else {
+    // ---------------------------------------------------------------- row warps
+    const unsigned lane_base = (unsigned)(warp * 32) << 16;
+    float *myrow = Xst + tid * MROW;
+    float *ep = Ep + warp * 32 * 36;
+    // own row of the tile starting at c0 -> staging (every thread arrives on x_full, with its
+    // row's bytes when it has one, so a phase completes only after all passed the previous one)
+    auto stage = [&](int cnt, int c0, int s) {
+      if (c0 + tid < cnt) {
+        mbar_expect_tx_tc(x_full, (unsigned)(MROW * 4));
+        bulk_g2s_tc(myrow, M + (size_t)s * MROW, MROW * 4, x_full);
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(x_full)) : "memory");
+      }
+    };
+    // D rows (dof order) -> Y rows (dof order, stride YSD), transposed through shared memory in
+    // 32-column chunks: every store instruction writes four contiguous 128-byte row pieces
+    auto epilogue = [&](unsigned tD, int cnt, int c0, unsigned yslot) {
+#pragma unroll
+      for (int cb = 0; cb < NT / 32; ++cb) {
+        unsigned v[32];
+        tc_ld32(tD + lane_base + cb * 32, v);
+        tc_wait_ld();
+        float4 *dst = reinterpret_cast<float4 *>(ep + lane * 36);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = 4 * k + (lane >> 3), c4 = lane & 7;
+          const unsigned ys = __shfl_sync(0xffffffffu, yslot, r);
+          const int col = cb * 32 + c4 * 4;
+          if (c0 + warp * 32 + r < cnt && col < YSD)
+            __stcs(reinterpret_cast<float4 *>(Y + (size_t)ys * YSD + col),
+                   reinterpret_cast<const float4 *>(ep + r * 36)[c4]);  // streamed: keep M, T in L2
+        }
+        __syncwarp();
+      }
+    };
+    for (;;) {
+      __syncthreads();  // the issuer fetched the next item
+      const int it = item_sh[0];
+      __syncthreads();
+      if (it >= nitems) break;
+      const int4 item = items[it];
+      const int pos0 = item.x, cnt = item.y;
+      const int ntile = (cnt + 127) / 128;
+      auto src_of = [&](int r) { return r < cnt ? (int)ssrc[pos0 + r] : 0; };
+      int s_pf = src_of(128 + tid);  // source of the next tile's row (loaded a tile ahead)
+      unsigned y_prev = 0u, y_cur = tid < cnt ? sidx[pos0 + tid] : 0u;
+      stage(cnt, 0, src_of(tid));
+      for (int i = 0; i < ntile; ++i) {
+        const int r0 = i * 128 + tid;
+        const int s_next = s_pf;
+        s_pf = src_of(r0 + 256);
+        const unsigned y_next = r0 + 128 < cnt ? sidx[pos0 + r0 + 128] : 0u;
+        // X(i): own row -> registers; the staging row is refilled with X(i+1) at once
+        mbar_wait_tc(x_full, ph_x);
+        ph_x ^= 1;
+        float xf[MROW];
+#pragma unroll
+        for (int q = 0; q < MROW / 4; ++q) {
+          const float4 v4 = reinterpret_cast<const float4 *>(myrow)[q];
+          xf[4 * q] = v4.x;
+          xf[4 * q + 1] = v4.y;
+          xf[4 * q + 2] = v4.z;
+          xf[4 * q + 3] = v4.w;
+        }
+        if (i + 1 < ntile) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          stage(cnt, (i + 1) * 128, s_next);
+        }
+        if (i > 0) {  // MMA(i-1) done: A free, D((i-1) & 1) ready
+          mbar_wait_tc(mma_done, ph_m);
+          ph_m ^= 1;
+          tc_fence_after();
+        }
+        const bool valid = r0 < cnt;
+#pragma unroll
+        for (int cb = 0; cb < NT / 32; ++cb) {
+          unsigned vh[32], vl[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int d = cb * 32 + q;
+            const float x = (d < KD && valid) ? xf[dof_to_float(d)] : 0.f;
+            vh[q] = f32_to_tf32(x);
+            vl[q] = f32_to_tf32(x - __uint_as_float(vh[q]));
+          }
+          tc_st32(tXh + lane_base + cb * 32, vh);
+          tc_st32(tXl + lane_base + cb * 32, vl);
+        }
+        tc_wait_st();
+        tc_fence_before();
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(a_full)) : "memory");
+        if (i > 0) epilogue(tmem + (2 + ((i - 1) & 1)) * NT, cnt, (i - 1) * 128, y_prev);
+        y_prev = y_cur;
+        y_cur = y_next;
+      }
+      // last tile
+      mbar_wait_tc(mma_done, ph_m);
       ph_m ^= 1;
       tc_fence_after();
-      if (more) {
-        load_A(r1 < cnt, cnt, (i + 2) * 128, s_after);  // X(i+1) -> TMEM, X(i+2) starts streaming
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) issue_mma(tmem + (2 + ((i + 1) & 1)) * NT);
-      }
-      epilogue(tDi, cnt, i * 128, y_cur);  // overlaps MMA(i+1)
+      epilogue(tmem + (2 + ((ntile - 1) & 1)) * NT, cnt, (ntile - 1) * 128, y_prev);
       tc_fence_before();
-      __syncthreads();
-      y_cur = y_nxt;
     }
   }
   tc_fence_before();
@@ -443,7 +458,7 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
       cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       cfg = true;                                                                            \
     }                                                                                        \
-    k_m2l_tc<PP><<<grid, 128, smem, st>>>(items, counters, sidx, ssrc, Timg,                 \
+    k_m2l_tc<PP><<<grid, 160, smem, st>>>(items, counters, sidx, ssrc, Timg,                 \
                                          reinterpret_cast<const float *>(M), Y, queue);      \
   } break;
   switch (p) {
