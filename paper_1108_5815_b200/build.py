@@ -23,17 +23,20 @@ def stale() -> bool:
     return os.path.getmtime(LIB) < max(os.path.getmtime(d) for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, jobs: int = 8, out: str | None = None,
+          extra: list[str] | None = None) -> str:
+    """Build libfmm.so (or `out` with `extra` nvcc flags, e.g. a -DFMM_TC_PROF instrumented copy)."""
+    lib = out or LIB
+    if out is None and not force and not stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if out is None else "build_alt")
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + FLAGS
+        cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + FLAGS + (extra or [])
         log = open(obj + ".log", "w")
         procs.append((subprocess.Popen(cmd, stdout=log, stderr=subprocess.STDOUT), obj, log))
     ok = True
@@ -45,11 +48,11 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
         ok &= pr.returncode == 0
     if not ok:
         raise RuntimeError("nvcc failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-o", tmp] + objs +
                           ["-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "shared"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -247,15 +247,17 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
   constexpr int KD = dof_of(p), NT = tc_dim(p);
   constexpr int YSD = dof_stride(p), MROW = 2 * nc_stride(p);
   constexpr unsigned TBYTES = 2u * NT * NT * 4u;
+  constexpr int KH = (NT / 32 + 1) / 2;  // 32-column chunks of A's first K half
   static_assert(4 * NT <= 512, "TMEM budget");
   extern __shared__ __align__(1024) unsigned char sh_tc[];
   unsigned *Bimg = reinterpret_cast<unsigned *>(sh_tc);                      // Th | Tl
   float *Xst = reinterpret_cast<float *>(sh_tc + TBYTES);                     // [128][MROW]
   float *Ep = Xst + 128 * MROW;                                                // [4][32][36]
   unsigned long long *bars = reinterpret_cast<unsigned long long *>(Ep + 4 * 32 * 36);
-  unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 4);
-  volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 5);
-  unsigned long long *t_full = &bars[0], *mma_done = &bars[1], *x_full = &bars[2], *a_full = &bars[3];
+  unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 6);
+  volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 7);
+  unsigned long long *t_full = &bars[0], *mma_done = &bars[1], *x_full = &bars[2];
+  unsigned long long *a_full = &bars[3], *mma_h0 = &bars[5];  // a_full[2]: the two K halves of A
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool issuer = warp == 4;
 
@@ -271,6 +273,8 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
     mbar_init_tc(mma_done, 1);
     mbar_init_tc(x_full, 128);
     mbar_init_tc(a_full, 128);
+    mbar_init_tc(a_full + 1, 128);
+    mbar_init_tc(mma_h0, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   tc_fence_before();
@@ -302,19 +306,23 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
         mbar_wait_tc(t_full, ph_t);
         ph_t ^= 1;
         for (int i = 0; i < ntile; ++i) {
-          mbar_wait_tc(a_full, ph_a);  // A(i) in TMEM, D(i & 1) drained by the epilogue
-          ph_a ^= 1;
-          tc_fence_after();
           const unsigned tD = tmem + (2 + (i & 1)) * NT;
+          // two K halves: the row warps refill A's first half while the second half multiplies
 #pragma unroll
-          for (int ks = 0; ks < NT / 8; ++ks) {
-            const unsigned long long bh = make_bdesc(bh_addr + ks * 2 * NT * 16, NT);
-            const unsigned long long bl = make_bdesc(bl_addr + ks * 2 * NT * 16, NT);
-            tc_mma_ts(tD, tXh + ks * 8, bh, IDESC, ks > 0 ? 1u : 0u);
-            tc_mma_ts(tD, tXh + ks * 8, bl, IDESC, 1u);
-            tc_mma_ts(tD, tXl + ks * 8, bh, IDESC, 1u);
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait_tc(a_full + h, ph_a);  // A(i) half h in TMEM (D(i & 1) drained)
+            tc_fence_after();
+#pragma unroll
+            for (int ks = (h ? KH * 4 : 0); ks < (h ? NT / 8 : KH * 4); ++ks) {
+              const unsigned long long bh = make_bdesc(bh_addr + ks * 2 * NT * 16, NT);
+              const unsigned long long bl = make_bdesc(bl_addr + ks * 2 * NT * 16, NT);
+              tc_mma_ts(tD, tXh + ks * 8, bh, IDESC, ks > 0 ? 1u : 0u);
+              tc_mma_ts(tD, tXh + ks * 8, bl, IDESC, 1u);
+              tc_mma_ts(tD, tXl + ks * 8, bh, IDESC, 1u);
+            }
+            tc_commit(h ? mma_done : mma_h0);
           }
-          tc_commit(mma_done);
+          ph_a ^= 1;
         }
       }
       __syncwarp();
@@ -393,33 +401,43 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           stage(cnt, (i + 1) * 128, s_next);
         }
-        if (i > 0) {  // MMA(i-1) done: A free, D((i-1) & 1) ready
-          mbar_wait_tc(mma_done, ph_m);
-          ph_m ^= 1;
-          tc_fence_after();
-        }
         const bool valid = r0 < cnt;
+        // A(i) in two K halves: half 0 once MMA(i-1) has consumed its half 0 (mma_h0), half 1
+        // once MMA(i-1) has completed (mma_done; D((i-1) & 1) is then ready as well)
 #pragma unroll
-        for (int cb = 0; cb < NT / 32; ++cb) {
-          unsigned vh[32], vl[32];
-#pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const int d = cb * 32 + q;
-            const float x = (d < KD && valid) ? xf[dof_to_float(d)] : 0.f;
-            vh[q] = f32_to_tf32(x);
-            vl[q] = f32_to_tf32(x - __uint_as_float(vh[q]));
+        for (int h = 0; h < 2; ++h) {
+          if (i > 0) {
+            mbar_wait_tc(h ? mma_done : mma_h0, ph_m);
+            tc_fence_after();
           }
-          tc_st32(tXh + lane_base + cb * 32, vh);
-          tc_st32(tXl + lane_base + cb * 32, vl);
+#pragma unroll
+          for (int cb = (h ? KH : 0); cb < (h ? NT / 32 : KH); ++cb) {
+            unsigned vh[32], vl[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const int d = cb * 32 + q;
+              const float x = (d < KD && valid) ? xf[dof_to_float(d < KD ? d : 0)] : 0.f;
+              // x = hi + lo, hi = x truncated to TF32 (exact); lo = x - hi is exact in FP32 and
+              // the tensor core reads its top 10 mantissa bits: 2 instructions, not the 10 of a
+              // rounding cvt.rna.tf32 (which sm_100a emulates)
+              vh[q] = __float_as_uint(x) & 0xFFFFE000u;
+              vl[q] = __float_as_uint(x - __uint_as_float(vh[q]));
+            }
+            tc_st32(tXh + lane_base + cb * 32, vh);
+            tc_st32(tXl + lane_base + cb * 32, vl);
+          }
+          tc_wait_st();
+          tc_fence_before();
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(a_full + h))
+                       : "memory");
         }
-        tc_wait_st();
-        tc_fence_before();
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(a_full)) : "memory");
+        if (i > 0) ph_m ^= 1;
         if (i > 0) epilogue(tmem + (2 + ((i - 1) & 1)) * NT, cnt, (i - 1) * 128, y_prev);
         y_prev = y_cur;
         y_cur = y_next;
       }
       // last tile
+      mbar_wait_tc(mma_h0, ph_m);
       mbar_wait_tc(mma_done, ph_m);
       ph_m ^= 1;
       tc_fence_after();
@@ -452,7 +470,7 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
   cudaMemsetAsync(queue, 0, sizeof(int), st);
 #define M2L_TC_CASE(PP)                                                                        \
   case PP: {                                                                                 \
-    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + 4 * 32 * 36 * 4 + 64; \
+    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + 4 * 32 * 36 * 4 + 128; \
     static bool cfg = false;                                                                 \
     if (!cfg) {                                                                              \
       cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
