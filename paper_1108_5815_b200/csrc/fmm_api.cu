@@ -71,6 +71,7 @@ struct fmm_ctx {
   fmm_cost_t cost{};
   fmm_stats_t stats{};
   bool timing = false;
+  bool deterministic = false;  // fmm_set_deterministic
   cudaEvent_t ev[EV_N] = {};
   std::string err;
   M2LTiles tiles{};
@@ -106,7 +107,7 @@ struct fmm_ctx {
   // M2L class batching
   DBuf<int> m2l_pair_t, m2l_flag, m2l_cid, m2l_cstart, m2l_counters;
   DBuf<unsigned> m2l_keys_in, m2l_keys;
-  DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep, m2l_ssrc;
+  DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep, m2l_ssrc, m2l_stgt;
   DBuf<float> m2l_T;
   DBuf<unsigned> m2l_Ttc;
   bool m2l_tc_used = false;
@@ -124,6 +125,8 @@ struct fmm_ctx {
   DBuf<int> out_off, out_cnt, cnt4, excl4;
   DBuf<unsigned> outA, outB, stack;
   int stack_cap = 2048;
+  size_t trav_cap[4] = {0, 0, 0, 0};  // list buffer sizes seen so far (traverse)
+  int *d_bk = nullptr;                // device bookkeeping of the traversal (TravArgs::bk)
   int64_t ntask[3] = {0, 0, 0};
   bool have_tree = false;
   int64_t last_n = 0;
@@ -311,6 +314,10 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
 
 // ---- a9: traversal ----------------------------------------------------------------------------
 static int traverse(fmm_ctx *h) {
+  // Level-synchronous target-centric traversal (traverse.cu). All bookkeeping stays on the
+  // device: list buffers are sized from the previous evaluation (or an estimate), the write pass
+  // of a level whose lists would not fit does nothing, and one read-back at the end decides
+  // whether to re-run with larger buffers (stack or lists) -- no host round trip per level.
   cudaStream_t st = h->stream;
   const int nc = h->ncells;
   for (int k = 0; k < 3; ++k) {
@@ -324,86 +331,104 @@ static int traverse(fmm_ctx *h) {
   const int warps_per_block = 4;
   const int grid_blocks = 148 * 8;
   const size_t nwarps = (size_t)grid_blocks * warps_per_block;
-restart:
-  CK(h->stack.ensure(nwarps * h->stack_cap));
-  CK(cudaMemsetAsync(h->d_overflow, 0, sizeof(unsigned), st));
-  CK(cudaMemsetAsync(h->d_stats, 0, 2 * sizeof(unsigned long long), st));
-  int64_t base[3] = {0, 0, 0};
-  unsigned *in_src = nullptr;
-  DBuf<unsigned> *outbuf[2] = {&h->outA, &h->outB};
-  for (int level = 0; level <= h->depth; ++level) {
-    const int nt = h->level_cnt[level], t0 = h->level_off[level];
-    CK(h->cnt4.ensure((size_t)4 * nt));
-    CK(h->excl4.ensure((size_t)4 * nt));
-    TravArgs A{};
-    A.C = h->cells();
-    A.t0 = t0;
-    A.nt = nt;
-    A.level = level;
-    A.mode = h->mode;
-    A.stack_cap = h->stack_cap;
-    A.grid_blocks = std::min(grid_blocks, (nt + warps_per_block - 1) / warps_per_block);
-    A.tlo = h->part_lo;
-    A.thi = h->part_hi;
-    A.theta = h->theta;
-    A.t_pp = h->cost.t_pp;
-    A.t_mp = h->cost.t_mp;
-    A.t_ml = h->cost.t_ml;
-    A.in_src = in_src;
-    A.in_off = h->out_off.p;
-    A.in_cnt = h->out_cnt.p;
-    A.scratch = h->stack.p;
-    A.overflow = h->d_overflow;
-    A.cnt4 = h->cnt4.p;
-    A.excl = h->excl4.p;
-    A.stats = h->d_stats;
-    launch_traverse(A, false, st);
-    CKL();
-    if (int rc = cub_scan(h, h->cnt4.p, h->excl4.p, 4 * nt)) return rc;
-    launch_trav_totals(h->excl4.p, h->cnt4.p, nt, h->d_small, st);
-    CKL();
-    CK(cudaMemcpyAsync(h->h_small, h->d_small, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h->h_small + 8, h->d_overflow, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  int maxnt = 1;
+  for (int level = 0; level <= h->depth; ++level) maxnt = std::max(maxnt, h->level_cnt[level]);
+  CK(h->cnt4.ensure((size_t)4 * maxnt));
+  CK(h->excl4.ensure((size_t)4 * maxnt));
+  // capacities: at least the previous evaluation's totals, else an estimate per target cell
+  size_t cap[4];
+  for (int k = 0; k < 4; ++k) {
+    const size_t est = (size_t)256 * nc + 1024;
+    cap[k] = std::max(est, h->trav_cap[k]);
+    cap[k] = std::min(cap[k], (size_t)INT32_MAX - 1);
+  }
+  for (int attempt = 0;; ++attempt) {
+    CK(h->stack.ensure(nwarps * h->stack_cap));
+    for (int k = 0; k < 3; ++k) CK(h->lsrc[k].ensure(cap[k]));
+    CK(h->p2p_rng.ensure(cap[2]));
+    CK(h->outA.ensure(cap[3]));
+    CK(h->outB.ensure(cap[3]));
+    int hb[20] = {0};
+    for (int k = 0; k < 4; ++k) hb[8 + k] = (int)cap[k];
+    CK(cudaMemcpyAsync(h->d_bk, hb, sizeof hb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(h->d_overflow, 0, sizeof(unsigned), st));
+    CK(cudaMemsetAsync(h->d_stats, 0, 2 * sizeof(unsigned long long), st));
+    unsigned *in_src = nullptr;
+    DBuf<unsigned> *outbuf[2] = {&h->outA, &h->outB};
+    for (int level = 0; level <= h->depth; ++level) {
+      const int nt = h->level_cnt[level], t0 = h->level_off[level];
+      TravArgs A{};
+      A.C = h->cells();
+      A.t0 = t0;
+      A.nt = nt;
+      A.level = level;
+      A.mode = h->mode;
+      A.stack_cap = h->stack_cap;
+      A.grid_blocks = std::min(grid_blocks, (nt + warps_per_block - 1) / warps_per_block);
+      A.tlo = h->part_lo;
+      A.thi = h->part_hi;
+      A.theta = h->theta;
+      A.t_pp = h->cost.t_pp;
+      A.t_mp = h->cost.t_mp;
+      A.t_ml = h->cost.t_ml;
+      A.in_src = in_src;
+      A.in_off = h->out_off.p;
+      A.in_cnt = h->out_cnt.p;
+      A.scratch = h->stack.p;
+      A.overflow = h->d_overflow;
+      A.cnt4 = h->cnt4.p;
+      A.excl = h->excl4.p;
+      A.stats = h->d_stats;
+      A.bk = h->d_bk;
+      for (int k = 0; k < 3; ++k) {
+        A.lsrc[k] = h->lsrc[k].p;
+        A.loff[k] = h->loff[k].p;
+        A.lcnt[k] = h->lcnt[k].p;
+      }
+      A.p2p_rng = h->p2p_rng.p;
+      DBuf<unsigned> *ob = outbuf[level & 1];
+      A.out_src = ob->p;
+      A.out_off = h->out_off.p;
+      A.out_cnt = h->out_cnt.p;
+      launch_traverse(A, false, st);
+      CKL();
+      if (int rc = cub_scan(h, h->cnt4.p, h->excl4.p, 4 * nt)) return rc;
+      launch_trav_totals(h->excl4.p, h->cnt4.p, nt, h->d_bk, st);
+      CKL();
+      launch_traverse(A, true, st);
+      CKL();
+      in_src = ob->p;
+    }
+    int hb2[20];
+    unsigned ovf = 0;
+    unsigned long long hs[2];
+    CK(cudaMemcpyAsync(hb2, h->d_bk, sizeof hb2, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ovf, h->d_overflow, sizeof ovf, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hs, h->d_stats, sizeof hs, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (h->h_small[8]) {
+    if (ovf) {  // a warp's traversal stack overflowed: larger stacks, again
       h->stack_cap *= 2;
       if ((size_t)h->stack_cap * nwarps > ((size_t)1 << 31))
         return fail(h, FMM_E_OOM, "traversal stack exceeds 8 GiB");
-      goto restart;
+      continue;
     }
-    int tot[4];
-    for (int c = 0; c < 4; ++c) {
-      tot[c] = h->h_small[4 + c];
-      A.excl_base[c] = h->h_small[c];
+    if (hb2[12]) {  // a list buffer was too small: grow to what the count passes have seen so far
+      if (attempt > 8) return fail(h, FMM_E_OOM, "interaction lists do not fit");
+      for (int k = 0; k < 4; ++k) {
+        const size_t need = (size_t)(k < 3 ? hb2[16 + k] : 0);
+        cap[k] = std::min((size_t)INT32_MAX - 1, std::max(cap[k] * 2, need + need / 4 + 1024));
+      }
+      continue;
     }
     for (int k = 0; k < 3; ++k) {
-      if (base[k] + tot[k] > INT32_MAX) return fail(h, FMM_E_OOM, "interaction list exceeds 2^31 entries");
-      CK(h->lsrc[k].ensure_keep((size_t)(base[k] + tot[k]) + 1, (size_t)base[k], st));
-      A.lsrc[k] = h->lsrc[k].p;
-      A.loff[k] = h->loff[k].p;
-      A.lcnt[k] = h->lcnt[k].p;
-      A.base[k] = (int)base[k];
+      h->ntask[k] = hb2[16 + k];
+      h->trav_cap[k] = std::max(h->trav_cap[k], (size_t)hb2[16 + k] + 1);
     }
-    CK(h->p2p_rng.ensure_keep((size_t)(base[2] + tot[2]) + 1, (size_t)base[2], st));
-    A.p2p_rng = h->p2p_rng.p;
-    DBuf<unsigned> *ob = outbuf[level & 1];
-    CK(ob->ensure((size_t)tot[3] + 1));
-    A.out_src = ob->p;
-    A.out_off = h->out_off.p;
-    A.out_cnt = h->out_cnt.p;
-    A.base[3] = 0;
-    launch_traverse(A, true, st);
-    CKL();
-    for (int k = 0; k < 3; ++k) base[k] += tot[k];
-    in_src = ob->p;
+    h->trav_cap[3] = std::max(h->trav_cap[3], cap[3]);
+    h->stats.p2p_pairs = (int64_t)hs[0];
+    h->stats.m2p_evals = (int64_t)hs[1];
+    return FMM_OK;
   }
-  for (int k = 0; k < 3; ++k) h->ntask[k] = base[k];
-  unsigned long long hs[2];
-  CK(cudaMemcpyAsync(hs, h->d_stats, sizeof hs, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  h->stats.p2p_pairs = (int64_t)hs[0];
-  h->stats.m2p_evals = (int64_t)hs[1];
-  return FMM_OK;
 }
 
 static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
@@ -486,7 +511,11 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(h->m2l_counters.ensure(8));
     CK(h->m2l_items.ensure((size_t)np + 1));
     CK(h->m2l_small.ensure(np));
-    CK(h->m2l_Y.ensure((size_t)np * m2l_y_stride(p)));
+    // tensor-core GEMMs accumulate straight into L unless bit-reproducibility is requested
+    const char *cc = getenv("FMM_M2L_CUDA_CORES");
+    const bool use_tc = m2l_gemm_supported(p) && m2l_tc_supported(p) && !(cc && cc[0] && cc[0] != '0');
+    const bool accum = use_tc && !h->deterministic;
+    if (!accum) CK(h->m2l_Y.ensure((size_t)np * m2l_y_stride(p)));
     CK(h->cub_tmp.ensure(m2l_temp_bytes(np)));
     M2LWork W{};
     W.C = h->cells();
@@ -512,6 +541,10 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(h->m2l_ssrc.ensure(np));
     W.class_rep = h->m2l_class_rep.p;
     W.ssrc = h->m2l_ssrc.p;
+    if (accum) {
+      CK(h->m2l_stgt.ensure(np));
+      W.stgt = h->m2l_stgt.p;
+    }
     CK(m2l_prepare(W, np, h->ncells, st));
     h->stats.launches += 6;
     h->stats.cub_calls += 2;
@@ -519,8 +552,6 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(cudaStreamSynchronize(st));
     const int ngclass = h->h_small[3];
     // class GEMMs on the tensor cores (tcgen05, 3xTF32) unless disabled / unsupported
-    const char *cc = getenv("FMM_M2L_CUDA_CORES");
-    const bool use_tc = !W.direct_all && m2l_tc_supported(p) && !(cc && cc[0] && cc[0] != '0');
     if (use_tc) {
       CK(h->m2l_Ttc.ensure((size_t)std::max(1, ngclass) * m2l_tc_T_words(p)));
       CK(m2l_tc_build_T(p, W, ngclass, h->m2l_Ttc.p, st));
@@ -532,10 +563,12 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.launches += 1;
     record(h, EV_M2L_PREP);
     if (use_tc) {
-      CK(m2l_tc_gemm(p, W, h->m2l_Ttc.p, h->M.p, st));
+      if (accum)
+        CK(cudaMemsetAsync(h->L.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
+      CK(m2l_tc_gemm(p, W, h->m2l_Ttc.p, h->M.p, st, accum ? h->L.p : nullptr));
       h->stats.launches += 1;
     }
-    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st, use_tc));
+    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st, use_tc, accum));
     h->stats.launches += 2;
     h->m2l_tc_used = use_tc;
   }
@@ -708,6 +741,7 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
     if (cudaMalloc(&h->d_root, sizeof(RootInfo)) || cudaMalloc(&h->d_mm, 8 * sizeof(unsigned)) ||
         cudaMalloc(&h->d_small, 16 * sizeof(int)) || cudaMalloc(&h->d_overflow, sizeof(unsigned)) ||
         cudaMalloc(&h->d_stats, 4 * sizeof(unsigned long long)) ||
+        cudaMalloc(&h->d_bk, 32 * sizeof(int)) ||
         cudaMallocHost(&h->h_small, 16 * sizeof(int))) {
       rc = fail(h, FMM_E_OOM, "small device allocations failed");
       break;
@@ -738,7 +772,7 @@ int fmm_destroy(fmm_t h) {
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
   h->sh_keys_in.release(); h->sh_keys.release(); h->sh_vals_in.release(); h->sh_cells.release();
   h->sh_src.release(); h->sh_T.release(); h->sh_items.release(); h->sh_counters.release();
-  h->m2l_Y.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_T.release();
+  h->m2l_Y.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_stgt.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();
@@ -747,6 +781,7 @@ int fmm_destroy(fmm_t h) {
   if (h->d_small) cudaFree(h->d_small);
   if (h->d_overflow) cudaFree(h->d_overflow);
   if (h->d_stats) cudaFree(h->d_stats);
+  if (h->d_bk) cudaFree(h->d_bk);
   if (h->h_small) cudaFreeHost(h->h_small);
   for (int i = 0; i < EV_N; ++i)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
@@ -815,6 +850,12 @@ int fmm_set_mode(fmm_t h, int mode) {
 int fmm_set_timing(fmm_t h, int enable) {
   if (!h) return FMM_E_INVALID;
   h->timing = enable != 0;
+  return FMM_OK;
+}
+
+int fmm_set_deterministic(fmm_t h, int enable) {
+  if (!h) return FMM_E_INVALID;
+  h->deterministic = enable != 0;
   return FMM_OK;
 }
 

@@ -42,7 +42,11 @@ struct TravArgs {
   unsigned *scratch, *overflow;
   int *cnt4;
   const int *excl;
-  int base[4], excl_base[4];
+  // device-resident bookkeeping (no host round trip per level), see k_trav_totals:
+  //   [0..3] this level's scan value at the first target of each category, [4..7] where this
+  //   level's lists start in lsrc[k] / the out buffer, [8..11] capacities, [12] overflow flag,
+  //   [16..18] running list sizes
+  int *bk;
   unsigned *lsrc[3];
   int *loff[3], *lcnt[3];
   unsigned *out_src;
@@ -51,7 +55,7 @@ struct TravArgs {
   unsigned long long *stats;  // [0] P2P particle pairs, [1] M2P target evaluations
 };
 void launch_traverse(const TravArgs &A, bool write, cudaStream_t st);
-void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *out8, cudaStream_t st);
+void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *bk, cudaStream_t st);
 
 // ---- expansions.cu ----
 struct M2LTiles {
@@ -78,6 +82,7 @@ struct M2LWork {
   unsigned *keys_in, *keys;  // 24-bit class keys
   unsigned *idx_in, *sidx;  // pair indices sorted by class key
   unsigned *ssrc;           // source cell of each class-sorted pair
+  unsigned *stgt;           // target cell of each class-sorted pair (accumulate mode), or null
   int *flag, *cid, *cstart, *counters;
   int4 *items;              // GEMM work items (first sorted position, count, representative pair)
   unsigned *small;          // pairs on the direct path
@@ -96,14 +101,14 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
 size_t m2l_T_floats(int p);
 cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st);
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
-                        float2 *L, cudaStream_t st, bool gemm_done = false);
+                        float2 *L, cudaStream_t st, bool gemm_done = false, bool accum = false);
 
 // ---- m2l_tc.cu (tcgen05 3xTF32 class GEMM) ----
 bool m2l_tc_supported(int p);
 size_t m2l_tc_T_words(int p);
 cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg, cudaStream_t st);
 cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
-                        cudaStream_t st);
+                        cudaStream_t st, float2 *Lacc = nullptr);
 
 struct TcShiftWork {
   unsigned *keys_in, *keys, *vals_in, *cells;  // (level<<3 | octant) sort of all non-root cells
@@ -117,7 +122,8 @@ struct TcShiftWork {
 };
 cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *queue,
                           const unsigned *sidx, const unsigned *ssrc, const unsigned *Timg,
-                          const float2 *M, float *Y, int grid, cudaStream_t st);
+                          const float2 *M, float *Y, int grid, cudaStream_t st,
+                          float *Lacc = nullptr);
 cudaError_t tc_shift_build_ops(int p, unsigned *Tm2m, unsigned *Tl2l, cudaStream_t st);
 size_t tc_shift_sort_bytes(int ncells);
 cudaError_t tc_shift_prepare(int ncells, int depth, const TcShiftWork &S, CellsView C,

@@ -137,11 +137,13 @@ __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
 __global__ void k_m2l_class_flags(int npairs, const unsigned *__restrict__ skeys,
                                   const unsigned *__restrict__ sidx,
                                   const unsigned *__restrict__ src, int *__restrict__ flag,
-                                  unsigned *__restrict__ ssrc) {
+                                  unsigned *__restrict__ ssrc, const int *__restrict__ pair_t,
+                                  unsigned *__restrict__ stgt) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
     const unsigned k = skeys[i];
     flag[i] = (i == 0 || k != skeys[i - 1] || k == M2L_KEY_OWN) ? 1 : 0;
     ssrc[i] = src[sidx[i]];  // source cell in class-sorted order (one coalesced load later)
+    if (stgt) stgt[i] = (unsigned)pair_t[sidx[i]];
   }
 }
 
@@ -433,7 +435,8 @@ __global__ void __launch_bounds__(128) k_m2l_pairs(int p, const unsigned *__rest
                                                    const int *__restrict__ pair_t,
                                                    const unsigned *__restrict__ src, CellsView C,
                                                    const float2 *__restrict__ M,
-                                                   float *__restrict__ Y, int ydof) {
+                                                   float *__restrict__ Y, int ydof,
+                                                   float *__restrict__ Lacc) {
   extern __shared__ float2 sh_pairs[];
   const int NC = nc_of(p), KR = 2 * NC, YS = (KR + 3) & ~3;
   const int P2 = 2 * p, nI = (P2 + 1) * (P2 + 1), nM = (p + 1) * (p + 1);
@@ -471,7 +474,11 @@ __global__ void __launch_bounds__(128) k_m2l_pairs(int p, const unsigned *__rest
       }
       const float sgn = ((j + k) & 1) ? -1.f : 1.f;
       const float sc = sgn * (g.vform ? ldexpf(1.f, -g.dl * (j + 1)) : 1.f);
-      if (ydof) {  // tensor-core layout: dof order, stride dof_stride(p)
+      if (Lacc) {  // accumulate mode: straight into the target's expansion
+        float *lr = Lacc + (size_t)pair_t[e] * 2 * nc_stride(p) + 2 * o;
+        atomicAdd(lr, sc * re);
+        if (k > 0) atomicAdd(lr + 1, sc * im);
+      } else if (ydof) {  // tensor-core layout: dof order, stride dof_stride(p)
         const int d = j * j + (k == 0 ? 0 : 2 * k - 1);
         Y[(size_t)e * dof_stride(p) + d] = sc * re;
         if (k > 0) Y[(size_t)e * dof_stride(p) + d + 1] = sc * im;
@@ -560,7 +567,8 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
                                       M2L_KEY_BITS, st);
   if (e) return e;
-  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.src, W.flag, W.ssrc);
+  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.src, W.flag, W.ssrc,
+                                                    W.pair_t, W.stgt);
   bytes = 0;
   e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, W.flag, W.cid, npairs, st);
   if (e) return e;
@@ -591,7 +599,7 @@ cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st) {
 }
 
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
-                        float2 *L, cudaStream_t st, bool gemm_done) {
+                        float2 *L, cudaStream_t st, bool gemm_done, bool accum) {
   if (!W.direct_all && !gemm_done) {
     const size_t smem = m2l_gemm_smem(p);
     const int KR = 2 * nc_of(p);
@@ -626,9 +634,10 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
       configured = smem;
     }
     k_m2l_pairs<<<148 * 4, 128, smem, st>>>(p, W.small, W.counters, W.pair_t, W.src, W.C, M, W.Y,
-                                            gemm_done ? 1 : 0);
+                                            gemm_done ? 1 : 0,
+                                            accum ? reinterpret_cast<float *>(L) : nullptr);
   }
-  {
+  if (!accum) {
     const long long nthr = (long long)ncells * ((gemm_done ? dof_stride(p) : m2l_y_stride(p)) / 4);
     int b = (int)std::min<long long>((nthr + 255) / 256, 148 * 16);
     b = b > 0 ? b : 1;

@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
                                                    const unsigned *__restrict__ ssrc,
                                                    const unsigned *__restrict__ Timg,
                                                    const float *__restrict__ M,
-                                                   float *__restrict__ Y, int *queue) {
+                                                   float *__restrict__ Y, int *queue,
+                                                   float *__restrict__ Lacc) {
   constexpr int KD = dof_of(p), NT = tc_dim(p);
   constexpr int YSD = dof_stride(p), MROW = 2 * nc_stride(p);
   constexpr unsigned TBYTES = 2u * NT * NT * 4u;
@@ -344,7 +345,42 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
     };
     // D rows (dof order) -> Y rows (dof order, stride YSD), transposed through shared memory in
     // 32-column chunks: every store instruction writes four contiguous 128-byte row pieces
+    // Lacc != nullptr ("accumulate" mode): `yslot` is the pair's target cell and the row is added
+    // to its expansion (float order, row stride MROW) with 16-byte vector reductions in L2 --
+    // no Y round trip through HBM, but the summation order is not fixed
+    auto epilogue_acc = [&](unsigned tD, int cnt, int c0, unsigned trow) {
+      constexpr int KR = 2 * nc_of(p);
+      unsigned dv[NT];
+#pragma unroll
+      for (int cb = 0; cb < NT / 32; ++cb) {
+        unsigned v[32];
+        tc_ld32(tD + lane_base + cb * 32, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) dv[cb * 32 + q] = v[q];
+      }
+      tc_wait_ld();
+      if (c0 + tid < cnt) {
+        float *dst = Lacc + (size_t)trow * MROW;
+#pragma unroll
+        for (int q = 0; q < MROW / 4; ++q) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int f = 4 * q + e;
+            const int d = f < KR ? float_to_dof(f) : -1;
+            o[e] = d >= 0 ? __uint_as_float(dv[d]) : 0.f;
+          }
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q), "f"(o[0]),
+                       "f"(o[1]), "f"(o[2]), "f"(o[3])
+                       : "memory");
+        }
+      }
+    };
     auto epilogue = [&](unsigned tD, int cnt, int c0, unsigned yslot) {
+      if (Lacc) {
+        epilogue_acc(tD, cnt, c0, yslot);
+        return;
+      }
 #pragma unroll
       for (int cb = 0; cb < NT / 32; ++cb) {
         unsigned v[32];
@@ -466,7 +502,7 @@ cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg,
 
 cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *queue,
                           const unsigned *sidx, const unsigned *ssrc, const unsigned *Timg,
-                          const float2 *M, float *Y, int grid, cudaStream_t st) {
+                          const float2 *M, float *Y, int grid, cudaStream_t st, float *Lacc) {
   cudaMemsetAsync(queue, 0, sizeof(int), st);
 #define M2L_TC_CASE(PP)                                                                        \
   case PP: {                                                                                 \
@@ -477,7 +513,7 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
       cfg = true;                                                                            \
     }                                                                                        \
     k_m2l_tc<PP><<<grid, 160, smem, st>>>(items, counters, sidx, ssrc, Timg,                 \
-                                         reinterpret_cast<const float *>(M), Y, queue);      \
+                                         reinterpret_cast<const float *>(M), Y, queue, Lacc); \
   } break;
   switch (p) {
     M2L_TC_CASE(1) M2L_TC_CASE(2) M2L_TC_CASE(3) M2L_TC_CASE(4) M2L_TC_CASE(5) M2L_TC_CASE(6)
@@ -489,9 +525,10 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
 }
 
 cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
-                        cudaStream_t st) {
-  return tc_class_gemm(p, W.items, W.counters, W.counters + 4, W.sidx, W.ssrc, Timg, M, W.Y, 148,
-                       st);
+                        cudaStream_t st, float2 *Lacc) {
+  // accumulate mode: the epilogue's per-row "slot" is the pair's target cell (W.stgt)
+  return tc_class_gemm(p, W.items, W.counters, W.counters + 4, Lacc ? W.stgt : W.sidx, W.ssrc, Timg,
+                       M, W.Y, 148, st, reinterpret_cast<float *>(Lacc));
 }
 
 // ================================================================================================

@@ -46,6 +46,15 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
   const int nw = (gridDim.x * blockDim.x) >> 5;
   unsigned *stack = A.scratch + (size_t)gw * A.stack_cap;
 
+  int bk_excl[4] = {0, 0, 0, 0}, bk_base[4] = {0, 0, 0, 0};
+  if (WRITE) {
+    if (A.bk[12]) return;  // a list would overflow its buffer: the host re-runs with larger ones
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      bk_excl[c] = A.bk[c];
+      bk_base[c] = A.bk[4 + c];
+    }
+  }
   for (int k = gw; k < A.nt; k += nw) {
     const int t = A.t0 + k;
     const int4 gt = C.grid[t];
@@ -71,7 +80,7 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
     if (WRITE) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int o = A.base[c] + A.excl[c * A.nt + k] - A.excl_base[c];
+        const int o = bk_base[c] + A.excl[c * A.nt + k] - bk_excl[c];
         dst[c] = (c < 3 ? A.lsrc[c] : A.out_src) + o;
         if (lane == 0) {
           if (c < 3) {
@@ -185,12 +194,19 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
   }
 }
 
-// level totals: bases of the four sub-arrays of the one exclusive scan, and the level sizes
-__global__ void k_trav_totals(const int *excl, const int *cnt4, int nt, int *out8) {
+// level totals from the one exclusive scan over the four categories: where each category's
+// scan starts, where this level's lists go (running sizes) and an overflow flag when a buffer
+// is too small (the write pass then does nothing and the host re-runs the traversal)
+__global__ void k_trav_totals(const int *excl, const int *cnt4, int nt, int *bk) {
   for (int c = 0; c < 4; ++c) {
-    out8[c] = excl[c * nt];
+    const int e0 = excl[c * nt];
     const int last = (c + 1) * nt - 1;
-    out8[4 + c] = excl[last] + cnt4[last] - excl[c * nt];
+    const long long tot = (long long)excl[last] + cnt4[last] - e0;
+    bk[c] = e0;
+    const long long start = c < 3 ? bk[16 + c] : 0;
+    bk[4 + c] = (int)start;
+    if (start + tot + 1 > bk[8 + c]) bk[12] = 1;
+    if (c < 3) bk[16 + c] = (int)min(start + tot, (long long)INT32_MAX);
   }
 }
 
@@ -201,6 +217,6 @@ void launch_traverse(const TravArgs &A, bool write, cudaStream_t st) {
   else
     k_traverse<false><<<blocks, 128, 0, st>>>(A);
 }
-void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *out8, cudaStream_t st) {
-  k_trav_totals<<<1, 1, 0, st>>>(excl, cnt4, nt, out8);
+void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *bk, cudaStream_t st) {
+  k_trav_totals<<<1, 1, 0, st>>>(excl, cnt4, nt, bk);
 }

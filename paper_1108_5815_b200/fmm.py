@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 HYBRID, FMM_MODE, TREECODE, DIRECT = 0, 1, 2, 3
 MODES = {"hybrid": HYBRID, "fmm": FMM_MODE, "treecode": TREECODE, "direct": DIRECT}
 SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_host", "fmm_set_stream",
-           "fmm_set_mode", "fmm_set_timing", "fmm_tune", "fmm_get_cost_model",
+           "fmm_set_mode", "fmm_set_timing", "fmm_set_deterministic", "fmm_tune", "fmm_get_cost_model",
            "fmm_set_cost_model", "fmm_get_stats", "fmm_export_tree", "fmm_export_lists",
            "fmm_export_perm", "fmm_set_partition", "fmm_get_partition", "fmm_partition_indices",
            "fmm_strerror", "fmm_last_error"]
@@ -66,6 +66,7 @@ def load_library():
     L.fmm_set_stream.argtypes = [vp, vp]
     L.fmm_set_mode.argtypes = [vp, C.c_int]
     L.fmm_set_timing.argtypes = [vp, C.c_int]
+    L.fmm_set_deterministic.argtypes = [vp, C.c_int]
     L.fmm_tune.argtypes = [vp]
     L.fmm_get_cost_model.argtypes = [vp, P(CostModel)]
     L.fmm_set_cost_model.argtypes = [vp, P(CostModel)]
@@ -131,6 +132,10 @@ class FMM:
 
     def set_timing(self, on: bool):
         self._check(self.L.fmm_set_timing(self.h, int(bool(on))), "fmm_set_timing")
+
+    def set_deterministic(self, on: bool):
+        """Bit-reproducible M2L summation order (slower); see fmm_set_deterministic in fmm.h."""
+        self._check(self.L.fmm_set_deterministic(self.h, int(bool(on))), "fmm_set_deterministic")
 
     def set_stream(self, stream):
         self._check(self.L.fmm_set_stream(self.h, C.c_void_p(stream)), "fmm_set_stream")
