@@ -38,7 +38,8 @@ UNIT = "particles/s"
 FP32_LANES_PER_SM = 128
 N_SM = 148
 P2P_FLOP_PER_PAIR = 18      # 3 FADD d, 1 FMUL + 2 FFMA r^2, 2 FMUL q/r^3, 1 FMUL q/r, 1 FADD, 3 FFMA
-CPU_SAMPLE_N = 125_000      # C2 recipe at 1/8 size: same leaf occupancy (30.5), one level shallower
+CPU_SAMPLE_N = 1_000_000  # cpu_baseline: the full C2 instance (about 6-10 s of the FP64 oracle)
+REF_SAMPLE_N = 125_000    # --impl reference steps: C2 recipe at 1/8 size (same leaf occupancy)
 
 
 def m2l_flops(p: int) -> int:
@@ -118,8 +119,8 @@ def cpu_baseline(cost, p, theta, ncrit, mode_name):
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": CPU_SAMPLE_N / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "seconds": dt,
-            "sample": f"full oracle FMM (FP64, OpenMP) of a {CPU_SAMPLE_N}-particle instance of the "
-                      f"C2 recipe (uniform cube, q=1/N, p={p}, theta={theta}, ncrit={ncrit}, "
+            "sample": f"full oracle FMM (FP64, OpenMP) of the {CPU_SAMPLE_N}-particle C2 instance "
+                      f"(same seed as the GPU workload (uniform cube, q=1/N, p={p}, theta={theta}, ncrit={ncrit}, "
                       f"{mode_name}, the GPU's measured cost model)"}
 
 
@@ -131,7 +132,7 @@ def run_reference(args):
     from oracle import oracle as O
 
     cfg = CONFIGS["C2"]
-    xyz, q = make_particles(CPU_SAMPLE_N, "uniform", 2)
+    xyz, q = make_particles(REF_SAMPLE_N, "uniform", 2)
     cost = (1.3e-12, 4.1e-10, 7.7e-9)  # a B200 cost model (measured by fmm_create), fixed here
     times = []
     for it in range(args.warmup + args.steps):
@@ -140,16 +141,16 @@ def run_reference(args):
         if it >= args.warmup:
             times.append(time.perf_counter() - t)
     ms = 1e3 * sum(times) / len(times)
-    value = CPU_SAMPLE_N / (ms * 1e-3)
+    value = REF_SAMPLE_N / (ms * 1e-3)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C2 recipe, bounded instance N={CPU_SAMPLE_N}", "n": CPU_SAMPLE_N,
+        "config": {"workload": f"C2 recipe, bounded instance N={REF_SAMPLE_N}", "n": REF_SAMPLE_N,
                    "p": cfg["p"], "theta": cfg["theta"], "ncrit": cfg["ncrit"], "mode": "hybrid"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"each step: full FP64 oracle FMM of a {CPU_SAMPLE_N}-particle "
+                         "sample": f"each step: full FP64 oracle FMM of a {REF_SAMPLE_N}-particle "
                                    "instance of the C2 recipe on the host cores"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -289,7 +290,7 @@ def run_ours(args):
                 "traffic": traffic.get("k_m2l_tc"), "peak_source": tf32_src,
                 "tf32_flop_per_pair": m2l_tc_flops, "fp32_equiv_tflops": m2l_gflops / 1e3,
                 "fp32_equiv_flop_per_pair": m2l_flops(p),
-                "note": "time includes the per-target reduction of the pair slots"}
+                "note": "time = the tcgen05 class GEMM launch, which also adds every pair's result into its target (red.global.add.v4.f32)"}
     if p2p_ms >= m2l_ms:
         roofline = dict(p2p_line, secondary=m2l_line)
     else:
