@@ -182,7 +182,10 @@ def run_ours(args):
     X = torch.from_numpy(xyz).cuda()
     Q = torch.from_numpy(q).cuda()
     t0 = time.perf_counter()
-    f = FMM(p=p, theta=theta, ncrit=ncrit, mode=args.mode, tune=True)
+    f = FMM(p=p, theta=theta, ncrit=ncrit, mode=args.mode, tune=args.deterministic)
+    f.set_deterministic(args.deterministic)
+    if not args.deterministic:
+        f.tune()  # the kernel pre-calculation times the M2L the evaluations will use
     tune_s = time.perf_counter() - t0
     if world > 1:
         f = DistFMM(f, world, rank)
@@ -304,6 +307,8 @@ def run_ours(args):
                                "auto-tuned hybrid" if world == 1 else
                                f"C2 per rank ({world} x 1M, one global problem)",
                    "n_per_rank": n_local, "p": p, "theta": theta, "ncrit": ncrit, "mode": args.mode,
+                   "m2l_sum": ("ordered per-target reduction (fmm_set_deterministic(1))" if args.deterministic
+                               else "L2 vector reductions, unordered (fmm_set_deterministic(0))"),
                    "l2": "flushed (512 MiB write) before every timed step"},
         "time_to_solution_ms": ms_step,
         "phases_ms": {k: v / steps for k, v in phase.items()},
@@ -334,6 +339,8 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--mode", default="hybrid", choices=["hybrid", "fmm", "treecode"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="ordered M2L reduction (the library default); default here: L2 reductions")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -106,10 +106,10 @@ int fmm_set_stream(fmm_t h, void *stream);
 int fmm_set_mode(fmm_t h, int mode);
 /* 1 = record per-phase CUDA events (small overhead), 0 = off (default). */
 int fmm_set_timing(fmm_t h, int enable);
-/* 1 = bit-reproducible results: every target's M2L results are summed in its interaction-list
- * order (per-pair slots in HBM + one reduction pass). 0 (default) = the tensor-core M2L adds each
- * pair's local expansion straight into its target with vector reductions in L2; the summation
- * order then varies from run to run (differences at FP32 rounding level), and it is faster. */
+/* 1 (default) = bit-reproducible results: every target's M2L results are summed in its
+ * interaction-list order (per-pair slots in HBM + one reduction pass). 0 = the tensor-core M2L adds
+ * each pair's local expansion straight into its target with vector reductions in L2: faster, but
+ * the summation order then varies from run to run (differences at FP32 rounding level). */
 int fmm_set_deterministic(fmm_t h, int enable);
 
 /* Re-run the kernel pre-calculation on this device. */

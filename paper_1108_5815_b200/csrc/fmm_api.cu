@@ -71,7 +71,7 @@ struct fmm_ctx {
   fmm_cost_t cost{};
   fmm_stats_t stats{};
   bool timing = false;
-  bool deterministic = false;  // fmm_set_deterministic
+  bool deterministic = true;  // fmm_set_deterministic (bit-reproducible by default)
   cudaEvent_t ev[EV_N] = {};
   std::string err;
   M2LTiles tiles{};
@@ -561,10 +561,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
       CK(m2l_build_T(p, W, ngclass, st));
     }
     h->stats.launches += 1;
-    record(h, EV_M2L_PREP);
+    if (accum) CK(cudaMemsetAsync(h->L.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
+    record(h, EV_M2L_PREP);  // ms_m2l = the GEMM (+ the rare-class direct path / reduction)
     if (use_tc) {
-      if (accum)
-        CK(cudaMemsetAsync(h->L.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
       CK(m2l_tc_gemm(p, W, h->m2l_Ttc.p, h->M.p, st, accum ? h->L.p : nullptr));
       h->stats.launches += 1;
     }

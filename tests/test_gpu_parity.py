@@ -105,18 +105,19 @@ def test_p10_four_digits_vs_direct(O, handles, dist):
 
 
 def test_deterministic(handles):
-    """fmm_set_deterministic(1): bit-identical repeated evaluations; the default (M2L results
-    reduced in L2 in arbitrary order) agrees with it to FP32 rounding."""
+    """fmm_set_deterministic(1) (the default): bit-identical repeated evaluations; the fast mode
+    (M2L results reduced in L2 in arbitrary order) agrees with it to FP32 rounding."""
     xyz, q = make_particles(50000, "plummer", 9)
     f = handles(8, 0.5, 32, "hybrid")
     f.set_deterministic(True)
-    try:
-        a = run(f, xyz, q)
-        b = run(f, xyz, q)
-    finally:
-        f.set_deterministic(False)
+    a = run(f, xyz, q)
+    b = run(f, xyz, q)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-    c = run(f, xyz, q)
+    f.set_deterministic(False)
+    try:
+        c = run(f, xyz, q)
+    finally:
+        f.set_deterministic(True)
     rel = lambda x, y: float(np.linalg.norm(x - y) / np.linalg.norm(y))  # noqa: E731
     assert rel(c[0], a[0]) < 1e-6 and rel(c[1], a[1]) < 1e-6
 
@@ -176,7 +177,7 @@ def test_repeated_evaluations_stable(handles):
                     assert np.array_equal(out[0], ref[n][0]) and np.array_equal(out[1], ref[n][1])
                 else:
                     assert rel(out[0], ref[n][0]) < 1e-6 and rel(out[1], ref[n][1]) < 1e-6
-    f.set_deterministic(False)
+    f.set_deterministic(True)
 
 
 @pytest.mark.parametrize("mode", ["fmm", "hybrid"])
