@@ -171,7 +171,11 @@ __device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int 
   switch (S) {
     case 1: p2p_tile_rawS<MASK, 1>(sp, ns, h, tx, ty, tz, acc); break;
     case 2: p2p_tile_rawS<MASK, 2>(sp, ns, h, tx, ty, tz, acc); break;
+    case 3: p2p_tile_rawS<MASK, 3>(sp, ns, h, tx, ty, tz, acc); break;
     case 4: p2p_tile_rawS<MASK, 4>(sp, ns, h, tx, ty, tz, acc); break;
+    case 5: p2p_tile_rawS<MASK, 5>(sp, ns, h, tx, ty, tz, acc); break;
+    case 6: p2p_tile_rawS<MASK, 6>(sp, ns, h, tx, ty, tz, acc); break;
+    case 7: p2p_tile_rawS<MASK, 7>(sp, ns, h, tx, ty, tz, acc); break;
     default: p2p_tile_rawS<MASK, 8>(sp, ns, h, tx, ty, tz, acc); break;
   }
 }
@@ -213,10 +217,14 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
     int anc[FMM_LEVELS + 1], na = 0;
     for (int a = leaf; a >= 0 && na <= FMM_LEVELS; a = C.parent[a]) anc[na++] = a;
     for (int c0 = 0; c0 < tn; c0 += 32) {
+      // G = ceil(nt / 2) target pairs x S = min(8, 32 / G) source slices (lanes with h >= S
+      // idle): no padding of the target count to a power of two (a 17-target leaf keeps 27 of
+      // 32 lanes busy instead of 17 of 32 target slots)
       const int nt = min(32, tn - c0);
-      const int G = nt <= 8 ? 4 : nt <= 16 ? 8 : 16;
-      const int S = 32 / G;
+      const int G = (nt + 1) >> 1;
+      const int S = min(8, 32 / G);
       const int grp = lane % G, h = lane / G;
+      const bool active = h < S;
       const int i0 = c0 + 2 * grp, i1 = i0 + 1;
       const float4 t0 = i0 < tn ? pos[tb + i0] : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 t1 = i1 < tn ? pos[tb + i1] : t0;
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
         __syncwarp();
         for (int j = lane; j < n; j += 32) sh[wib][0][j] = pos[tb + j0 + j];
         __syncwarp();
-        p2p_tile_raw<true>(sh[wib][0], n, h, S, tx, ty, tz, acc);
+        p2p_tile_raw<true>(sh[wib][0], active ? n : 0, h, S, tx, ty, tz, acc);
       }
       // (2) all other source cells of the P2P lists of the leaf and its ancestors, as particle
       // ranges collected into shared memory (batches of P2P_RANGES), streamed by cp.async into a
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
           const int nxt = issue(buf ^ 1);
           cp_async_wait1();  // tile `buf` has landed
           __syncwarp();
-          p2p_tile_raw<false>(sh[wib][buf], cur, h, S, tx, ty, tz, acc);
+          p2p_tile_raw<false>(sh[wib][buf], active ? cur : 0, h, S, tx, ty, tz, acc);
           __syncwarp();
           buf ^= 1;
           cur = nxt;
@@ -293,17 +301,21 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
         cp_async_wait0();
         __syncwarp();
       }
-      // reduce the S source slices (lanes grp, grp + G, ...), fixed butterfly order
+      // reduce the S source slices (lanes grp, grp + G, ...) in slice order
       float2 r[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) r[k] = upk(acc[k]);
-      for (int o = G; o < 32; o <<= 1) {
+      float2 tot[4] = {r[0], r[1], r[2], r[3]};
+      for (int sl = 1; sl < S; ++sl) {  // slice order: deterministic
+        const int from = grp + sl * G;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          r[k].x += __shfl_xor_sync(0xffffffffu, r[k].x, o);
-          r[k].y += __shfl_xor_sync(0xffffffffu, r[k].y, o);
+          tot[k].x += __shfl_sync(0xffffffffu, r[k].x, from);
+          tot[k].y += __shfl_sync(0xffffffffu, r[k].y, from);
         }
       }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = tot[k];
       if (h == 0) {
         if (i0 < tn) acc_out[tb + i0] = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
         if (i1 < tn) acc_out[tb + i1] = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
