@@ -96,6 +96,7 @@ struct fmm_ctx {
   DBuf<uint64_t> cprefix;
   DBuf<int> nch, excl, leafflag, leaves, bnd;
   DBuf<int2> crange;
+  DBuf<int4> cpack;  // packed cell records for the traversal
   std::vector<int> level_off, level_cnt;
   int ncells = 0, nleaves = 0, depth = 0;
   // Morton partition of the targets (multi-GPU); nparts = 1: everything
@@ -328,6 +329,9 @@ static int traverse(fmm_ctx *h) {
   }
   CK(h->out_off.ensure(nc));
   CK(h->out_cnt.ensure(nc));
+  CK(h->cpack.ensure((size_t)2 * nc));
+  launch_pack_cells(nc, h->cells(), h->cpack.p, st);
+  h->stats.launches += 1;
   const int warps_per_block = 4;
   const int grid_blocks = 148 * 8;
   const size_t nwarps = (size_t)grid_blocks * warps_per_block;
@@ -359,6 +363,7 @@ static int traverse(fmm_ctx *h) {
       const int nt = h->level_cnt[level], t0 = h->level_off[level];
       TravArgs A{};
       A.C = h->cells();
+      A.pk = h->cpack.p;
       A.t0 = t0;
       A.nt = nt;
       A.level = level;
@@ -762,7 +767,7 @@ int fmm_destroy(fmm_t h) {
   h->keys_in.release(); h->keys.release(); h->idx_in.release(); h->perm.release();
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
-  h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release();
+  h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();
   h->tleaves.release();
   h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();

@@ -34,6 +34,7 @@ void launch_leaf_scatter(int ncells, const int *flag, const int *excl, int *leav
 // ---- traverse.cu ----
 struct TravArgs {
   CellsView C;
+  const int4 *pk;  // packed cell records (k_pack_cells): [2c] = grid, [2c+1] = beg, cnt, child0, nchild
   int t0, nt, level, mode, stack_cap, grid_blocks;
   int tlo, thi;  // targets restricted to cells intersecting sorted particle range [tlo, thi)
   double theta, t_pp, t_mp, t_ml;
@@ -55,6 +56,7 @@ struct TravArgs {
   unsigned long long *stats;  // [0] P2P particle pairs, [1] M2P target evaluations
 };
 void launch_traverse(const TravArgs &A, bool write, cudaStream_t st);
+void launch_pack_cells(int ncells, CellsView C, int4 *pk, cudaStream_t st);
 void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *bk, cudaStream_t st);
 
 // ---- expansions.cu ----

@@ -37,6 +37,29 @@ __device__ __forceinline__ int select_kind(const TravArgs &A, int nt, int ns) {
   return CAT_P2P;
 }
 
+// packed cell record (built once per tree by k_pack_cells): one 32-byte sector per cell instead
+// of four scattered loads on the traversal's latency-bound path
+struct CellRec {
+  int4 g;  // doubled-grid centre, level
+  int4 b;  // beg, cnt, child0, nchild
+};
+__device__ __forceinline__ CellRec load_rec(const int4 *pk, unsigned c) {
+  CellRec r;
+  r.g = __ldg(pk + 2 * (size_t)c);
+  r.b = __ldg(pk + 2 * (size_t)c + 1);
+  return r;
+}
+
+__global__ void k_pack_cells(int ncells, CellsView C, int4 *pk) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  pk[2 * c] = C.grid[c];
+  pk[2 * c + 1] = make_int4(C.beg[c], C.cnt[c], C.child0[c], C.nchild[c]);
+}
+void launch_pack_cells(int ncells, CellsView C, int4 *pk, cudaStream_t st) {
+  if (ncells > 0) k_pack_cells<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, C, pk);
+}
+
 template <bool WRITE>
 __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
   const CellsView C = A.C;
@@ -55,11 +78,13 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
       bk_base[c] = A.bk[4 + c];
     }
   }
+  unsigned long long warp_pp = 0, warp_mp = 0;
   for (int k = gw; k < A.nt; k += nw) {
     const int t = A.t0 + k;
-    const int4 gt = C.grid[t];
-    const int tcnt = C.cnt[t];
-    if (!(C.beg[t] < A.thi && C.beg[t] + tcnt > A.tlo)) {  // outside this rank's target partition
+    const CellRec rt = load_rec(A.pk, t);
+    const int4 gt = rt.g;
+    const int tcnt = rt.b.y;
+    if (!(rt.b.x < A.thi && rt.b.x + tcnt > A.tlo)) {  // outside this rank's target partition
       if (lane == 0) {
         if (WRITE) {
           for (int c = 0; c < 3; ++c) {
@@ -74,7 +99,7 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
       }
       continue;
     }
-    const bool tleaf = C.nchild[t] == 0;
+    const bool tleaf = rt.b.w == 0;
     int n[4] = {0, 0, 0, 0};
     unsigned *dst[4] = {nullptr, nullptr, nullptr, nullptr};
     if (WRITE) {
@@ -93,23 +118,24 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
         }
       }
     }
-    unsigned long long pp_pairs = 0, mp_evals = 0;
+    unsigned long long pp_pairs = 0, mp_evals = 0;  // this target's lane partials
     int top = 0;
     bool overflow = false;
 
     // classify (t, s) and append it to its category with ballots (deterministic order)
     auto consider_and_put = [&](bool valid, unsigned s, int forced_cat) {
       int cat = CAT_NONE;
-      int scnt = 0;
+      int scnt = 0, sbeg = 0;
       if (valid) {
         if (forced_cat >= 0) {
           cat = forced_cat;
         } else {
-          const int4 gs = C.grid[s];
-          scnt = C.cnt[s];
-          if (mac_accept(gt, gs, A.theta))
+          const CellRec rs = load_rec(A.pk, s);
+          scnt = rs.b.y;
+          sbeg = rs.b.x;
+          if (mac_accept(gt, rs.g, A.theta))
             cat = select_kind(A, tcnt, scnt);
-          else if (tleaf && C.nchild[s] == 0)
+          else if (tleaf && rs.b.w == 0)
             cat = CAT_P2P;
           else
             cat = CAT_PUSH;
@@ -131,7 +157,7 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
         } else {
           if (WRITE && cat == c) {
             dst[c][n[c] + pos] = s;
-            if (c == CAT_P2P) A.p2p_rng[(dst[c] - A.lsrc[2]) + n[c] + pos] = make_int2(C.beg[s], C.cnt[s]);
+            if (c == CAT_P2P) A.p2p_rng[(dst[c] - A.lsrc[2]) + n[c] + pos] = make_int2(sbeg, scnt);
           }
           n[c] += __popc(b);
         }
@@ -159,14 +185,16 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
       const bool valid = lane < nb;
       const unsigned s = valid ? stack[top + lane] : 0u;
       __syncwarp();
-      int snch = 0;
+      int snch = 0, sc0 = 0;
       bool split_src = false;
       if (valid) {
-        snch = C.nchild[s];
-        split_src = tleaf || (snch > 0 && C.grid[s].w <= gt.w);
+        const CellRec rs = load_rec(A.pk, s);
+        snch = rs.b.w;
+        sc0 = rs.b.z;
+        split_src = tleaf || (snch > 0 && rs.g.w <= gt.w);
       }
       consider_and_put(valid && !split_src, s, CAT_OUT);  // target splits: defer to children
-      const int c0 = split_src ? C.child0[s] : 0;
+      const int c0 = split_src ? sc0 : 0;
       const int m = split_src ? snch : 0;
       int mmax = m;
       for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
@@ -182,14 +210,18 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) A.cnt4[c * A.nt + k] = n[c];
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        pp_pairs += __shfl_xor_sync(0xffffffffu, pp_pairs, o);
-        mp_evals += __shfl_xor_sync(0xffffffffu, mp_evals, o);
-      }
-      if (lane == 0) {
-        atomicAdd(&A.stats[0], pp_pairs);
-        atomicAdd(&A.stats[1], mp_evals);
-      }
+      warp_pp += pp_pairs;  // one atomic per warp at the end, not two per target
+      warp_mp += mp_evals;
+    }
+  }
+  if (!WRITE) {
+    for (int o = 16; o > 0; o >>= 1) {
+      warp_pp += __shfl_xor_sync(0xffffffffu, warp_pp, o);
+      warp_mp += __shfl_xor_sync(0xffffffffu, warp_mp, o);
+    }
+    if (lane == 0 && (warp_pp | warp_mp)) {
+      atomicAdd(&A.stats[0], warp_pp);
+      atomicAdd(&A.stats[1], warp_mp);
     }
   }
 }
