@@ -68,6 +68,11 @@ struct fmm_ctx {
   int p = 4, ncrit = 32, mode = FMM_HYBRID;
   double theta = 0.5;
   cudaStream_t own_stream = nullptr, stream = nullptr;
+  // the upward sweep runs on `aux`, concurrently with the traversal and the M2L class sort
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_up = nullptr;
+  DBuf<char> cub_tmp_aux;
+  DBuf<float> sh_Y;  // per-cell slots of the tensor-core M2M / L2L
   fmm_cost_t cost{};
   fmm_stats_t stats{};
   bool timing = false;
@@ -187,6 +192,9 @@ static int fail(fmm_ctx *h, int code, const char *fmt, ...) {
 
 static void record(fmm_ctx *h, int e) {
   if (h->timing) cudaEventRecord(h->ev[e], h->stream);
+}
+static void record_on(fmm_ctx *h, int e, cudaStream_t s) {
+  if (h->timing) cudaEventRecord(h->ev[e], s);
 }
 
 static int check_device_ptr(fmm_ctx *h, const void *ptr, const char *name) {
@@ -442,11 +450,15 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   const int p = h->p, NC = nc_of(p);
   if (int rc = build_tree(h, xyz, q, n)) return rc;
   record(h, EV_TREE);
-  // a7/a8 upward sweep
+  // a7/a8 upward sweep, on the aux stream: it overlaps the traversal and the M2L class sort (which
+  // do not read M); the stream joins before the first kernel that reads M
+  CK(cudaEventRecord(h->ev_fork, st));
+  CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+  cudaStream_t ua = h->aux;
   const int NCS = nc_stride(p);
   CK(h->M.ensure((size_t)h->ncells * NCS));
   CK(h->L.ensure((size_t)h->ncells * NCS));
-  if (NCS != NC) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
+  if (NCS != NC) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, ua));
   // M2M / L2L: octant-class GEMMs on the tensor cores (p <= 10) unless disabled
   const char *scc = getenv("FMM_SHIFT_CUDA_CORES");
   const bool shift_tc = m2l_tc_supported(p) && h->ncells > 1 && !(scc && scc[0] && scc[0] != '0');
@@ -455,7 +467,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     const size_t tw = m2l_tc_T_words(p);
     if (h->sh_T_p != p) {
       CK(h->sh_T.ensure(16 * tw));
-      CK(tc_shift_build_ops(p, h->sh_T.p, h->sh_T.p + 8 * tw, st));
+      CK(tc_shift_build_ops(p, h->sh_T.p, h->sh_T.p + 8 * tw, ua));
       h->stats.launches += 1;
       h->sh_T_p = p;
     }
@@ -468,8 +480,8 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(h->sh_src.ensure(ns));
     CK(h->sh_items.ensure((size_t)(FMM_LEVELS + 2) * S.items_per_level));
     CK(h->sh_counters.ensure((size_t)(FMM_LEVELS + 2) * 8));
-    CK(h->cub_tmp.ensure(tc_shift_sort_bytes(ns)));
-    CK(h->m2l_Y.ensure((size_t)h->ncells * m2l_y_stride(p)));
+    CK(h->cub_tmp_aux.ensure(tc_shift_sort_bytes(ns)));
+    CK(h->sh_Y.ensure((size_t)h->ncells * m2l_y_stride(p)));
     S.keys_in = h->sh_keys_in.p;
     S.keys = h->sh_keys.p;
     S.vals_in = h->sh_vals_in.p;
@@ -479,25 +491,26 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     S.lvl_counters = h->sh_counters.p;
     S.Tm2m = h->sh_T.p;
     S.Tl2l = h->sh_T.p + 8 * tw;
-    S.tmp = h->cub_tmp.p;
-    S.tmp_bytes = h->cub_tmp.cap;
-    CK(tc_shift_prepare(h->ncells, h->depth, S, h->cells(), st));
+    S.tmp = h->cub_tmp_aux.p;
+    S.tmp_bytes = h->cub_tmp_aux.cap;
+    CK(tc_shift_prepare(h->ncells, h->depth, S, h->cells(), ua));
     h->stats.launches += 3;
     h->stats.cub_calls += 1;
   }
-  launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, st);
+  launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, ua);
   CKL();
   for (int level = h->depth - 1; level >= 0; --level) {
     if (shift_tc) {
       CK(tc_shift_m2m_level(p, level, h->level_off[level], h->level_cnt[level], h->cells(), S,
-                            h->M.p, h->m2l_Y.p, st));
+                            h->M.p, h->sh_Y.p, ua));
       h->stats.launches += 2;
     } else {
-      launch_m2m(p, h->level_off[level], h->level_cnt[level], h->cells(), h->M.p, st);
+      launch_m2m(p, h->level_off[level], h->level_cnt[level], h->cells(), h->M.p, ua);
     }
     CKL();
   }
-  record(h, EV_UP);
+  record_on(h, EV_UP, ua);
+  CK(cudaEventRecord(h->ev_up, ua));
   if (int rc = traverse(h)) return rc;
   record(h, EV_TRAV);
   record(h, EV_M2L_PREP);  // re-recorded after the class sort when there are M2L pairs
@@ -567,6 +580,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     }
     h->stats.launches += 1;
     if (accum) CK(cudaMemsetAsync(h->L.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
+    CK(cudaStreamWaitEvent(st, h->ev_up, 0));  // join: the multipoles are complete
     record(h, EV_M2L_PREP);  // ms_m2l = the GEMM (+ the rare-class direct path / reduction)
     if (use_tc) {
       CK(m2l_tc_gemm(p, W, h->m2l_Ttc.p, h->M.p, st, accum ? h->L.p : nullptr));
@@ -576,6 +590,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.launches += 2;
     h->m2l_tc_used = use_tc;
   }
+  CK(cudaStreamWaitEvent(st, h->ev_up, 0));  // (no M2L pairs: join here)
   record(h, EV_M2L);
   // a12 P2P (writes acc), a11 M2P (adds)
   const int *tl = h->nparts > 1 ? h->tleaves.p : h->leaves.p;
@@ -594,7 +609,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     for (int level = 1; level <= h->depth; ++level) {
       if (shift_tc) {
         CK(tc_shift_l2l_level(p, level, h->level_off[level], h->level_cnt[level], S, h->L.p,
-                              h->m2l_Y.p, st));
+                              h->sh_Y.p, st));
         h->stats.launches += 2;
       } else {
         launch_l2l(p, h->level_off[level], h->level_cnt[level], h->cells(), h->L.p, st);
@@ -659,8 +674,12 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     cudaEventElapsedTime(&ms[0], h->ev[EV_START], h->ev[EV_DOWN]);
     h->stats.ms_total = ms[0];
     h->stats.ms_tree = ms[EV_TREE];
-    h->stats.ms_upward = ms[EV_UP];
-    h->stats.ms_traverse = ms[EV_TRAV] + ms[EV_M2L_PREP];  // class sort counted as bookkeeping
+    // the upward sweep (aux stream) overlaps the traversal: both are measured from EV_TREE
+    float up = 0.f, trav = 0.f;
+    cudaEventElapsedTime(&up, h->ev[EV_TREE], h->ev[EV_UP]);
+    cudaEventElapsedTime(&trav, h->ev[EV_TREE], h->ev[EV_TRAV]);
+    h->stats.ms_upward = up;
+    h->stats.ms_traverse = trav + ms[EV_M2L_PREP];  // class sort counted as bookkeeping
     h->stats.ms_m2l = ms[EV_M2L];
     h->stats.ms_p2p = ms[EV_P2P];
     h->stats.ms_m2p = ms[EV_M2P];
@@ -741,6 +760,12 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
     if ((e = cudaGetDevice(&h->device)) != cudaSuccess) { rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e)); break; }
     if ((e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking)) != cudaSuccess) { rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e)); break; }
     h->stream = h->own_stream;
+    if ((e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming)) != cudaSuccess) {
+      rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e));
+      break;
+    }
     for (int i = 0; i < EV_N; ++i) cudaEventCreate(&h->ev[i]);
     if (cudaMalloc(&h->d_root, sizeof(RootInfo)) || cudaMalloc(&h->d_mm, 8 * sizeof(unsigned)) ||
         cudaMalloc(&h->d_small, 16 * sizeof(int)) || cudaMalloc(&h->d_overflow, sizeof(unsigned)) ||
@@ -776,7 +801,7 @@ int fmm_destroy(fmm_t h) {
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
   h->sh_keys_in.release(); h->sh_keys.release(); h->sh_vals_in.release(); h->sh_cells.release();
   h->sh_src.release(); h->sh_T.release(); h->sh_items.release(); h->sh_counters.release();
-  h->m2l_Y.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_stgt.release(); h->m2l_T.release();
+  h->m2l_Y.release(); h->sh_Y.release(); h->cub_tmp_aux.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_stgt.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();
@@ -790,6 +815,9 @@ int fmm_destroy(fmm_t h) {
   for (int i = 0; i < EV_N; ++i)
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_up) cudaEventDestroy(h->ev_up);
   delete h;
   return FMM_OK;
 }

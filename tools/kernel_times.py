@@ -45,3 +45,10 @@ gaps.sort(reverse=True)
 print("largest idle gaps (us):")
 for g in gaps[:12]:
     print(f"  {g[0]:7.1f}  after {g[1]}  before {g[2]}")
+if os.environ.get("TIMELINE"):
+    t0 = evs[0].time_range.start
+    acc_idle = 0.0
+    for a, b in zip(evs, evs[1:]):
+        g = b.time_range.start - a.time_range.end
+        acc_idle += max(g, 0)
+        print(f"{a.time_range.start - t0:9.1f} {a.time_range.elapsed_us():8.1f}  gap {g:6.1f}  cum_idle {acc_idle:7.1f}  {a.name.split('(')[0][:50]}")
