@@ -67,12 +67,25 @@ def route_results(idx: torch.Tensor, vals: torch.Tensor, offsets: torch.Tensor, 
     return out
 
 
+def broadcast_cost_model(fmm, group=None, src: int = 0):
+    """Give every rank rank `src`'s measured cost table (the kind choice of a
+    pair must not depend on which rank evaluates it, so that the union of the per-rank lists is
+    the one-GPU list set)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
+        else torch.device("cpu")
+    t = torch.tensor(list(fmm.cost_model()), dtype=torch.float64, device=dev)
+    dist.broadcast(t, src=src, group=group)
+    fmm.set_cost_model(*[float(v) for v in t.tolist()])
+
+
 class DistFMM:
     """Wraps a single-GPU `FMM` handle for a torch.distributed job (one rank per GPU)."""
 
-    def __init__(self, fmm, world: int, rank: int, group=None):
+    def __init__(self, fmm, world: int, rank: int, group=None, share_cost_model: bool = True):
         self.f, self.world, self.rank, self.group = fmm, world, rank, group
         self.f.set_partition(world, rank)
+        if share_cost_model and world > 1:
+            broadcast_cost_model(self.f, group)
 
     def __getattr__(self, name):  # set_timing, stats, cost_model, ... of the local handle
         return getattr(self.f, name)

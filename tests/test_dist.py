@@ -66,3 +66,40 @@ def test_gather_partition_route_world2(tmp_path):
     assert sum(r[2] for r in res) == N  # every target evaluated by exactly one rank
     for r in res:
         assert r[0] == 0.0 and r[1] == 0.0  # routed rows are the owner's rows, bit for bit
+
+
+class _FakeHandle:
+    """Stands in for FMM: only the cost-table accessors broadcast_cost_model uses."""
+
+    def __init__(self, c):
+        self.c = tuple(c)
+
+    def cost_model(self):
+        return self.c
+
+    def set_cost_model(self, *c):
+        self.c = tuple(c)
+
+
+def _cost_worker(rank, world, port, result_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1108_5815_b200.dist import broadcast_cost_model
+
+    h = _FakeHandle((1.0e-12 * (rank + 1), 3.0e-10 * (rank + 1), 7.0e-9 * (rank + 1)))
+    broadcast_cost_model(h)
+    np.save(os.path.join(result_dir, f"c{rank}.npy"), np.array(h.c))
+    dist.destroy_process_group()
+
+
+def test_cost_table_is_rank0s_on_every_rank(tmp_path):
+    # SURVEY §8(e) step 6: one cost table for all ranks, or the kind choice of a pair would depend
+    # on the rank that evaluates it
+    world = 2
+    mp.start_processes(_cost_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       start_method="spawn")
+    c = [np.load(tmp_path / f"c{r}.npy") for r in range(world)]
+    assert np.array_equal(c[0], c[1]) and np.array_equal(c[0], [1.0e-12, 3.0e-10, 7.0e-9])
