@@ -10,7 +10,9 @@ sweep, traversal, M2L/M2P/P2P, downward sweep) on inputs already resident in HBM
 (a 512 MiB write) before every timed step, outside the timed interval. `value` = particles
 evaluated per second over all ranks (N / time-to-solution); `ms_per_step` = time-to-solution.
 
-N > 1 (torchrun, one process per GPU, NCCL): see paper_1108_5815_b200/dist.py; rank 0 prints.
+N > 1 (torchrun, one process per GPU): one distributed handle per rank (fmm_create_dist, NCCL
+inside libfmm.so); weak scaling, each rank contributes one C2 instance shifted into
+its own unit cube, so the job is ONE global problem of N x 1M particles; rank 0 prints.
 
 `--impl reference` times the CPU FP64 oracle (oracle/, the only other arm this tier has) on the
 host cores: each step is the full oracle FMM of a bounded instance of the same recipe.
@@ -167,8 +169,13 @@ def run_ours(args):
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # FMM_BENCH_DIST=1 runs the distributed handle (NCCL) even at N=1 (a 1-rank communicator)
+    use_dist = world > 1 or os.environ.get("FMM_BENCH_DIST") == "1"
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank,
+                                world_size=world)
         from paper_1108_5815_b200.dist import DistFMM
     cfg = dict(CONFIGS[args.config])
     p, theta, ncrit = cfg["p"], cfg["theta"], cfg["ncrit"]
@@ -182,18 +189,19 @@ def run_ours(args):
     X = torch.from_numpy(xyz).cuda()
     Q = torch.from_numpy(q).cuda()
     t0 = time.perf_counter()
-    f = FMM(p=p, theta=theta, ncrit=ncrit, mode=args.mode, tune=args.deterministic)
+    if use_dist:  # distributed handle: NCCL communicator inside libfmm (fmm_create_dist)
+        f = DistFMM(p=p, theta=theta, ncrit=ncrit, mode=args.mode, tune=args.deterministic)
+    else:
+        f = FMM(p=p, theta=theta, ncrit=ncrit, mode=args.mode, tune=args.deterministic)
     f.set_deterministic(args.deterministic)
     if not args.deterministic:
         f.tune()  # the kernel pre-calculation times the M2L the evaluations will use
     tune_s = time.perf_counter() - t0
-    if world > 1:
-        f = DistFMM(f, world, rank)
     stream = torch.cuda.current_stream()
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 512 MiB > L2
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -322,11 +330,15 @@ def run_ours(args):
                 "d2h_bytes_per_step": 16 * n_local},
         "clocks": clk.summary(),
     }
+    if use_dist:
+        line["comm"] = {k: stats[k] for k in ("n_global", "rank_lo", "rank_hi", "n_straddle",
+                                               "let_cells", "let_particles", "bytes_sent", "ms_comm")}
+        line["config"]["parallelism"] = f"Morton domain decomposition x{world}, LET alltoallv (NCCL)"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(f.cost_model(), p, theta, ncrit, args.mode)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

@@ -48,7 +48,7 @@ enum fmm_status {
   FMM_E_NONFINITE = -3,  /* a coordinate or charge is not finite; outputs untouched */
   FMM_E_CUDA = -4,       /* CUDA runtime / kernel failure */
   FMM_E_OOM = -5,        /* device allocation failed */
-  FMM_E_NCCL = -6,       /* reserved for the multi-GPU path */
+  FMM_E_NCCL = -6,       /* NCCL (or in-process group) collective failure, multi-GPU handles */
   FMM_E_STATE = -7       /* export called before any evaluation */
 };
 
@@ -78,6 +78,13 @@ typedef struct {
   double ms_total, ms_tree, ms_upward, ms_traverse, ms_m2l, ms_p2p, ms_m2p, ms_downward;
   int64_t launches;                 /* libfmm kernels launched by the evaluation (CUB's excluded) */
   int64_t cub_calls;                /* CUB radix-sort / scan calls (library kernels) */
+  /* multi-GPU handles (fmm_create_dist / fmm_create_in_group); zero otherwise */
+  int64_t n_global;                 /* particles over all ranks */
+  int64_t rank_lo, rank_hi;         /* this rank's targets: global Morton-order range [lo, hi) */
+  int64_t n_straddle;               /* cells whose particles span ranks (multipoles allreduced) */
+  int64_t let_cells, let_particles; /* remote multipoles / particles received (local essential tree) */
+  int64_t bytes_sent;               /* bytes this rank sent in all exchanges of the evaluation */
+  double ms_comm;                   /* host wall time inside collectives (includes waiting) */
 } fmm_stats_t;
 
 /* Create a handle on the current CUDA device. p = expansion order (coefficients n = 0..p,
@@ -143,6 +150,36 @@ int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, dou
 int fmm_set_partition(fmm_t h, int nparts, int part);
 int fmm_get_partition(fmm_t h, int64_t *lo, int64_t *hi);
 int fmm_partition_indices(fmm_t h, int64_t *d_out, int64_t cap, int64_t *count_out);
+
+/* ---- Multi-GPU: one handle per rank, one rank per GPU ----
+ * A distributed handle takes the rank's own particle shard in fmm_evaluate (any size, any subset;
+ * n may be 0 on some ranks) and returns phi / grad for exactly those particles in the caller's
+ * order. fmm_evaluate is then COLLECTIVE: every rank of the group must call it (same mode and
+ * cost model; the cost model measured by rank 0 is broadcast at creation so that the per-pair
+ * kind choice, and hence the union of the lists, equals a single-GPU evaluation of the union).
+ * The method inside: global bbox (allreduce) -> local keys + sort -> the global
+ * adaptive octree built level by level from allreduced split bounds (no particle moves) -> ranks
+ * own contiguous Morton runs of whole leaves, balanced by count -> particle alltoallv -> P2M/M2M,
+ * allreduce of the multipoles of cells that straddle ranks -> traversal of the own targets ->
+ * receiver-driven local essential tree: the remote multipoles and particle ranges the lists name
+ * are requested and received (alltoallv) -> M2L / P2P / M2P / L2L / L2P -> results sent back to
+ * the ranks that own the particles. FMM_DIRECT is not available on distributed handles.
+ * Global particle count < 2^30. Errors: FMM_E_INVALID, FMM_E_NCCL, plus those of fmm_create.
+ *
+ * fmm_comm_unique_id: NCCL unique id (rank 0 creates it, the caller broadcasts the 128 bytes,
+ *   e.g. with torch.distributed). NCCL is loaded at run time (dlopen libnccl.so.2).
+ * fmm_create_dist: handle on the current CUDA device joined to an NCCL communicator of nranks.
+ * fmm_group_create / fmm_create_in_group: an IN-PROCESS group of nranks handles (one host thread
+ *   per handle; the handles may share one GPU). Collectives are device copies between barriers;
+ *   the distributed algorithm is the same as over NCCL (used to test it on one GPU). The group
+ *   must outlive its handles; at most 16 ranks. */
+typedef struct fmm_group *fmm_group_t;
+int fmm_comm_unique_id(unsigned char h_id[128]);
+int fmm_create_dist(fmm_t *out, int p, double theta, int ncrit, int nranks, int rank,
+                    const unsigned char h_id[128]);
+int fmm_group_create(fmm_group_t *out, int nranks);
+int fmm_group_destroy(fmm_group_t g);
+int fmm_create_in_group(fmm_t *out, int p, double theta, int ncrit, fmm_group_t g, int rank);
 
 const char *fmm_strerror(int code);
 const char *fmm_last_error(fmm_t h);

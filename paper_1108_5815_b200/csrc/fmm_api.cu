@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -17,6 +18,7 @@
 #include <vector>
 
 #include "../../include/fmm.h"
+#include "comm.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -138,6 +140,26 @@ struct fmm_ctx {
   int64_t last_n = 0;
   RootInfo h_root{};
 
+  // ---- multi-GPU; comm == nullptr: single GPU ----
+  FmmComm *comm = nullptr;
+  int64_t n_glob = 0;
+  int nloc = 0, own_lo = 0, own_hi = 0, nstrad = 0;
+  std::vector<int> roff;                       // rank boundaries (global sorted index), R+1
+  std::vector<int64_t> scnt_p, rcnt_p;         // particle alltoallv counts (forward direction)
+  DBuf<int> d_off, d_lb, d_cnt;
+  DBuf<int64_t> d_i64;
+  DBuf<uint64_t> d_K, lkeys_in, lkeys, rkeys, rkeys_s;
+  DBuf<unsigned> lidx_in, lperm, ridx_in, rperm;
+  DBuf<float4> lpos, rpos, pbuf_s, pbuf_r;
+  DBuf<int> strad_flag, strad_excl, need_m, need_p, dexcl, psize, pexcl;
+  DBuf<unsigned> strad_ids, req_ids, req_own, req_own_s, mreq_s, rreq_ids;
+  DBuf<unsigned> pcell, pown, pown_s, pidx, pidx_s;
+  DBuf<int> prsize, prexcl, psz2, pex2;
+  DBuf<int2> prng, prng_s, rreq_rng;
+  DBuf<float2> rows_s, rows_r;
+  DBuf<float> rphi, rgrad, sphi, sgrad;
+  DBuf<double> d_cost;
+
   CellsView cells() {
     CellsView C;
     C.beg = cbeg.p;
@@ -219,25 +241,16 @@ static int cub_scan(fmm_ctx *h, const int *in, int *out, int n) {
   return FMM_OK;
 }
 
-// ---- a1-a5: bbox, keys, sort, gather, tree ----------------------------------------------------
-static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
-  cudaStream_t st = h->stream;
-  CK(h->keys_in.ensure(n));
-  CK(h->keys.ensure(n));
-  CK(h->idx_in.ensure(n));
-  CK(h->perm.ensure(n));
-  CK(h->pos.ensure(n));
-  CK(h->acc.ensure(n));
-  launch_keys(xyz, n, h->d_root, h->keys_in.p, h->idx_in.p, st);
-  CKL();
-  size_t bytes = 0;
-  CK(sort_keys(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
-  CK(h->cub_tmp.ensure(bytes));
-  CK(sort_keys(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
-  ++h->stats.cub_calls;
-  launch_gather(xyz, q, h->perm.p, n, h->pos.p, st);
-  CKL();
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
+// Level-synchronous adaptive octree over n particles (a4/a5): one host readback of the child count
+// per level. keys = sorted Morton keys; nloc < 0: the keys are all n particles (single GPU);
+// nloc >= 0: they are this rank's local shard and the split bounds are allreduced (dist.cu).
+static int build_levels(fmm_ctx *h, int64_t n, const uint64_t *keys, int nloc) {
+  cudaStream_t st = h->stream;
   // level-synchronous adaptive octree: one host readback of the child count per level
   size_t cap = std::max<size_t>(1024, (size_t)(2 * n / std::max(1, h->ncrit)) + 64);
   auto ensure_cells = [&](size_t need, size_t keep) -> cudaError_t {
@@ -263,9 +276,15 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
     CK(h->excl.ensure(nl));
     CK(h->crange.ensure((size_t)8 * nl));
     CK(h->bnd.ensure((size_t)8 * nl));
-    launch_split(c0, nl, level, h->ncrit, h->keys.p, h->cells(), h->cprefix.p, h->nch.p,
-                 h->crange.p, h->bnd.p, st);
-    h->stats.launches += 1;
+    launch_split_bounds(c0, nl, level, h->ncrit, keys, nloc, h->cells(), h->cprefix.p, h->bnd.p, st);
+    CKL();
+    if (h->comm) {  // distributed build: global child bounds = sum of the per-rank local bounds
+      const double t0 = now_ms();
+      const int rc = h->comm->allreduce(h->bnd.p, (size_t)8 * nl, CT_I32, CO_SUM, st);
+      h->stats.ms_comm += now_ms() - t0;
+      if (rc) return fail(h, rc, "split-bound allreduce: %s", h->comm->err.c_str());
+    }
+    launch_split_ranges(c0, nl, level, h->ncrit, h->cells(), h->bnd.p, h->nch.p, h->crange.p, st);
     CKL();
     if (int rc = cub_scan(h, h->nch.p, h->excl.p, nl)) return rc;
     launch_level_total(h->nch.p, h->excl.p, nl, h->d_small, st);
@@ -298,6 +317,30 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
   CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   h->nleaves = h->h_small[0];
+  return FMM_OK;
+}
+
+// ---- a1-a5: bbox, keys, sort, gather, tree ----------------------------------------------------
+static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
+  cudaStream_t st = h->stream;
+  CK(h->keys_in.ensure(n));
+  CK(h->keys.ensure(n));
+  CK(h->idx_in.ensure(n));
+  CK(h->perm.ensure(n));
+  CK(h->pos.ensure(n));
+  CK(h->acc.ensure(n));
+  launch_keys(xyz, n, h->d_root, h->keys_in.p, h->idx_in.p, st);
+  CKL();
+  size_t bytes = 0;
+  CK(sort_keys(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
+  CK(h->cub_tmp.ensure(bytes));
+  CK(sort_keys(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
+  ++h->stats.cub_calls;
+  launch_gather(xyz, q, h->perm.p, n, h->pos.p, st);
+  CKL();
+
+  if (int rc = build_levels(h, n, h->keys.p, -1)) return rc;
+  const int total = h->ncells;
   // target leaves of this handle's partition
   h->part_lo = 0;
   h->part_hi = (int)n;
@@ -318,6 +361,353 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
     h->part_lo = h->tleaves_n ? h->h_small[8] : 0;
     h->part_hi = h->tleaves_n ? h->h_small[9] : 0;
   }
+  return FMM_OK;
+}
+
+// ---- multi-GPU: distributed tree, partition, local essential tree ----
+#define CC(call)                                                                    \
+  do {                                                                              \
+    const double t0_ = now_ms();                                                    \
+    const int rc_ = (call);                                                         \
+    h->stats.ms_comm += now_ms() - t0_;                                             \
+    if (rc_) return fail(h, rc_, "%s: %s", #call, h->comm->err.c_str());            \
+  } while (0)
+
+// recv[r * k + j] = item j of what peer r sends to this rank (send[r * k + j] = item j for peer r)
+static int exchange_counts(fmm_ctx *h, const std::vector<int64_t> &send,
+                           std::vector<int64_t> &recv, int k) {
+  const int R = h->comm->nranks, me = h->comm->rank;
+  cudaStream_t st = h->stream;
+  const size_t blk = (size_t)R * k;
+  CK(h->d_i64.ensure(blk * (R + 1)));
+  CK(cudaMemcpyAsync(h->d_i64.p, send.data(), sizeof(int64_t) * blk, cudaMemcpyHostToDevice, st));
+  CC(h->comm->allgather(h->d_i64.p, h->d_i64.p + blk, sizeof(int64_t) * blk, st));
+  std::vector<int64_t> all(blk * R);
+  CK(cudaMemcpyAsync(all.data(), h->d_i64.p + blk, sizeof(int64_t) * blk * R, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  recv.assign(blk, 0);
+  for (int r = 0; r < R; ++r)
+    for (int j = 0; j < k; ++j) recv[(size_t)r * k + j] = all[((size_t)r * R + me) * k + j];
+  return FMM_OK;
+}
+
+// alltoallv of elements of `elem` bytes; counts per peer taken from column `col` of k-wide rows
+static int a2av(fmm_ctx *h, const void *send, const std::vector<int64_t> &scnt, void *recv,
+                const std::vector<int64_t> &rcnt, size_t elem, int k = 1, int col = 0) {
+  const int R = h->comm->nranks, me = h->comm->rank;
+  std::vector<size_t> sc(R), sd(R), rc(R), rd(R);
+  size_t so = 0, ro = 0;
+  for (int r = 0; r < R; ++r) {
+    sc[r] = (size_t)scnt[(size_t)r * k + col] * elem;
+    sd[r] = so;
+    so += sc[r];
+    rc[r] = (size_t)rcnt[(size_t)r * k + col] * elem;
+    rd[r] = ro;
+    ro += rc[r];
+  }
+  h->stats.bytes_sent += (int64_t)(so - sc[me]);
+  CC(h->comm->alltoallv(send, sc.data(), sd.data(), recv, rc.data(), rd.data(), h->stream));
+  return FMM_OK;
+}
+
+// ids of the flagged cells (ascending); returns their number in *count
+static int compact_flags(fmm_ctx *h, const int *flag, int n, unsigned *ids, int *count) {
+  cudaStream_t st = h->stream;
+  CK(h->dexcl.ensure(std::max(n, 1)));
+  if (int rc = cub_scan(h, flag, h->dexcl.p, n)) return rc;
+  launch_leaf_scatter(n, flag, h->dexcl.p, (int *)ids, st);
+  CKL();
+  launch_level_total(flag, h->dexcl.p, n, h->d_small, st);
+  CKL();
+  CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *count = h->h_small[0];
+  return FMM_OK;
+}
+
+// sort (owner, value) pairs by owner (stable) and count per owner on the host
+static int sort_by_owner(fmm_ctx *h, const unsigned *own, unsigned *own_s, const unsigned *val,
+                         unsigned *val_s, int n, std::vector<int64_t> &cnt) {
+  cudaStream_t st = h->stream;
+  const int R = h->comm->nranks;
+  int bits = 1;
+  while ((1 << bits) < R) ++bits;
+  if (n > 0) {
+    size_t bytes = 0;
+    CK(sort_owner_pairs(nullptr, bytes, own, own_s, val, val_s, n, bits, st));
+    CK(h->cub_tmp.ensure(bytes));
+    CK(sort_owner_pairs(h->cub_tmp.p, bytes, own, own_s, val, val_s, n, bits, st));
+    ++h->stats.cub_calls;
+  }
+  CK(h->d_cnt.ensure(R));
+  CK(cudaMemsetAsync(h->d_cnt.p, 0, sizeof(int) * R, st));
+  launch_owner_hist(own_s, n, h->d_cnt.p, st);
+  if (n > 0) CKL();
+  std::vector<int> c(R);
+  CK(cudaMemcpyAsync(c.data(), h->d_cnt.p, sizeof(int) * R, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cnt.assign(c.begin(), c.end());
+  return FMM_OK;
+}
+
+// a1-a5 + partition + particle exchange. After this, pos / perm hold this rank's particles at
+// their GLOBAL Morton positions [own_lo, own_hi); the tree is the global one (same on every rank).
+static int dist_build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t nloc) {
+  cudaStream_t st = h->stream;
+  FmmComm *cm = h->comm;
+  const int R = cm->nranks, me = cm->rank;
+  // a1: global bounding box -> root cube (identical on every rank); global particle count
+  launch_bbox_local(xyz, q, nloc, h->d_mm, h->d_root, st);
+  h->stats.launches += 2;
+  CKL();
+  CC(cm->allreduce(h->d_mm, 3, CT_U32, CO_MIN, st));
+  CC(cm->allreduce(h->d_mm + 3, 4, CT_U32, CO_MAX, st));
+  launch_root_from_mm(h->d_mm, h->d_root, st);
+  h->stats.launches += 1;
+  CKL();
+  CK(h->d_i64.ensure(64));
+  int64_t nn = nloc;
+  CK(cudaMemcpyAsync(h->d_i64.p, &nn, sizeof nn, cudaMemcpyHostToDevice, st));
+  CC(cm->allreduce(h->d_i64.p, 1, CT_I64, CO_SUM, st));
+  CK(cudaMemcpyAsync(&nn, h->d_i64.p, sizeof nn, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h->h_root, h->d_root, sizeof(RootInfo), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h->h_root.nonfinite) return fail(h, FMM_E_NONFINITE, "non-finite coordinate or charge on some rank");
+  if (nn >= ((int64_t)1 << 30)) return fail(h, FMM_E_INVALID, "global n = %lld exceeds 2^30", (long long)nn);
+  h->n_glob = nn;
+  h->nloc = (int)nloc;
+  const int N = (int)nn;
+  // a2/a3 on the local shard: keys, sort, Morton-ordered float4
+  const size_t nl1 = std::max<int64_t>(nloc, 1);
+  CK(h->lkeys_in.ensure(nl1));
+  CK(h->lkeys.ensure(nl1));
+  CK(h->lidx_in.ensure(nl1));
+  CK(h->lperm.ensure(nl1));
+  CK(h->lpos.ensure(nl1));
+  if (nloc > 0) {
+    launch_keys(xyz, nloc, h->d_root, h->lkeys_in.p, h->lidx_in.p, st);
+    CKL();
+    size_t bytes = 0;
+    CK(sort_keys(nullptr, bytes, h->lkeys_in.p, h->lkeys.p, h->lidx_in.p, h->lperm.p, nloc, st));
+    CK(h->cub_tmp.ensure(bytes));
+    CK(sort_keys(h->cub_tmp.p, bytes, h->lkeys_in.p, h->lkeys.p, h->lidx_in.p, h->lperm.p, nloc, st));
+    ++h->stats.cub_calls;
+    launch_gather(xyz, q, h->lperm.p, nloc, h->lpos.p, st);
+    CKL();
+  }
+  // a4/a5: the global adaptive octree, level by level from allreduced split bounds
+  if (int rc = build_levels(h, N, h->lkeys.p, (int)nloc)) return rc;
+  // partition: contiguous runs of whole leaves, balanced by particle count
+  CK(h->d_off.ensure(R + 1));
+  CK(h->d_K.ensure(R + 1));
+  CK(h->d_lb.ensure(R + 1));
+  launch_partition(h->leaves.p, h->nleaves, h->cells(), h->cprefix.p, N, R, h->d_off.p, h->d_K.p, st);
+  CKL();
+  launch_key_bounds(h->lkeys.p, (int)nloc, h->d_K.p, R, h->d_lb.p, st);
+  CKL();
+  h->roff.assign(R + 1, 0);
+  std::vector<int> lb(R + 1);
+  CK(cudaMemcpyAsync(h->roff.data(), h->d_off.p, sizeof(int) * (R + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(lb.data(), h->d_lb.p, sizeof(int) * (R + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->own_lo = h->roff[me];
+  h->own_hi = h->roff[me + 1];
+  h->scnt_p.assign(R, 0);
+  for (int r = 0; r < R; ++r) h->scnt_p[r] = lb[r + 1] - lb[r];
+  if (int rc = exchange_counts(h, h->scnt_p, h->rcnt_p, 1)) return rc;
+  int64_t nown = 0;
+  for (int r = 0; r < R; ++r) nown += h->rcnt_p[r];
+  if (nown != h->own_hi - h->own_lo)
+    return fail(h, FMM_E_INVALID, "partition: received %lld particles for range [%d, %d)",
+                (long long)nown, h->own_lo, h->own_hi);
+  // particle alltoallv (Morton-sorted float4 + keys); each rank receives its leaves' particles
+  const size_t no1 = std::max<int64_t>(nown, 1);
+  CK(h->rpos.ensure(no1));
+  CK(h->rkeys.ensure(no1));
+  CK(h->rkeys_s.ensure(no1));
+  CK(h->ridx_in.ensure(no1));
+  CK(h->rperm.ensure(no1));
+  if (int rc = a2av(h, h->lpos.p, h->scnt_p, h->rpos.p, h->rcnt_p, sizeof(float4))) return rc;
+  if (int rc = a2av(h, h->lkeys.p, h->scnt_p, h->rkeys.p, h->rcnt_p, sizeof(uint64_t))) return rc;
+  // global sorted order of the own particles: stable sort by key (ties: source rank, then source
+  // order -- the order of a single sort of the concatenated shards)
+  CK(h->pos.ensure(std::max(N, 1)));
+  CK(h->acc.ensure(std::max(N, 1)));
+  CK(h->perm.ensure(std::max(N, 1)));
+  if (nown > 0) {
+    launch_iota(h->ridx_in.p, (int)nown, st);
+    CKL();
+    size_t bytes = 0;
+    CK(sort_keys(nullptr, bytes, h->rkeys.p, h->rkeys_s.p, h->ridx_in.p, h->rperm.p, nown, st));
+    CK(h->cub_tmp.ensure(bytes));
+    CK(sort_keys(h->cub_tmp.p, bytes, h->rkeys.p, h->rkeys_s.p, h->ridx_in.p, h->rperm.p, nown, st));
+    ++h->stats.cub_calls;
+    launch_gather4(h->rpos.p, h->rperm.p, (int)nown, h->pos.p + h->own_lo, st);
+    CKL();
+    CK(cudaMemcpyAsync(h->perm.p + h->own_lo, h->rperm.p, sizeof(unsigned) * nown,
+                       cudaMemcpyDeviceToDevice, st));
+  }
+  // own target leaves
+  const int total = h->ncells;
+  CK(h->tleaves.ensure(total));
+  launch_range_leaf_flags(total, h->cells(), h->own_lo, h->own_hi, h->leafflag.p, st);
+  CKL();
+  if (int rc = compact_flags(h, h->leafflag.p, total, (unsigned *)h->tleaves.p, &h->tleaves_n)) return rc;
+  h->part_lo = h->own_lo;
+  h->part_hi = h->own_hi;
+  // cells whose particles span several ranks: their multipoles are summed over the ranks
+  CK(h->strad_flag.ensure(total));
+  CK(h->strad_ids.ensure(total));
+  launch_straddle_flags(total, h->cells(), h->d_off.p, R, h->strad_flag.p, st);
+  CKL();
+  if (int rc = compact_flags(h, h->strad_flag.p, total, h->strad_ids.p, &h->nstrad)) return rc;
+  h->stats.n_global = N;
+  h->stats.rank_lo = h->own_lo;
+  h->stats.rank_hi = h->own_hi;
+  h->stats.n_straddle = h->nstrad;
+  return FMM_OK;
+}
+
+// Receiver-driven local essential tree (after the traversal; waits for the upward sweep). The
+// lists name every source this rank's targets need; multipoles of cells outside [own_lo, own_hi)
+// that do not straddle, and P2P source particles outside it, are requested from their owners.
+static int dist_let(fmm_ctx *h) {
+  cudaStream_t st = h->stream;
+  FmmComm *cm = h->comm;
+  const int R = cm->nranks, me = cm->rank, nc = h->ncells;
+  const int NCS = nc_stride(h->p);
+  CK(h->need_m.ensure(nc));
+  CK(h->need_p.ensure(nc));
+  CK(cudaMemsetAsync(h->need_m.p, 0, sizeof(int) * nc, st));
+  CK(cudaMemsetAsync(h->need_p.p, 0, sizeof(int) * nc, st));
+  launch_need_flags(h->lists(), (int)h->ntask[0], (int)h->ntask[1], (int)h->ntask[2], h->cells(),
+                    h->strad_flag.p, h->own_lo, h->own_hi, h->need_m.p, h->need_p.p, st);
+  CKL();
+  // multipole requests: cell ids grouped by owner
+  int nm = 0, npc = 0;
+  CK(h->req_ids.ensure(nc));
+  CK(h->req_own.ensure(nc));
+  CK(h->req_own_s.ensure(nc));
+  CK(h->mreq_s.ensure(nc));
+  if (int rc = compact_flags(h, h->need_m.p, nc, h->req_ids.p, &nm)) return rc;
+  launch_owner_of_cells(h->req_ids.p, nm, h->cells(), h->d_off.p, R, h->req_own.p, st);
+  std::vector<int64_t> cntM, cntP;
+  if (int rc = sort_by_owner(h, h->req_own.p, h->req_own_s.p, h->req_ids.p, h->mreq_s.p, nm, cntM)) return rc;
+  // particle requests: the remote pieces of every P2P source range, grouped by owner
+  CK(h->pcell.ensure(nc));
+  if (int rc = compact_flags(h, h->need_p.p, nc, h->pcell.p, &npc)) return rc;
+  CK(h->psize.ensure(std::max(npc, 1)));
+  CK(h->pexcl.ensure(std::max(npc, 1) + 1));
+  launch_piece_count(h->pcell.p, npc, h->cells(), h->d_off.p, R, me, h->psize.p, st);
+  int npieces = 0;
+  if (npc > 0) {
+    CKL();
+    if (int rc = cub_scan(h, h->psize.p, h->pexcl.p, npc)) return rc;
+    launch_level_total(h->psize.p, h->pexcl.p, npc, h->d_small, st);
+    CKL();
+    CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    npieces = h->h_small[0];
+  }
+  const size_t np1 = std::max(npieces, 1);
+  CK(h->pown.ensure(np1));
+  CK(h->pown_s.ensure(np1));
+  CK(h->pidx.ensure(np1));
+  CK(h->pidx_s.ensure(np1));
+  CK(h->prng.ensure(np1));
+  CK(h->prng_s.ensure(np1));
+  CK(h->prsize.ensure(np1));
+  CK(h->prexcl.ensure(np1 + 1));
+  launch_piece_write(h->pcell.p, npc, h->cells(), h->d_off.p, R, me, h->pexcl.p, h->pown.p,
+                     h->pidx.p, h->prng.p, st);
+  if (int rc = sort_by_owner(h, h->pown.p, h->pown_s.p, h->pidx.p, h->pidx_s.p, npieces, cntP)) return rc;
+  launch_gather_int2(h->prng.p, h->pidx_s.p, npieces, h->prng_s.p, h->prsize.p, st);
+  // particles per owner: exclusive scan of the sorted piece sizes, read at the owner boundaries
+  std::vector<int64_t> partP(R, 0);
+  if (npieces > 0) {
+    CKL();
+    if (int rc = cub_scan(h, h->prsize.p, h->prexcl.p, npieces)) return rc;
+    std::vector<int> ex(npieces + 1);
+    CK(cudaMemcpyAsync(ex.data(), h->prexcl.p, sizeof(int) * npieces, cudaMemcpyDeviceToHost, st));
+    std::vector<int2> last(1);
+    CK(cudaMemcpyAsync(last.data(), h->prng_s.p + npieces - 1, sizeof(int2), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ex[npieces] = ex[npieces - 1] + (last[0].y - last[0].x);
+    int64_t s0 = 0;
+    for (int r = 0; r < R; ++r) {
+      const int64_t s1 = s0 + cntP[r];
+      partP[r] = ex[s1] - ex[s0];
+      s0 = s1;
+    }
+  }
+  // request exchange: counts (multipoles, pieces, particles) then ids and ranges
+  std::vector<int64_t> send3((size_t)3 * R), recv3;
+  for (int r = 0; r < R; ++r) {
+    send3[3 * r] = cntM[r];
+    send3[3 * r + 1] = cntP[r];
+    send3[3 * r + 2] = partP[r];
+  }
+  if (int rc = exchange_counts(h, send3, recv3, 3)) return rc;
+  int64_t rM = 0, rP = 0, rPart = 0, gotPart = 0;
+  for (int r = 0; r < R; ++r) {
+    rM += recv3[3 * r];
+    rP += recv3[3 * r + 1];
+    rPart += recv3[3 * r + 2];
+    gotPart += partP[r];
+  }
+  CK(h->rreq_ids.ensure(std::max<int64_t>(rM, 1)));
+  CK(h->rreq_rng.ensure(std::max<int64_t>(rP, 1)));
+  if (int rc = a2av(h, h->mreq_s.p, send3, h->rreq_ids.p, recv3, sizeof(unsigned), 3, 0)) return rc;
+  if (int rc = a2av(h, h->prng_s.p, send3, h->rreq_rng.p, recv3, sizeof(int2), 3, 1)) return rc;
+  // the multipoles are complete once the upward sweep is done and the straddling cells are summed
+  CK(cudaStreamWaitEvent(st, h->ev_up, 0));
+  if (h->nstrad > 0) {
+    CK(h->rows_s.ensure((size_t)h->nstrad * NCS));
+    launch_rows(h->M.p, h->rows_s.p, NCS, h->strad_ids.p, h->nstrad, false, st);
+    CKL();
+    CC(cm->allreduce(h->rows_s.p, (size_t)h->nstrad * NCS * 2, CT_F32, CO_SUM, st));
+    launch_rows(h->rows_s.p, h->M.p, NCS, h->strad_ids.p, h->nstrad, true, st);
+    CKL();
+  }
+  // serve: multipole rows and particle ranges, in the order they were requested
+  CK(h->rows_s.ensure((size_t)std::max<int64_t>(rM, 1) * NCS));
+  CK(h->rows_r.ensure((size_t)std::max(nm, 1) * NCS));
+  launch_rows(h->M.p, h->rows_s.p, NCS, h->rreq_ids.p, (int)rM, false, st);
+  if (rM > 0) CKL();
+  if (int rc = a2av(h, h->rows_s.p, recv3, h->rows_r.p, send3, sizeof(float2) * NCS, 3, 0)) return rc;
+  launch_rows(h->rows_r.p, h->M.p, NCS, h->mreq_s.p, nm, true, st);
+  if (nm > 0) CKL();
+  CK(h->psz2.ensure(std::max<int64_t>(rP, 1)));
+  CK(h->pex2.ensure(std::max<int64_t>(rP, 1) + 1));
+  CK(h->pbuf_s.ensure(std::max<int64_t>(rPart, 1)));
+  CK(h->pbuf_r.ensure(std::max<int64_t>(gotPart, 1)));
+  if (rP > 0) {
+    launch_range_sizes(h->rreq_rng.p, (int)rP, h->psz2.p, st);
+    CKL();
+    if (int rc = cub_scan(h, h->psz2.p, h->pex2.p, (int)rP)) return rc;
+    launch_range_copy(h->pos.p, h->rreq_rng.p, h->pex2.p, (int)rP, h->pbuf_s.p, false, st);
+    CKL();
+  }
+  if (int rc = a2av(h, h->pbuf_s.p, recv3, h->pbuf_r.p, send3, sizeof(float4), 3, 2)) return rc;
+  if (npieces > 0) {
+    launch_range_copy(h->pos.p, h->prng_s.p, h->prexcl.p, npieces, h->pbuf_r.p, true, st);
+    CKL();
+  }
+  h->stats.let_cells = nm;
+  h->stats.let_particles = gotPart;
+  return FMM_OK;
+}
+
+// results of the own particles (written by L2P in received order) back to the ranks that own
+// them, then into the caller's order
+static int dist_return(fmm_ctx *h, float *phi, float *grad) {
+  const int64_t nloc = h->nloc;
+  CK(h->sphi.ensure(std::max<int64_t>(nloc, 1)));
+  CK(h->sgrad.ensure(3 * std::max<int64_t>(nloc, 1)));
+  if (int rc = a2av(h, h->rphi.p, h->rcnt_p, h->sphi.p, h->scnt_p, sizeof(float))) return rc;
+  if (int rc = a2av(h, h->rgrad.p, h->rcnt_p, h->sgrad.p, h->scnt_p, 3 * sizeof(float))) return rc;
+  launch_scatter_results(h->sphi.p, h->sgrad.p, h->lperm.p, (int)nloc, phi, grad, h->stream);
+  if (nloc > 0) CKL();
   return FMM_OK;
 }
 
@@ -448,7 +838,11 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
                          float *grad) {
   cudaStream_t st = h->stream;
   const int p = h->p, NC = nc_of(p);
-  if (int rc = build_tree(h, xyz, q, n)) return rc;
+  if (h->comm) {
+    if (int rc = dist_build_tree(h, xyz, q, n)) return rc;
+  } else {
+    if (int rc = build_tree(h, xyz, q, n)) return rc;
+  }
   record(h, EV_TREE);
   // a7/a8 upward sweep, on the aux stream: it overlaps the traversal and the M2L class sort (which
   // do not read M); the stream joins before the first kernel that reads M
@@ -458,7 +852,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   const int NCS = nc_stride(p);
   CK(h->M.ensure((size_t)h->ncells * NCS));
   CK(h->L.ensure((size_t)h->ncells * NCS));
-  if (NCS != NC) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, ua));
+  // (distributed: every cell starts at zero -- only the own leaves get a P2M, so the M2M leaves
+  // straddling cells with this rank's partial sum and remote cells at zero)
+  if (NCS != NC || h->comm) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, ua));
   // M2M / L2L: octant-class GEMMs on the tensor cores (p <= 10) unless disabled
   const char *scc = getenv("FMM_SHIFT_CUDA_CORES");
   const bool shift_tc = m2l_tc_supported(p) && h->ncells > 1 && !(scc && scc[0] && scc[0] != '0');
@@ -497,7 +893,8 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.launches += 3;
     h->stats.cub_calls += 1;
   }
-  launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, ua);
+  if (h->comm) launch_p2m(p, h->tleaves.p, h->tleaves_n, h->cells(), h->pos.p, h->M.p, ua);
+  else launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, ua);
   CKL();
   for (int level = h->depth - 1; level >= 0; --level) {
     if (shift_tc) {
@@ -512,6 +909,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   record_on(h, EV_UP, ua);
   CK(cudaEventRecord(h->ev_up, ua));
   if (int rc = traverse(h)) return rc;
+  if (h->comm) {  // local essential tree: remote multipoles and particles this rank's lists name
+    if (int rc = dist_let(h)) return rc;
+  }
   record(h, EV_TRAV);
   record(h, EV_M2L_PREP);  // re-recorded after the class sort when there are M2L pairs
   // a10 M2L (writes every cell's local expansion, zero where no M2L)
@@ -593,7 +993,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   CK(cudaStreamWaitEvent(st, h->ev_up, 0));  // (no M2L pairs: join here)
   record(h, EV_M2L);
   // a12 P2P (writes acc), a11 M2P (adds)
-  const int *tl = h->nparts > 1 ? h->tleaves.p : h->leaves.p;
+  const int *tl = (h->nparts > 1 || h->comm) ? h->tleaves.p : h->leaves.p;
   const int ntl = h->tleaves_n;
   launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p,
                     h->d_small + 12, st);
@@ -617,20 +1017,47 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
       CKL();
     }
   }
-  launch_l2p(p, tl, ntl, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, phi,
-             grad, far_local ? 1 : 0, st);
+  float *ophi = phi, *ograd = grad;
+  if (h->comm) {  // results in received order, routed back to the owners below
+    const int64_t nown = std::max(h->own_hi - h->own_lo, 1);
+    CK(h->rphi.ensure(nown));
+    CK(h->rgrad.ensure(3 * nown));
+    ophi = h->rphi.p;
+    ograd = h->rgrad.p;
+  }
+  launch_l2p(p, tl, ntl, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, ophi,
+             ograd, far_local ? 1 : 0, st);
   CKL();
+  if (h->comm) {
+    if (int rc = dist_return(h, phi, grad)) return rc;
+  }
   record(h, EV_DOWN);
   h->have_tree = true;
   return FMM_OK;
 }
 
+static void read_phase_times(fmm_ctx *h);
 static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
                          float *grad) {
   cudaStream_t st = h->stream;
   memset(&h->stats, 0, sizeof h->stats);
   h->stats.n = n;
   h->stats.p = h->p;
+  if (h->comm) {  // collective: every rank runs the pipeline, also with an empty shard
+    if (h->mode == FMM_DIRECT) return fail(h, FMM_E_INVALID, "FMM_DIRECT on a distributed handle");
+    record(h, EV_START);
+    h->last_n = n;
+    if (int rc = evaluate_tree(h, xyz, q, n, phi, grad)) return rc;
+    h->stats.ncells = h->ncells;
+    h->stats.nleaves = h->nleaves;
+    h->stats.depth = h->depth;
+    h->stats.n_m2l = h->ntask[0];
+    h->stats.n_m2p = h->ntask[1];
+    h->stats.n_p2p = h->ntask[2];
+    CK(cudaStreamSynchronize(st));
+    if (h->timing) read_phase_times(h);
+    return FMM_OK;
+  }
   if (n == 0) return FMM_OK;
   if (n > (int64_t)1 << 28) return fail(h, FMM_E_INVALID, "n = %lld exceeds 2^28 per device", (long long)n);
   record(h, EV_START);
@@ -668,7 +1095,12 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.n_p2p = h->ntask[2];
   }
   CK(cudaStreamSynchronize(st));
-  if (h->timing) {
+  if (h->timing) read_phase_times(h);
+  return FMM_OK;
+}
+
+static void read_phase_times(fmm_ctx *h) {
+  {
     float ms[EV_N];
     for (int e = 1; e < EV_N; ++e) cudaEventElapsedTime(&ms[e], h->ev[e - 1], h->ev[e]);
     cudaEventElapsedTime(&ms[0], h->ev[EV_START], h->ev[EV_DOWN]);
@@ -685,7 +1117,6 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.ms_m2p = ms[EV_M2P];
     h->stats.ms_downward = ms[EV_DOWN];
   }
-  return FMM_OK;
 }
 
 // ---- a6: kernel pre-calculation ------------------------------------
@@ -805,6 +1236,23 @@ int fmm_destroy(fmm_t h) {
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
   h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
   h->outA.release(); h->outB.release(); h->stack.release();
+  for (auto *b : {&h->d_off, &h->d_lb, &h->d_cnt, &h->strad_flag, &h->strad_excl, &h->need_m,
+                  &h->need_p, &h->dexcl, &h->psize, &h->pexcl, &h->prsize, &h->prexcl, &h->psz2,
+                  &h->pex2})
+    b->release();
+  for (auto *b : {&h->lidx_in, &h->lperm, &h->ridx_in, &h->rperm, &h->strad_ids, &h->req_ids,
+                  &h->req_own, &h->req_own_s, &h->mreq_s, &h->rreq_ids, &h->pcell, &h->pown,
+                  &h->pown_s, &h->pidx, &h->pidx_s})
+    b->release();
+  for (auto *b : {&h->d_K, &h->lkeys_in, &h->lkeys, &h->rkeys, &h->rkeys_s}) b->release();
+  for (auto *b : {&h->lpos, &h->rpos, &h->pbuf_s, &h->pbuf_r}) b->release();
+  for (auto *b : {&h->prng, &h->prng_s, &h->rreq_rng}) b->release();
+  for (auto *b : {&h->rphi, &h->rgrad, &h->sphi, &h->sgrad}) b->release();
+  h->rows_s.release();
+  h->rows_r.release();
+  h->d_i64.release();
+  h->d_cost.release();
+  delete h->comm;
   if (h->d_root) cudaFree(h->d_root);
   if (h->d_mm) cudaFree(h->d_mm);
   if (h->d_small) cudaFree(h->d_small);
@@ -826,18 +1274,21 @@ int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float
                  float *d_grad) {
   if (!h) return FMM_E_INVALID;
   if (n < 0) return fail(h, FMM_E_INVALID, "n < 0");
-  if (n == 0) {
+  if (n == 0 && !h->comm) {
     memset(&h->stats, 0, sizeof h->stats);
     return FMM_OK;
   }
-  if (!d_xyz || !d_q || !d_phi || !d_grad) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
+  if (n > 0 && (!d_xyz || !d_q || !d_phi || !d_grad)) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
   int cur = -1;
   cudaGetDevice(&cur);
   if (cur != h->device) cudaSetDevice(h->device);
-  int rc = check_device_ptr(h, d_xyz, "xyz");
-  if (!rc) rc = check_device_ptr(h, d_q, "q");
-  if (!rc) rc = check_device_ptr(h, d_phi, "phi");
-  if (!rc) rc = check_device_ptr(h, d_grad, "grad");
+  int rc = FMM_OK;
+  if (n > 0) {
+    rc = check_device_ptr(h, d_xyz, "xyz");
+    if (!rc) rc = check_device_ptr(h, d_q, "q");
+    if (!rc) rc = check_device_ptr(h, d_phi, "phi");
+    if (!rc) rc = check_device_ptr(h, d_grad, "grad");
+  }
   if (!rc) rc = evaluate_impl(h, d_xyz, d_q, n, d_phi, d_grad);
   if (cur != h->device && cur >= 0) cudaSetDevice(cur);
   return rc;
@@ -847,17 +1298,18 @@ int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, 
                       float *h_grad) {
   if (!h) return FMM_E_INVALID;
   if (n < 0) return fail(h, FMM_E_INVALID, "n < 0");
-  if (n == 0) return FMM_OK;
-  if (!h_xyz || !h_q || !h_phi || !h_grad) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
-  CK(h->host_stage.ensure(8 * (size_t)n));  // grow-only device staging (no per-call malloc)
+  if (n == 0 && !h->comm) return FMM_OK;
+  if (n > 0 && (!h_xyz || !h_q || !h_phi || !h_grad)) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
+  CK(h->host_stage.ensure(8 * std::max<size_t>((size_t)n, 1)));  // grow-only device staging (no per-call malloc)
   float *d = h->host_stage.p;
   float *xyz = d, *q = d + 3 * n, *phi = d + 4 * n, *grad = d + 5 * n;
   int rc = FMM_OK;
-  cudaError_t e = cudaMemcpyAsync(xyz, h_xyz, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, h->stream);
-  if (!e) e = cudaMemcpyAsync(q, h_q, sizeof(float) * n, cudaMemcpyHostToDevice, h->stream);
+  cudaError_t e = cudaSuccess;
+  if (n > 0) e = cudaMemcpyAsync(xyz, h_xyz, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, h->stream);
+  if (!e && n > 0) e = cudaMemcpyAsync(q, h_q, sizeof(float) * n, cudaMemcpyHostToDevice, h->stream);
   if (e) rc = fail(h, FMM_E_CUDA, "H2D: %s", cudaGetErrorString(e));
   if (!rc) rc = evaluate_impl(h, xyz, q, n, phi, grad);
-  if (!rc) {
+  if (!rc && n > 0) {
     e = cudaMemcpyAsync(h_phi, phi, sizeof(float) * n, cudaMemcpyDeviceToHost, h->stream);
     if (!e) e = cudaMemcpyAsync(h_grad, grad, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, h->stream);
     if (!e) e = cudaStreamSynchronize(h->stream);
@@ -891,9 +1343,20 @@ int fmm_set_deterministic(fmm_t h, int enable) {
   return FMM_OK;
 }
 
+static int attach_comm(fmm_ctx *h, FmmComm *c);
+
 int fmm_tune(fmm_t h) {
   if (!h) return FMM_E_INVALID;
-  return tune_impl(h);
+  // the pre-calculation is a single-GPU run on synthetic data; a distributed handle then takes
+  // rank 0's table again (collective)
+  FmmComm *c = h->comm;
+  h->comm = nullptr;
+  int rc = tune_impl(h);
+  if (c) {
+    const int rc2 = attach_comm(h, c);
+    if (!rc) rc = rc2;
+  }
+  return rc;
 }
 
 int fmm_get_cost_model(fmm_t h, fmm_cost_t *out) {
@@ -974,6 +1437,7 @@ int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, dou
                     double *h_L) {
   if (!h) return FMM_E_INVALID;
   if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
+  if (h->comm) return fail(h, FMM_E_INVALID, "fmm_export_perm: not available on distributed handles");
   const int64_t n = h->last_n;
   if (cap < n) return fail(h, FMM_E_INVALID, "cap too small");
   std::vector<unsigned> perm(n);
@@ -987,6 +1451,7 @@ int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, dou
 
 int fmm_set_partition(fmm_t h, int nparts, int part) {
   if (!h) return FMM_E_INVALID;
+  if (h->comm) return fail(h, FMM_E_INVALID, "fmm_set_partition: distributed handles partition themselves");
   if (nparts < 1 || part < 0 || part >= nparts)
     return fail(h, FMM_E_INVALID, "bad partition %d of %d", part, nparts);
   h->nparts = nparts;
@@ -1015,6 +1480,85 @@ int fmm_partition_indices(fmm_t h, int64_t *d_out, int64_t cap, int64_t *count_o
     CK(cudaStreamSynchronize(h->stream));
   }
   return FMM_OK;
+}
+
+static int attach_comm(fmm_ctx *h, FmmComm *c) {
+  // rank 0's measured cost table on every rank (the per-pair kind choice must
+  // not depend on the rank that evaluates the pair)
+  h->comm = c;
+  double v[3] = {h->cost.t_pp, h->cost.t_mp, h->cost.t_ml};
+  if (c->rank != 0) v[0] = v[1] = v[2] = 0.0;
+  CK(h->d_cost.ensure(3));
+  CK(cudaMemcpyAsync(h->d_cost.p, v, sizeof v, cudaMemcpyHostToDevice, h->stream));
+  CC(c->allreduce(h->d_cost.p, 3, CT_F64, CO_SUM, h->stream));
+  CK(cudaMemcpyAsync(v, h->d_cost.p, sizeof v, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->cost.t_pp = v[0];
+  h->cost.t_mp = v[1];
+  h->cost.t_ml = v[2];
+  return FMM_OK;
+}
+
+int fmm_comm_unique_id(unsigned char h_id[128]) {
+  if (!h_id) return FMM_E_INVALID;
+  std::string err;
+  const int rc = comm_nccl_unique_id(h_id, err);
+  if (rc) fprintf(stderr, "fmm_comm_unique_id: %s\n", err.c_str());
+  return rc;
+}
+
+int fmm_create_dist(fmm_t *out, int p, double theta, int ncrit, int nranks, int rank,
+                    const unsigned char h_id[128]) {
+  if (!out) return FMM_E_INVALID;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks || !h_id) return FMM_E_INVALID;
+  int rc = fmm_create(out, p, theta, ncrit);
+  if (rc) return rc;
+  std::string err;
+  FmmComm *c = comm_nccl_create(nranks, rank, h_id, err);
+  if (!c) {
+    fprintf(stderr, "fmm_create_dist: %s\n", err.c_str());
+    fmm_destroy(*out);
+    *out = nullptr;
+    return FMM_E_NCCL;
+  }
+  if ((rc = attach_comm(*out, c))) {
+    fprintf(stderr, "fmm_create_dist: %s\n", (*out)->err.c_str());
+    fmm_destroy(*out);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+int fmm_group_create(fmm_group_t *out, int nranks) {
+  if (!out || nranks < 1 || nranks > 16) return FMM_E_INVALID;
+  *out = comm_group_create(nranks);
+  return FMM_OK;
+}
+
+int fmm_group_destroy(fmm_group_t g) {
+  comm_group_destroy(g);
+  return FMM_OK;
+}
+
+int fmm_create_in_group(fmm_t *out, int p, double theta, int ncrit, fmm_group_t g, int rank) {
+  if (!out) return FMM_E_INVALID;
+  *out = nullptr;
+  if (!g) return FMM_E_INVALID;
+  int rc = fmm_create(out, p, theta, ncrit);
+  if (rc) return rc;
+  std::string err;
+  FmmComm *c = comm_local_create(g, rank, err);
+  if (!c) {
+    fmm_destroy(*out);
+    *out = nullptr;
+    return FMM_E_INVALID;
+  }
+  if ((rc = attach_comm(*out, c))) {
+    fmm_destroy(*out);
+    *out = nullptr;
+  }
+  return rc;
 }
 
 const char *fmm_strerror(int code) {

@@ -20,6 +20,13 @@ void launch_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64_t *pr
                       cudaStream_t st);
 void launch_split(int c0, int nl, int level, int ncrit, const uint64_t *keys, CellsView C,
                   const uint64_t *prefix, int *nch, int2 *crange, int *bnd, cudaStream_t st);
+void launch_split_bounds(int c0, int nl, int level, int ncrit, const uint64_t *keys, int nloc,
+                         CellsView C, const uint64_t *prefix, int *bnd, cudaStream_t st);
+void launch_split_ranges(int c0, int nl, int level, int ncrit, CellsView C, const int *bnd,
+                         int *nch, int2 *crange, cudaStream_t st);
+void launch_bbox_local(const float *xyz, const float *q, int64_t n, unsigned *mm, RootInfo *root,
+                       cudaStream_t st);
+void launch_root_from_mm(const unsigned *mm, RootInfo *root, cudaStream_t st);
 void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int *excl,
                  const int2 *crange, const RootInfo *root, CellsView C, uint64_t *prefix,
                  cudaStream_t st);
@@ -143,3 +150,36 @@ void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cu
 // ---- synthetic batches for the kernel pre-calculation (autotune.cu) ----
 void launch_fill_random(float *dst, int64_t n, unsigned seed, float lo, float hi,
                         cudaStream_t st);
+
+// ---- dist.cu (multi-GPU evaluation) ----
+void launch_iota(unsigned *a, int n, cudaStream_t st);
+void launch_gather4(const float4 *src, const unsigned *perm, int n, float4 *dst, cudaStream_t st);
+void launch_partition(const int *leaves, int nleaves, CellsView C, const uint64_t *prefix, int N,
+                      int R, int *off, uint64_t *K, cudaStream_t st);
+void launch_key_bounds(const uint64_t *keys, int n, const uint64_t *K, int R, int *lb,
+                       cudaStream_t st);
+void launch_range_leaf_flags(int ncells, CellsView C, int lo, int hi, int *flag, cudaStream_t st);
+void launch_straddle_flags(int ncells, CellsView C, const int *off, int R, int *flag,
+                           cudaStream_t st);
+void launch_rows(const float2 *src, float2 *dst, int stride, const unsigned *ids, int n,
+                 bool to_ids, cudaStream_t st);
+void launch_need_flags(ListsView Ls, int n_m2l, int n_m2p, int n_p2p, CellsView C,
+                       const int *strad, int lo, int hi, int *needM, int *needP, cudaStream_t st);
+void launch_owner_of_cells(const unsigned *ids, int n, CellsView C, const int *off, int R,
+                           unsigned *owner, cudaStream_t st);
+void launch_piece_count(const unsigned *ids, int n, CellsView C, const int *off, int R, int me,
+                        int *cnt, cudaStream_t st);
+void launch_piece_write(const unsigned *ids, int n, CellsView C, const int *off, int R, int me,
+                        const int *excl, unsigned *owner, unsigned *pidx, int2 *rng,
+                        cudaStream_t st);
+void launch_gather_int2(const int2 *src, const unsigned *idx, int n, int2 *dst, int *size,
+                        cudaStream_t st);
+void launch_range_sizes(const int2 *rng, int n, int *size, cudaStream_t st);
+void launch_owner_hist(const unsigned *owner, int n, int *counts, cudaStream_t st);
+void launch_range_copy(float4 *pos, const int2 *rng, const int *roff, int n, float4 *buf,
+                       bool to_pos, cudaStream_t st);
+void launch_scatter_results(const float *rphi, const float *rgrad, const unsigned *perm, int n,
+                            float *phi, float *grad, cudaStream_t st);
+cudaError_t sort_owner_pairs(void *tmp, size_t &tmp_bytes, const unsigned *kin, unsigned *kout,
+                             const unsigned *vin, unsigned *vout, int n, int bits,
+                             cudaStream_t st);

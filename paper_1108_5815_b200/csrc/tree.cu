@@ -181,22 +181,30 @@ __global__ void k_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64
 // per (cell, octant o): bnd[8k + o] = first index of the cell whose child prefix is >= base + o
 // (8 independent searches instead of 8 sequential ones per cell: short latency chains at the top
 // levels where there are few cells and long ranges).
+// Distributed build (nloc >= 0): the keys are this rank's locally sorted shard and the search runs
+// over all of it, so bnd = the number of LOCAL keys below the child's first key; the sum of bnd
+// over the ranks (one allreduce per level) is the global sorted index of the child's first key,
+// i.e. exactly what a single-GPU build over the union would find. Unsplit cells write 0.
+__device__ __forceinline__ bool split_cell(int n, int ncrit, int level) {
+  return n > ncrit && level < FMM_LEVELS;
+}
+
 __global__ void __launch_bounds__(256) k_split(int c0, int nl, int level, int ncrit,
-                                               const uint64_t *__restrict__ keys, CellsView C,
-                                               const uint64_t *__restrict__ prefix,
+                                               const uint64_t *__restrict__ keys, int nloc,
+                                               CellsView C, const uint64_t *__restrict__ prefix,
                                                int *__restrict__ bnd) {
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= 8 * nl) return;
   const int k = id >> 3, o = id & 7;
   const int c = c0 + k;
   const int b = C.beg[c], n = C.cnt[c];
-  if (!(n > ncrit && level < FMM_LEVELS)) {
-    bnd[id] = -1;
+  if (!split_cell(n, ncrit, level)) {
+    bnd[id] = 0;
     return;
   }
   const int shift = 3 * (FMM_LEVELS - (level + 1));
   const uint64_t tgt = prefix[c] * 8 + (uint64_t)o;
-  int l = b, r = b + n;
+  int l = nloc >= 0 ? 0 : b, r = nloc >= 0 ? nloc : b + n;
   while (l < r) {
     const int m = (l + r) >> 1;
     if ((keys[m] >> shift) < tgt) l = m + 1;
@@ -206,15 +214,16 @@ __global__ void __launch_bounds__(256) k_split(int c0, int nl, int level, int nc
 }
 
 // child ranges from the 8 boundaries of each cell (non-empty octants, Morton order)
-__global__ void __launch_bounds__(256) k_split_ranges(int c0, int nl, CellsView C,
-                                                      const int *__restrict__ bnd,
+__global__ void __launch_bounds__(256) k_split_ranges(int c0, int nl, int level, int ncrit,
+                                                      CellsView C, const int *__restrict__ bnd,
                                                       int *__restrict__ nch,
                                                       int2 *__restrict__ crange) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nl) return;
   int cnt = 0;
-  if (bnd[8 * k] >= 0) {
-    const int c = c0 + k, end = C.beg[c] + C.cnt[c];
+  const int c = c0 + k;
+  if (split_cell(C.cnt[c], ncrit, level)) {
+    const int end = C.beg[c] + C.cnt[c];
     for (int o = 0; o < 8; ++o) {
       const int lo = bnd[8 * k + o], hi = o < 7 ? bnd[8 * k + o + 1] : end;
       if (hi > lo) crange[8 * k + cnt++] = make_int2(lo, (hi - lo) | (o << 28));
@@ -311,6 +320,20 @@ void launch_bbox(const float *xyz, const float *q, int64_t n, unsigned *mm, Root
   k_bbox<<<grid_for(n, 256), 256, 0, st>>>(xyz, q, n, mm, root);
   k_root<<<1, 1, 0, st>>>(mm, root);
 }
+// distributed bbox: the local min/max (and the non-finite flag in mm[6]) before the allreduce,
+// then the root cube from the reduced values
+__global__ void k_nonfinite_to_mm(unsigned *mm, RootInfo *root) { mm[6] = root->nonfinite; }
+__global__ void k_mm_to_nonfinite(const unsigned *mm, RootInfo *root) { root->nonfinite = mm[6]; }
+void launch_bbox_local(const float *xyz, const float *q, int64_t n, unsigned *mm, RootInfo *root,
+                       cudaStream_t st) {
+  k_bbox_init<<<1, 32, 0, st>>>(mm, root);
+  if (n > 0) k_bbox<<<grid_for(n, 256), 256, 0, st>>>(xyz, q, n, mm, root);
+  k_nonfinite_to_mm<<<1, 1, 0, st>>>(mm, root);
+}
+void launch_root_from_mm(const unsigned *mm, RootInfo *root, cudaStream_t st) {
+  k_mm_to_nonfinite<<<1, 1, 0, st>>>(mm, root);
+  k_root<<<1, 1, 0, st>>>(mm, root);
+}
 void launch_keys(const float *xyz, int64_t n, const RootInfo *root, uint64_t *keys, unsigned *idx,
                  cudaStream_t st) {
   k_keys<<<grid_for(n, 256), 256, 0, st>>>(xyz, n, root, keys, idx);
@@ -333,8 +356,16 @@ void launch_root_cell(int64_t n, const RootInfo *root, CellsView C, uint64_t *pr
 }
 void launch_split(int c0, int nl, int level, int ncrit, const uint64_t *keys, CellsView C,
                   const uint64_t *prefix, int *nch, int2 *crange, int *bnd, cudaStream_t st) {
-  k_split<<<(8 * nl + 255) / 256, 256, 0, st>>>(c0, nl, level, ncrit, keys, C, prefix, bnd);
-  k_split_ranges<<<(nl + 255) / 256, 256, 0, st>>>(c0, nl, C, bnd, nch, crange);
+  launch_split_bounds(c0, nl, level, ncrit, keys, -1, C, prefix, bnd, st);
+  launch_split_ranges(c0, nl, level, ncrit, C, bnd, nch, crange, st);
+}
+void launch_split_bounds(int c0, int nl, int level, int ncrit, const uint64_t *keys, int nloc,
+                         CellsView C, const uint64_t *prefix, int *bnd, cudaStream_t st) {
+  k_split<<<(8 * nl + 255) / 256, 256, 0, st>>>(c0, nl, level, ncrit, keys, nloc, C, prefix, bnd);
+}
+void launch_split_ranges(int c0, int nl, int level, int ncrit, CellsView C, const int *bnd,
+                         int *nch, int2 *crange, cudaStream_t st) {
+  k_split_ranges<<<(nl + 255) / 256, 256, 0, st>>>(c0, nl, level, ncrit, C, bnd, nch, crange);
 }
 void launch_emit(int c0, int nl, int next0, int level, const int *nch, const int *excl,
                  const int2 *crange, const RootInfo *root, CellsView C, uint64_t *prefix,

@@ -15,7 +15,8 @@ SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_host", "fm
            "fmm_set_mode", "fmm_set_timing", "fmm_set_deterministic", "fmm_tune", "fmm_get_cost_model",
            "fmm_set_cost_model", "fmm_get_stats", "fmm_export_tree", "fmm_export_lists",
            "fmm_export_perm", "fmm_set_partition", "fmm_get_partition", "fmm_partition_indices",
-           "fmm_strerror", "fmm_last_error"]
+           "fmm_comm_unique_id", "fmm_create_dist", "fmm_group_create", "fmm_group_destroy",
+           "fmm_create_in_group", "fmm_strerror", "fmm_last_error"]
 
 
 class FmmError(RuntimeError):
@@ -35,7 +36,10 @@ class Stats(C.Structure):
                 ("ms_total", C.c_double), ("ms_tree", C.c_double), ("ms_upward", C.c_double),
                 ("ms_traverse", C.c_double), ("ms_m2l", C.c_double), ("ms_p2p", C.c_double),
                 ("ms_m2p", C.c_double), ("ms_downward", C.c_double),
-                ("launches", C.c_int64), ("cub_calls", C.c_int64)]
+                ("launches", C.c_int64), ("cub_calls", C.c_int64),
+                ("n_global", C.c_int64), ("rank_lo", C.c_int64), ("rank_hi", C.c_int64),
+                ("n_straddle", C.c_int64), ("let_cells", C.c_int64), ("let_particles", C.c_int64),
+                ("bytes_sent", C.c_int64), ("ms_comm", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -77,6 +81,11 @@ def load_library():
     L.fmm_set_partition.argtypes = [vp, C.c_int, C.c_int]
     L.fmm_get_partition.argtypes = [vp, P(i64), P(i64)]
     L.fmm_partition_indices.argtypes = [vp, vp, i64, P(i64)]
+    L.fmm_comm_unique_id.argtypes = [vp]
+    L.fmm_create_dist.argtypes = [P(vp), C.c_int, dp, C.c_int, C.c_int, C.c_int, vp]
+    L.fmm_group_create.argtypes = [P(vp), C.c_int]
+    L.fmm_group_destroy.argtypes = [vp]
+    L.fmm_create_in_group.argtypes = [P(vp), C.c_int, dp, C.c_int, vp, C.c_int]
     L.fmm_strerror.argtypes = [C.c_int]
     L.fmm_strerror.restype = C.c_char_p
     L.fmm_last_error.argtypes = [vp]
@@ -94,23 +103,71 @@ def _ptr(a) -> int:
     return a.data_ptr()
 
 
+class LocalGroup:
+    """In-process group of `nranks` distributed handles (fmm_group_create): one host thread per
+    handle, the ranks may share one GPU. Runs the multi-GPU algorithm on a single device."""
+
+    def __init__(self, nranks: int):
+        self.L = load_library()
+        g = C.c_void_p()
+        rc = self.L.fmm_group_create(C.byref(g), int(nranks))
+        if rc != 0:
+            raise FmmError(f"fmm_group_create: {self.L.fmm_strerror(rc).decode()}")
+        self.g, self.nranks = g, nranks
+
+    def close(self):
+        if getattr(self, "g", None):
+            self.L.fmm_group_destroy(self.g)
+            self.g = None
+
+    __del__ = close
+
+
+def nccl_unique_id() -> np.ndarray:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks)."""
+    L = load_library()
+    uid = np.zeros(128, np.uint8)
+    rc = L.fmm_comm_unique_id(uid.ctypes.data)
+    if rc != 0:
+        raise FmmError(f"fmm_comm_unique_id: {L.fmm_strerror(rc).decode()}")
+    return uid
+
+
 class FMM:
-    """Handle on the current CUDA device: FMM(p, theta, ncrit, mode='hybrid')."""
+    """Handle on the current CUDA device: FMM(p, theta, ncrit, mode='hybrid').
+
+    Distributed handles (fmm.h, multi-GPU): `nccl=(nranks, rank, uid)` joins an NCCL communicator
+    (uid from `nccl_unique_id()` on rank 0); `group=(LocalGroup, rank)` joins an in-process group.
+    Their `evaluate` is collective and takes / returns the rank's own particle shard."""
 
     def __init__(self, p: int = 10, theta: float = 0.4, ncrit: int = 64, mode: str = "hybrid",
-                 tune: bool = True):
+                 tune: bool = True, nccl=None, group=None):
         self.L = load_library()
         self.p, self.theta, self.ncrit = p, theta, ncrit
+        self.distributed = nccl is not None or group is not None
         h = C.c_void_p()
         if not tune:
             os.environ["FMM_NO_TUNE"] = "1"
         try:
-            rc = self.L.fmm_create(C.byref(h), int(p), float(theta), int(ncrit))
+            if nccl is not None:
+                nr, rk, uid = nccl
+                uid = np.ascontiguousarray(np.asarray(uid, np.uint8).reshape(128))
+                rc = self.L.fmm_create_dist(C.byref(h), int(p), float(theta), int(ncrit), int(nr),
+                                            int(rk), uid.ctypes.data)
+                what = "fmm_create_dist"
+            elif group is not None:
+                grp, rk = group
+                rc = self.L.fmm_create_in_group(C.byref(h), int(p), float(theta), int(ncrit),
+                                                grp.g, int(rk))
+                what = "fmm_create_in_group"
+            else:
+                rc = self.L.fmm_create(C.byref(h), int(p), float(theta), int(ncrit))
+                what = "fmm_create"
         finally:
             if not tune:
                 os.environ.pop("FMM_NO_TUNE", None)
         if rc != 0:
-            raise FmmError(f"fmm_create: {self.L.fmm_strerror(rc).decode()}")
+            raise FmmError(f"{what}: {self.L.fmm_strerror(rc).decode()}")
         self.h = h
         self.set_mode(mode)
 
@@ -168,6 +225,8 @@ class FMM:
             phi = torch.empty(n, dtype=torch.float32, device=xyz.device)
         if grad is None:
             grad = torch.empty((n, 3), dtype=torch.float32, device=xyz.device)
+        if n == 0 and not self.distributed:
+            return phi, grad
         self._check(self.L.fmm_set_stream(self.h, C.c_void_p(torch.cuda.current_stream().cuda_stream)),
                     "fmm_set_stream")
         self._check(self.L.fmm_evaluate(self.h, xyz.data_ptr(), q.data_ptr(), n, phi.data_ptr(),

@@ -1,0 +1,150 @@
+"""GPU tests of the distributed evaluation (include/fmm.h multi-GPU section): R ranks
+as an in-process group on one GPU (fmm_group_create / fmm_create_in_group, one host thread per
+rank). The algorithm and every kernel are those of the NCCL path; only the transport differs.
+
+Bars: the global tree of every rank equals the single-GPU tree bit for bit; the union of the
+per-rank interaction lists equals the single-GPU lists (as a set, no rank listing a pair twice);
+phi / grad of every particle match the single-GPU evaluation and the FP64 oracle within 1e-5
+relative L2 (SURVEY §8(c) bar), whatever the initial (random, uneven) distribution of particles.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from fmm_inputs import make_particles
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import oracle as O  # noqa: E402
+from paper_1108_5815_b200 import FMM  # noqa: E402
+from paper_1108_5815_b200.fmm import LocalGroup  # noqa: E402
+
+COST = (2e-12, 6e-11, 2.5e-9)
+
+
+def shards(n, R, seed, empty_rank=None):
+    """Random, uneven assignment of the particle indices to R ranks (optionally one empty)."""
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n)
+    w = rng.uniform(0.3, 1.7, R)
+    if empty_rank is not None:
+        w[empty_rank] = 0.0
+    cuts = np.floor(np.cumsum(w) / w.sum() * n).astype(int)
+    cuts[-1] = n
+    return np.split(perm, cuts[:-1])
+
+
+def run_group(R, xyz, q, parts, p, theta, ncrit, mode, evals=1):
+    grp = LocalGroup(R)
+    out = [None] * R
+    errs = []
+
+    def worker(r):
+        f = None
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                f = FMM(p=p, theta=theta, ncrit=ncrit, mode=mode, tune=False, group=(grp, r))
+                f.set_cost_model(*COST)
+                x = torch.from_numpy(np.ascontiguousarray(xyz[parts[r]])).cuda()
+                c = torch.from_numpy(np.ascontiguousarray(q[parts[r]])).cuda()
+                for _ in range(evals):
+                    phi, grad = f.evaluate(x, c)
+                s.synchronize()
+                out[r] = dict(phi=phi.cpu().numpy().astype(np.float64),
+                              grad=grad.cpu().numpy().astype(np.float64),
+                              lists=f.export_lists(), tree=f.export_tree(), stats=f.stats())
+        except Exception as e:  # noqa: BLE001
+            errs.append((r, e))
+        finally:
+            if f is not None:
+                f.close()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in th), "a rank hung"
+    grp.close()
+    assert not errs, errs
+    return out
+
+
+def single(xyz, q, p, theta, ncrit, mode):
+    f = FMM(p=p, theta=theta, ncrit=ncrit, mode=mode, tune=False)
+    f.set_cost_model(*COST)
+    phi, grad = f.evaluate(torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda())
+    torch.cuda.synchronize()
+    res = dict(phi=phi.cpu().numpy().astype(np.float64), grad=grad.cpu().numpy().astype(np.float64),
+               lists=f.export_lists(), tree=f.export_tree())
+    f.close()
+    return res
+
+
+def as_set(lists):
+    c = O.canonical_tasks(lists)
+    return c, {tuple(r) for r in c.tolist()}
+
+
+CASES = [  # (R, dist, n, p, theta, ncrit, mode, empty rank)
+    (2, "uniform", 20000, 6, 0.5, 32, "hybrid", None),
+    (3, "plummer", 30000, 8, 0.45, 32, "hybrid", None),
+    (4, "uniform", 12000, 5, 0.4, 16, "fmm", 2),
+    (4, "plummer", 16000, 6, 0.5, 24, "treecode", None),
+    (2, "mixed", 5000, 10, 0.4, 64, "hybrid", 0),
+]
+
+
+@pytest.mark.parametrize("R,dist,n,p,theta,ncrit,mode,empty", CASES)
+def test_dist_equals_single_gpu(R, dist, n, p, theta, ncrit, mode, empty):
+    xyz, q = make_particles(n, dist, 50 + R)
+    parts = shards(n, R, 7 + R, empty)
+    ref = single(xyz, q, p, theta, ncrit, mode)
+    out = run_group(R, xyz, q, parts, p, theta, ncrit, mode)
+    # the global tree on every rank
+    for o in out:
+        for k in ("level", "prefix", "begin", "count"):
+            assert np.array_equal(o["tree"][k], ref["tree"][k]), k
+    # lists: union over the ranks = single-GPU lists; no rank lists a pair twice
+    _, ref_set = as_set(ref["lists"])
+    union = set()
+    for o in out:
+        c, s = as_set(o["lists"])
+        assert len(s) == len(c)
+        union |= s
+    assert union == ref_set
+    # fields, back in every rank's own order
+    phi = np.zeros(n)
+    grad = np.zeros((n, 3))
+    for r, o in enumerate(out):
+        assert o["phi"].shape == (len(parts[r]),)
+        phi[parts[r]] = o["phi"]
+        grad[parts[r]] = o["grad"]
+    assert O.rel_l2(phi, ref["phi"]) < 1e-6 and O.rel_l2(grad, ref["grad"]) < 1e-6
+    orc = O.fmm(xyz, q, p, theta, ncrit, {"hybrid": O.HYBRID, "fmm": O.FMM, "treecode": O.TREECODE}[mode],
+                cost=COST)
+    assert O.rel_l2(phi, orc.phi) < 1e-5 and O.rel_l2(grad, orc.grad) < 1e-5
+    # every rank's targets are whole leaves and the ranges tile [0, N)
+    lo = sorted((o["stats"]["rank_lo"], o["stats"]["rank_hi"]) for o in out)
+    assert lo[0][0] == 0 and lo[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(lo, lo[1:]))
+    if R > 1:
+        assert sum(o["stats"]["let_cells"] + o["stats"]["let_particles"] for o in out) > 0
+
+
+def test_dist_repeated_and_single_rank():
+    # a 1-rank group is the single-GPU path with a trivial exchange; repeated evaluations reuse
+    # the grown buffers
+    xyz, q = make_particles(6000, "plummer", 77)
+    ref = single(xyz, q, 6, 0.5, 32, "hybrid")
+    out = run_group(1, xyz, q, [np.arange(6000)], 6, 0.5, 32, "hybrid", evals=2)
+    assert O.rel_l2(out[0]["phi"], ref["phi"]) < 1e-6
+    out = run_group(3, xyz, q, shards(6000, 3, 1), 6, 0.5, 32, "hybrid", evals=3)
+    assert out[0]["stats"]["n_global"] == 6000
