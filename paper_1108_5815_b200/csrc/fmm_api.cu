@@ -119,7 +119,9 @@ struct fmm_ctx {
   DBuf<float> m2l_T;
   DBuf<unsigned> m2l_Ttc;
   bool m2l_tc_used = false;
-  DBuf<int4> m2l_items;
+  DBuf<int4> m2l_items, m2l_items_raw;
+  DBuf<int> m2l_rflag, m2l_rid, m2l_rstart, m2l_gid_of;
+  DBuf<unsigned> m2l_ikeys_in, m2l_ikeys, m2l_iidx_in, m2l_iidx;
   DBuf<float> m2l_Y;  // also the per-cell slots of the tensor-core M2M / L2L
   // M2M / L2L as octant-class GEMMs on the tensor cores
   DBuf<unsigned> sh_keys_in, sh_keys, sh_vals_in, sh_cells, sh_src, sh_T;
@@ -955,6 +957,35 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     W.tmp = h->cub_tmp.p;
     W.tmp_bytes = h->cub_tmp.cap;
     W.direct_all = m2l_gemm_supported(p) ? 0 : 1;
+    // spatial blocks for the execution order: none while the multipole + local arrays fit
+    // comfortably in L2 (126 MB); else the 8 octants of the root (FMM_M2L_BLK overrides, <= 2)
+    {
+      const double bytes = 2.0 * h->ncells * NCS * sizeof(float2);
+      // (measured at C4 / C5: one level of 8 blocks cuts the M2L time by 30-40 %; finer blocks
+      // make the per-item class-matrix loads dominate)
+      int bl = bytes > 96e6 ? 1 : 0;
+      const char *eb = getenv("FMM_M2L_BLK");
+      if (eb && eb[0]) bl = std::max(0, std::min(2, atoi(eb)));
+      W.blk_level = bl;
+    }
+    CK(h->m2l_rflag.ensure(np));
+    CK(h->m2l_rid.ensure(np));
+    CK(h->m2l_rstart.ensure((size_t)np + 1));
+    CK(h->m2l_gid_of.ensure(np));
+    CK(h->m2l_items_raw.ensure((size_t)np + 1));
+    CK(h->m2l_ikeys_in.ensure((size_t)np + 1));
+    CK(h->m2l_ikeys.ensure((size_t)np + 1));
+    CK(h->m2l_iidx_in.ensure((size_t)np + 1));
+    CK(h->m2l_iidx.ensure((size_t)np + 1));
+    W.rflag = h->m2l_rflag.p;
+    W.rid = h->m2l_rid.p;
+    W.rstart = h->m2l_rstart.p;
+    W.gid_of = h->m2l_gid_of.p;
+    W.items_raw = h->m2l_items_raw.p;
+    W.ikeys_in = h->m2l_ikeys_in.p;
+    W.ikeys = h->m2l_ikeys.p;
+    W.iidx_in = h->m2l_iidx_in.p;
+    W.iidx = h->m2l_iidx.p;
     CK(h->m2l_class_rep.ensure(np));
     CK(h->m2l_ssrc.ensure(np));
     W.class_rep = h->m2l_class_rep.p;
@@ -969,6 +1000,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(cudaMemcpyAsync(h->h_small, h->m2l_counters.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int ngclass = h->h_small[3];
+    CK(m2l_sort_items(W, h->h_small[1], st));
+    h->stats.launches += 1;
+    h->stats.cub_calls += 1;
     // class GEMMs on the tensor cores (tcgen05, 3xTF32) unless disabled / unsupported
     if (use_tc) {
       CK(h->m2l_Ttc.ensure((size_t)std::max(1, ngclass) * m2l_tc_T_words(p)));
@@ -1230,6 +1264,9 @@ int fmm_destroy(fmm_t h) {
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
+  h->m2l_items_raw.release(); h->m2l_rflag.release(); h->m2l_rid.release(); h->m2l_rstart.release();
+  h->m2l_gid_of.release(); h->m2l_ikeys_in.release(); h->m2l_ikeys.release();
+  h->m2l_iidx_in.release(); h->m2l_iidx.release();
   h->sh_keys_in.release(); h->sh_keys.release(); h->sh_vals_in.release(); h->sh_cells.release();
   h->sh_src.release(); h->sh_T.release(); h->sh_items.release(); h->sh_counters.release();
   h->m2l_Y.release(); h->sh_Y.release(); h->cub_tmp_aux.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_stgt.release(); h->m2l_T.release();

@@ -101,12 +101,18 @@ struct M2LWork {
   void *tmp;
   size_t tmp_bytes;
   int direct_all;           // 1: every pair on the direct path (p > 12)
+  // block-major execution order (m2l_sort_items): runs of a class split at target blocks
+  int blk_level;            // Morton level of the spatial blocks (0: one block)
+  int *rflag, *rid, *rstart, *gid_of;
+  int4 *items_raw;          // items as emitted (unordered); `items` = block-major order
+  unsigned *ikeys_in, *ikeys, *iidx_in, *iidx;
 };
 size_t m2l_gemm_smem(int p);
 bool m2l_gemm_supported(int p);
 int m2l_y_stride(int p);
 size_t m2l_temp_bytes(int npairs);
 cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st);
+cudaError_t m2l_sort_items(const M2LWork &W, int nitems, cudaStream_t st);
 size_t m2l_T_floats(int p);
 cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st);
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,

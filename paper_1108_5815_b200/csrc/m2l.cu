@@ -116,8 +116,9 @@ __global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
 // M2L_KEY_OWN and form classes of their own (evaluated by the direct per-pair path).
 #define M2L_KEY_BITS 24
 #define M2L_KEY_OWN 0xFFFFFFu
+__device__ __forceinline__ unsigned cell_block(int4 g, int bl);
 __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
-                          const unsigned *__restrict__ src, CellsView C,
+                          const unsigned *__restrict__ src, CellsView C, int bl,
                           unsigned *__restrict__ keys, unsigned *__restrict__ idx) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
     const unsigned s = src[e];
@@ -129,21 +130,49 @@ __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
     if (abs(dx) < 63 && abs(dy) < 63 && abs(dz) < 63 && dl >= -4 && dl <= 3)  // never all ones
       key = ((unsigned)(dl + 4) << 21) | ((unsigned)(dx + 64) << 14) | ((unsigned)(dy + 64) << 7) |
             (unsigned)(dz + 64);
-    keys[e] = key;
+    // below the class: the spatial block of the target, so that each class is ordered by block
+    // and a run (class, block) is contiguous whatever the target levels
+    keys[e] = (key << (3 * bl)) | cell_block(gt, bl);
     idx[e] = (unsigned)e;
   }
 }
 
+// Spatial block (Morton index at level bl) of a cell, from its doubled-grid centre. Work items are
+// executed block-major (m2l_sort_items), so that at large N the multipole rows of one block's
+// neighbourhood and the local rows of its targets stay in L2 while all classes touch them; in
+// class-major order every class would stream the whole M and L arrays through L2.
+__device__ __forceinline__ unsigned cell_block(int4 g, int bl) {
+  if (bl <= 0) return 0u;
+  const int sh = FMM_LEVELS + 1 - bl;
+  const unsigned bx = (unsigned)g.x >> sh, by = (unsigned)g.y >> sh, bz = (unsigned)g.z >> sh;
+  unsigned k = 0;
+  for (int b = 0; b < bl; ++b)
+    k |= (((bx >> b) & 1u) << (3 * b + 2)) | (((by >> b) & 1u) << (3 * b + 1)) | (((bz >> b) & 1u) << (3 * b));
+  return k;
+}
+
+// flag = first pair of a class; rflag = first pair of a run (a class's pairs, in target order,
+// split where the target's spatial block changes)
 __global__ void k_m2l_class_flags(int npairs, const unsigned *__restrict__ skeys,
                                   const unsigned *__restrict__ sidx,
                                   const unsigned *__restrict__ src, int *__restrict__ flag,
                                   unsigned *__restrict__ ssrc, const int *__restrict__ pair_t,
-                                  unsigned *__restrict__ stgt) {
+                                  unsigned *__restrict__ stgt, int bl, int *__restrict__ rflag) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
-    const unsigned k = skeys[i];
-    flag[i] = (i == 0 || k != skeys[i - 1] || k == M2L_KEY_OWN) ? 1 : 0;
+    const unsigned k = skeys[i], cls = k >> (3 * bl);
+    const int f = (i == 0 || cls != (skeys[i - 1] >> (3 * bl)) || cls == M2L_KEY_OWN) ? 1 : 0;
+    flag[i] = f;
     ssrc[i] = src[sidx[i]];  // source cell in class-sorted order (one coalesced load later)
     if (stgt) stgt[i] = (unsigned)pair_t[sidx[i]];
+    rflag[i] = f || k != skeys[i - 1];
+  }
+}
+
+__global__ void k_m2l_run_start(int npairs, const int *__restrict__ rflag,
+                                const int *__restrict__ rid, int *__restrict__ rstart) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    if (rflag[i]) rstart[rid[i]] = i;
+    if (i == npairs - 1) rstart[rid[i] + rflag[i]] = npairs;
   }
 }
 
@@ -160,28 +189,58 @@ __global__ void k_m2l_class_start(int npairs, const int *__restrict__ flag,
   }
 }
 
-// counters: [0] classes, [1] GEMM work items, [2] pairs on the direct path, [3] GEMM classes
-__global__ void k_m2l_items(int npairs, int direct_all, const int *__restrict__ flag,
-                            const int *__restrict__ cid, const int *__restrict__ cstart,
-                            const unsigned *__restrict__ sidx, int4 *__restrict__ items,
-                            unsigned *__restrict__ small, unsigned *__restrict__ class_rep,
-                            int *__restrict__ counters) {
+// counters: [0] classes, [1] GEMM work items, [2] pairs on the direct path, [3] GEMM classes.
+// Per class (the GEMM / direct decision is taken on the class's total pair count): a GEMM class
+// gets its T index gid, a rare class sends all its pairs to the direct path.
+__global__ void k_m2l_class_gid(int npairs, int direct_all, const int *__restrict__ flag,
+                                const int *__restrict__ cid, const int *__restrict__ cstart,
+                                const unsigned *__restrict__ sidx, int *__restrict__ gid_of,
+                                unsigned *__restrict__ small, unsigned *__restrict__ class_rep,
+                                int *__restrict__ counters) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
     if (!flag[i]) continue;
     const int c = cid[i];
     const int n = cstart[c + 1] - i;
     if (!direct_all && n >= M2L_SMALL) {
-      const int ni = (n + M2L_ITEM - 1) / M2L_ITEM;
-      const int base = atomicAdd(&counters[1], ni);
       const int gid = atomicAdd(&counters[3], 1);
       class_rep[gid] = sidx[i];
-      for (int a = 0; a < ni; ++a)
-        items[base + a] = make_int4(i + a * M2L_ITEM, min(M2L_ITEM, n - a * M2L_ITEM), (int)sidx[i], gid);
+      gid_of[c] = gid;
     } else {
+      gid_of[c] = -1;
       const int base = atomicAdd(&counters[2], n);
       for (int b = 0; b < n; ++b) small[base + b] = sidx[i + b];
     }
   }
+}
+// Per run of a GEMM class: work items of <= M2L_ITEM pairs, each with its execution-order key
+// (spatial block of the run's targets, class)
+__global__ void k_m2l_run_items(int npairs, const int *__restrict__ flag, const int *__restrict__ rflag,
+                                const int *__restrict__ rid, const int *__restrict__ rstart,
+                                const int *__restrict__ cid, const int *__restrict__ gid_of,
+                                const unsigned *__restrict__ sidx, const unsigned *__restrict__ skeys,
+                                int bl, int4 *__restrict__ items,
+                                unsigned *__restrict__ ikeys, unsigned *__restrict__ iidx,
+                                int *__restrict__ counters) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    if (!rflag[i]) continue;
+    // cid is an exclusive scan of the class flags: the class of position i is cid + flag - 1
+    const int gid = gid_of[cid[i] + flag[i] - 1];
+    if (gid < 0) continue;
+    const int n = rstart[rid[i] + 1] - i;
+    const int ni = (n + M2L_ITEM - 1) / M2L_ITEM;
+    const int base = atomicAdd(&counters[1], ni);
+    const unsigned key = ((skeys[i] & ((1u << (3 * bl)) - 1u)) << 20) | (unsigned)gid;
+    for (int a = 0; a < ni; ++a) {
+      items[base + a] = make_int4(i + a * M2L_ITEM, min(M2L_ITEM, n - a * M2L_ITEM), (int)sidx[i], gid);
+      ikeys[base + a] = key;
+      iidx[base + a] = (unsigned)(base + a);
+    }
+  }
+}
+__global__ void k_m2l_gather_items(int n, const unsigned *__restrict__ order,
+                                   const int4 *__restrict__ in, int4 *__restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = in[order[i]];
 }
 
 // ---- class translation matrices ---------------------------------------------------------------
@@ -558,36 +617,63 @@ int m2l_y_stride(int p) { return (2 * nc_of(p) + 3) & ~3; }
 cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st) {
   k_m2l_pair_targets<<<148 * 8, 128, 0, st>>>(ncells, W.off, W.cnt, W.pair_t);
   const int b = (npairs + 255) / 256 < 148 * 16 ? (npairs + 255) / 256 : 148 * 16;
-  k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.keys_in, W.idx_in);
+  k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.blk_level, W.keys_in,
+                                            W.idx_in);
+  const int kbits = M2L_KEY_BITS + 3 * W.blk_level;
   size_t bytes = 0;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, W.idx_in,
-                                                  W.sidx, npairs, 0, M2L_KEY_BITS, st);
+                                                  W.sidx, npairs, 0, kbits, st);
   if (e) return e;
   if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
   e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
-                                      M2L_KEY_BITS, st);
+                                      kbits, st);
   if (e) return e;
   k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.src, W.flag, W.ssrc,
-                                                    W.pair_t, W.stgt);
+                                                    W.pair_t, W.stgt, W.blk_level, W.rflag);
   bytes = 0;
   e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, W.flag, W.cid, npairs, st);
   if (e) return e;
   if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
   e = cub::DeviceScan::ExclusiveSum(W.tmp, bytes, W.flag, W.cid, npairs, st);
   if (e) return e;
+  e = cub::DeviceScan::ExclusiveSum(W.tmp, bytes, W.rflag, W.rid, npairs, st);
+  if (e) return e;
   cudaMemsetAsync(W.counters, 0, 4 * sizeof(int), st);
   k_m2l_class_start<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.flag, W.cid, W.cstart, W.counters);
-  k_m2l_items<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.direct_all, W.flag, W.cid, W.cstart, W.sidx,
-                                             W.items, W.small, W.class_rep, W.counters);
+  k_m2l_run_start<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.rflag, W.rid, W.rstart);
+  k_m2l_class_gid<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.direct_all, W.flag, W.cid, W.cstart,
+                                                 W.sidx, W.gid_of, W.small, W.class_rep, W.counters);
+  k_m2l_run_items<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.flag, W.rflag, W.rid, W.rstart, W.cid, W.gid_of,
+                                                 W.sidx, W.keys, W.blk_level, W.items_raw,
+                                                 W.ikeys_in, W.iidx_in, W.counters);
+  return cudaGetLastError();
+}
+
+// block-major execution order of the nitems work items (counters[1], read back by the host)
+cudaError_t m2l_sort_items(const M2LWork &W, int nitems, cudaStream_t st) {
+  if (nitems <= 0) return cudaSuccess;
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.ikeys_in, W.ikeys, W.iidx_in,
+                                                  W.iidx, nitems, 0, 32, st);
+  if (e) return e;
+  if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
+  e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.ikeys_in, W.ikeys, W.iidx_in, W.iidx, nitems,
+                                      0, 32, st);
+  if (e) return e;
+  const int b = (nitems + 255) / 256 < 148 * 8 ? (nitems + 255) / 256 : 148 * 8;
+  k_m2l_gather_items<<<b, 256, 0, st>>>(nitems, W.iidx, W.items_raw, W.items);
   return cudaGetLastError();
 }
 
 size_t m2l_temp_bytes(int npairs) {
   size_t a = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned *)nullptr, (unsigned *)nullptr,
-                                  (unsigned *)nullptr, (unsigned *)nullptr, npairs, 0, M2L_KEY_BITS);
+                                  (unsigned *)nullptr, (unsigned *)nullptr, npairs, 0, 32);
   cub::DeviceScan::ExclusiveSum(nullptr, b, (int *)nullptr, (int *)nullptr, npairs);
-  return a > b ? a : b;
+  size_t c = 0;  // the work-item sort (at most npairs items, 32-bit keys)
+  cub::DeviceRadixSort::SortPairs(nullptr, c, (unsigned *)nullptr, (unsigned *)nullptr,
+                                  (unsigned *)nullptr, (unsigned *)nullptr, npairs, 0, 32);
+  return std::max(a, std::max(b, c));
 }
 
 cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st) {

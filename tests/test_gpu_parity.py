@@ -212,7 +212,7 @@ def test_virtual_rank_partition_union(handles, mode):
     assert rel_l2(phi_u, full_phi) < 1e-6 and rel_l2(grad_u, full_grad) < 1e-6
 
 
-@pytest.mark.parametrize("cfg_name", ["C2", "C3"])
+@pytest.mark.parametrize("cfg_name", ["C2", "C3", "C4"])
 def test_full_size_sampled_parity(O, cfg_name):
     """BASELINE configs at full size in the bench's launch configuration (auto-tuned hybrid):
     sampled targets against the oracle's sampled-target mode (exact for those targets, same tree,
@@ -233,3 +233,25 @@ def test_full_size_sampled_parity(O, cfg_name):
     assert O.rel_l2(phi[s], ref.phi) < 1e-5 and O.rel_l2(grad[s], ref.grad) < 1e-5
     d = O.direct(xyz, q, s)
     assert O.rel_l2(phi[s], d[0]) < 1e-4 and O.rel_l2(grad[s], d[1]) < 1e-3
+
+
+@pytest.mark.parametrize("blk", [1, 2])
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_m2l_block_order(O, handles, monkeypatch, blk, deterministic):
+    # the block-major M2L execution order (m2l.cu m2l_sort_items; chosen automatically only at
+    # large N) forced on a moderate adaptive case: same lists, same fields as the oracle
+    xyz, q = make_particles(60000, "plummer", 41)
+    f = handles(8, 0.45, 32, "hybrid")
+    f.set_deterministic(deterministic)
+    try:
+        ref_phi, ref_grad = run(f, xyz, q)
+        monkeypatch.setenv("FMM_M2L_BLK", str(blk))
+        phi, grad = run(f, xyz, q)
+        lists = O.canonical_tasks(f.export_lists())
+    finally:
+        monkeypatch.delenv("FMM_M2L_BLK", raising=False)
+        f.set_deterministic(True)
+    assert O.rel_l2(phi, ref_phi) < 1e-6 and O.rel_l2(grad, ref_grad) < 1e-6
+    ref = O.fmm(xyz, q, 8, 0.45, 32, O.HYBRID, cost=COST)
+    assert np.array_equal(lists, O.canonical_tasks(ref.tasks))
+    assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
