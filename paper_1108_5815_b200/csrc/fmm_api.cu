@@ -61,7 +61,7 @@ struct DBuf {
   }
 };
 
-enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L_PREP, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_N };
+enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L_PREP, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_P2P0, EV_N };
 
 }  // namespace
 
@@ -72,7 +72,10 @@ struct fmm_ctx {
   cudaStream_t own_stream = nullptr, stream = nullptr;
   // the upward sweep runs on `aux`, concurrently with the traversal and the M2L class sort
   cudaStream_t aux = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_up = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_up = nullptr, ev_trav = nullptr, ev_near = nullptr;
+  // P2P / M2P run on `aux` after the traversal, overlapping the M2L class preparation and GEMM
+  // on the main stream (off while the kernel pre-calculation times the kernels in isolation)
+  bool overlap = true;
   DBuf<char> cub_tmp_aux;
   DBuf<float> sh_Y;  // per-cell slots of the tensor-core M2M / L2L
   fmm_cost_t cost{};
@@ -915,6 +918,29 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     if (int rc = dist_let(h)) return rc;
   }
   record(h, EV_TRAV);
+  // a12 P2P (writes acc), a11 M2P (adds): on the aux stream (after the upward sweep there) when
+  // overlapping, so that they run while the main stream sorts the M2L pairs into classes
+  const int *tl = (h->nparts > 1 || h->comm) ? h->tleaves.p : h->leaves.p;
+  const int ntl = h->tleaves_n;
+  auto near_field = [&](cudaStream_t ns) -> int {
+    record_on(h, EV_P2P0, ns);
+    launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p, h->d_small + 12, ns);
+    CKL();
+    record_on(h, EV_P2P, ns);
+    if (h->ntask[FMM_KIND_M2P] > 0) {
+      CK(cudaStreamWaitEvent(ns, h->ev_up, 0));  // M2P reads the multipoles
+      launch_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, h->d_small + 13, ns);
+      CKL();
+    }
+    record_on(h, EV_M2P, ns);
+    return FMM_OK;
+  };
+  if (h->overlap) {
+    CK(cudaEventRecord(h->ev_trav, st));
+    CK(cudaStreamWaitEvent(h->aux, h->ev_trav, 0));
+    if (int rc = near_field(h->aux)) return rc;
+    CK(cudaEventRecord(h->ev_near, h->aux));
+  }
   record(h, EV_M2L_PREP);  // re-recorded after the class sort when there are M2L pairs
   // a10 M2L (writes every cell's local expansion, zero where no M2L)
   const bool far_local = h->ntask[FMM_KIND_M2L] > 0;
@@ -1026,18 +1052,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   }
   CK(cudaStreamWaitEvent(st, h->ev_up, 0));  // (no M2L pairs: join here)
   record(h, EV_M2L);
-  // a12 P2P (writes acc), a11 M2P (adds)
-  const int *tl = (h->nparts > 1 || h->comm) ? h->tleaves.p : h->leaves.p;
-  const int ntl = h->tleaves_n;
-  launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p,
-                    h->d_small + 12, st);
-  CKL();
-  record(h, EV_P2P);
-  if (h->ntask[FMM_KIND_M2P] > 0) {
-    launch_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, h->d_small + 13, st);
-    CKL();
+  if (!h->overlap) {
+    if (int rc = near_field(st)) return rc;
   }
-  record(h, EV_M2P);
   // a13 L2L top-down, a14/a15 L2P + combine + un-permute
   if (far_local) {
     for (int level = 1; level <= h->depth; ++level) {
@@ -1059,6 +1076,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     ophi = h->rphi.p;
     ograd = h->rgrad.p;
   }
+  if (h->overlap) CK(cudaStreamWaitEvent(st, h->ev_near, 0));  // join: acc is complete
   launch_l2p(p, tl, ntl, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, ophi,
              ograd, far_local ? 1 : 0, st);
   CKL();
@@ -1111,6 +1129,7 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     record(h, EV_TRAV);
     record(h, EV_M2L_PREP);
     record(h, EV_M2L);
+    record(h, EV_P2P0);
     launch_p2p_direct(n, h->pos.p, phi, grad, st);
     CKL();
     record(h, EV_P2P);
@@ -1134,23 +1153,21 @@ static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n
 }
 
 static void read_phase_times(fmm_ctx *h) {
-  {
-    float ms[EV_N];
-    for (int e = 1; e < EV_N; ++e) cudaEventElapsedTime(&ms[e], h->ev[e - 1], h->ev[e]);
-    cudaEventElapsedTime(&ms[0], h->ev[EV_START], h->ev[EV_DOWN]);
-    h->stats.ms_total = ms[0];
-    h->stats.ms_tree = ms[EV_TREE];
-    // the upward sweep (aux stream) overlaps the traversal: both are measured from EV_TREE
-    float up = 0.f, trav = 0.f;
-    cudaEventElapsedTime(&up, h->ev[EV_TREE], h->ev[EV_UP]);
-    cudaEventElapsedTime(&trav, h->ev[EV_TREE], h->ev[EV_TRAV]);
-    h->stats.ms_upward = up;
-    h->stats.ms_traverse = trav + ms[EV_M2L_PREP];  // class sort counted as bookkeeping
-    h->stats.ms_m2l = ms[EV_M2L];
-    h->stats.ms_p2p = ms[EV_P2P];
-    h->stats.ms_m2p = ms[EV_M2P];
-    h->stats.ms_downward = ms[EV_DOWN];
-  }
+  auto el = [&](int a, int b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev[a], h->ev[b]);
+    return (double)ms;
+  };
+  h->stats.ms_total = el(EV_START, EV_DOWN);
+  h->stats.ms_tree = el(EV_START, EV_TREE);
+  // the upward sweep (aux stream) overlaps the traversal: both are measured from EV_TREE
+  h->stats.ms_upward = el(EV_TREE, EV_UP);
+  h->stats.ms_traverse = el(EV_TREE, EV_TRAV) + el(EV_TRAV, EV_M2L_PREP);  // + the class sort
+  h->stats.ms_m2l = el(EV_M2L_PREP, EV_M2L);
+  // P2P / M2P: their own events (on aux when overlapping the M2L, which the phases then do)
+  h->stats.ms_p2p = el(EV_P2P0, EV_P2P);
+  h->stats.ms_m2p = el(EV_P2P, EV_M2P);
+  h->stats.ms_downward = (h->overlap && h->mode != FMM_DIRECT) ? el(EV_M2L, EV_DOWN) : el(EV_M2P, EV_DOWN);
 }
 
 // ---- a6: kernel pre-calculation ------------------------------------
@@ -1168,7 +1185,8 @@ static int tune_impl(fmm_ctx *h) {
   launch_fill_random(q, n, 777u, 1.0f / n, 1.0f / n, h->stream);
   CKL();
   const int saved_mode = h->mode;
-  const bool saved_timing = h->timing;
+  const bool saved_timing = h->timing, saved_overlap = h->overlap;
+  h->overlap = false;  // each kernel timed alone
   h->timing = true;
   double t_pp[3], t_ml[3], t_mp[3];
   int rc = FMM_OK;
@@ -1188,6 +1206,7 @@ static int tune_impl(fmm_ctx *h) {
   }
   h->mode = saved_mode;
   h->timing = saved_timing;
+  h->overlap = saved_overlap;
   cudaFree(d);
   if (rc) return rc;
   auto med3 = [](double *a) { std::sort(a, a + 3); return a[1]; };
@@ -1227,7 +1246,9 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
     h->stream = h->own_stream;
     if ((e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming)) != cudaSuccess) {
+        (e = cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&h->ev_trav, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&h->ev_near, cudaEventDisableTiming)) != cudaSuccess) {
       rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e));
       break;
     }
@@ -1240,6 +1261,8 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
       rc = fail(h, FMM_E_OOM, "small device allocations failed");
       break;
     }
+    const char *no = getenv("FMM_NO_OVERLAP");
+    h->overlap = !(no && no[0] && no[0] != '0');
     const char *nt = getenv("FMM_NO_TUNE");
     if (!(nt && nt[0] && nt[0] != '0')) rc = tune_impl(h);
   } while (0);
@@ -1303,6 +1326,8 @@ int fmm_destroy(fmm_t h) {
   if (h->aux) cudaStreamDestroy(h->aux);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_up) cudaEventDestroy(h->ev_up);
+  if (h->ev_trav) cudaEventDestroy(h->ev_trav);
+  if (h->ev_near) cudaEventDestroy(h->ev_near);
   delete h;
   return FMM_OK;
 }

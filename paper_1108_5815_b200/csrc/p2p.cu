@@ -144,77 +144,39 @@ __device__ __forceinline__ void p2p_raw(const float4 sv, const f2x tx, const f2x
   gz = fma2(dz, qr3, gz);
 }
 
-// NP target pairs per lane (2 NP targets): the source is unpacked once and feeds NP independent
-// packed dependency chains (more ILP per source, one LDS.128 per 2 NP pairs)
-template <bool MASK, int NP>
-__device__ __forceinline__ void p2p_rawN(const float4 sv, const f2x *tx, const f2x *ty,
-                                         const f2x *tz, f2x *ph, f2x *gx, f2x *gy, f2x *gz) {
-  const f2x sx = pk(sv.x, sv.x), sy = pk(sv.y, sv.y), sz = pk(sv.z, sv.z), sq = pk(sv.w, sv.w);
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    const f2x dx = add2(sx, tx[k]);
-    const f2x dy = add2(sy, ty[k]);
-    const f2x dz = add2(sz, tz[k]);
-    f2x r2 = mul2(dx, dx);
-    r2 = fma2(dy, dy, r2);
-    r2 = fma2(dz, dz, r2);
-    const float2 r2f = upk(r2);
-    float rx = rsqrt_approx(r2f.x), ry = rsqrt_approx(r2f.y);
-    if (MASK) {
-      rx = r2f.x > 0.f ? rx : 0.f;
-      ry = r2f.y > 0.f ? ry : 0.f;
-    }
-    const f2x ri = pk(rx, ry);
-    const f2x qr = mul2(sq, ri);
-    ph[k] = add2(ph[k], qr);
-    const f2x qr3 = mul2(qr, mul2(ri, ri));
-    gx[k] = fma2(dx, qr3, gx[k]);
-    gy[k] = fma2(dy, qr3, gy[k]);
-    gz[k] = fma2(dz, qr3, gz[k]);
-  }
-}
-
-// S (source slices) is a compile-time constant so the LDS.128 of an unrolled step use immediate
-// offsets (no IMAD address arithmetic on the FMA pipe). acc[4 k + c]: pair k, component c.
-template <bool MASK, int S, int NP>
+// S (source slices) is a compile-time constant so the four LDS.128 of an unrolled step use
+// immediate offsets (no IMAD address arithmetic on the FMA pipe)
+template <bool MASK, int S>
 __device__ __forceinline__ void p2p_tile_rawS(const float4 *__restrict__ sp, int ns, int h,
-                                              const f2x *tx, const f2x *ty, const f2x *tz,
-                                              f2x *acc) {
-  constexpr int U = NP == 1 ? 4 : 2;  // sources per unrolled step
-  f2x ph[NP], gx[NP], gy[NP], gz[NP];
-#pragma unroll
-  for (int k = 0; k < NP; ++k) ph[k] = gx[k] = gy[k] = gz[k] = 0ull;
+                                              f2x tx, f2x ty, f2x tz, f2x acc[4]) {
+  f2x ph = 0ull, gx = 0ull, gy = 0ull, gz = 0ull;
   const float4 *q = sp + h;
-  const float4 *endU = sp + ns - (U - 1) * S;  // q + (U-1) S < sp + ns
-  for (; q < endU; q += U * S) {
-    float4 sv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) sv[u] = q[u * S];
-#pragma unroll
-    for (int u = 0; u < U; ++u) p2p_rawN<MASK, NP>(sv[u], tx, ty, tz, ph, gx, gy, gz);
+  const float4 *end4 = sp + ns - 3 * S;  // q + 3S < sp + ns
+  for (; q < end4; q += 4 * S) {
+    const float4 s0 = q[0], s1 = q[S], s2 = q[2 * S], s3 = q[3 * S];
+    p2p_raw<MASK>(s0, tx, ty, tz, ph, gx, gy, gz);
+    p2p_raw<MASK>(s1, tx, ty, tz, ph, gx, gy, gz);
+    p2p_raw<MASK>(s2, tx, ty, tz, ph, gx, gy, gz);
+    p2p_raw<MASK>(s3, tx, ty, tz, ph, gx, gy, gz);
   }
-  for (; q < sp + ns; q += S) p2p_rawN<MASK, NP>(q[0], tx, ty, tz, ph, gx, gy, gz);
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    acc[4 * k + 0] = add2(acc[4 * k + 0], ph[k]);
-    acc[4 * k + 1] = add2(acc[4 * k + 1], gx[k]);
-    acc[4 * k + 2] = add2(acc[4 * k + 2], gy[k]);
-    acc[4 * k + 3] = add2(acc[4 * k + 3], gz[k]);
-  }
+  for (; q < sp + ns; q += S) p2p_raw<MASK>(q[0], tx, ty, tz, ph, gx, gy, gz);
+  acc[0] = add2(acc[0], ph);
+  acc[1] = add2(acc[1], gx);
+  acc[2] = add2(acc[2], gy);
+  acc[3] = add2(acc[3], gz);
 }
-template <bool MASK, int NP>
+template <bool MASK>
 __device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int ns, int h, int S,
-                                             const f2x *tx, const f2x *ty, const f2x *tz,
-                                             f2x *acc) {
+                                             f2x tx, f2x ty, f2x tz, f2x acc[4]) {
   switch (S) {
-    case 1: p2p_tile_rawS<MASK, 1, NP>(sp, ns, h, tx, ty, tz, acc); break;
-    case 2: p2p_tile_rawS<MASK, 2, NP>(sp, ns, h, tx, ty, tz, acc); break;
-    case 3: p2p_tile_rawS<MASK, 3, NP>(sp, ns, h, tx, ty, tz, acc); break;
-    case 4: p2p_tile_rawS<MASK, 4, NP>(sp, ns, h, tx, ty, tz, acc); break;
-    case 5: p2p_tile_rawS<MASK, 5, NP>(sp, ns, h, tx, ty, tz, acc); break;
-    case 6: p2p_tile_rawS<MASK, 6, NP>(sp, ns, h, tx, ty, tz, acc); break;
-    case 7: p2p_tile_rawS<MASK, 7, NP>(sp, ns, h, tx, ty, tz, acc); break;
-    default: p2p_tile_rawS<MASK, 8, NP>(sp, ns, h, tx, ty, tz, acc); break;
+    case 1: p2p_tile_rawS<MASK, 1>(sp, ns, h, tx, ty, tz, acc); break;
+    case 2: p2p_tile_rawS<MASK, 2>(sp, ns, h, tx, ty, tz, acc); break;
+    case 3: p2p_tile_rawS<MASK, 3>(sp, ns, h, tx, ty, tz, acc); break;
+    case 4: p2p_tile_rawS<MASK, 4>(sp, ns, h, tx, ty, tz, acc); break;
+    case 5: p2p_tile_rawS<MASK, 5>(sp, ns, h, tx, ty, tz, acc); break;
+    case 6: p2p_tile_rawS<MASK, 6>(sp, ns, h, tx, ty, tz, acc); break;
+    case 7: p2p_tile_rawS<MASK, 7>(sp, ns, h, tx, ty, tz, acc); break;
+    default: p2p_tile_rawS<MASK, 8>(sp, ns, h, tx, ty, tz, acc); break;
   }
 }
 
@@ -228,10 +190,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-#ifndef P2P_NP
-#define P2P_NP 1  // target PAIRS per lane (2 NP targets per lane)
-#endif
-
 #ifndef P2P_RANGES
 #define P2P_RANGES 256  // per-warp list of source particle ranges (processed in batches)
 #endif
@@ -243,9 +201,10 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
                                                                float4 *__restrict__ acc_out,
                                                                float m1, int *next_leaf) {
   __shared__ __align__(16) float4 sh[P2P_WARPS][2][P2P_TILE];
+  __shared__ __align__(16) float4 shq[P2P_WARPS][64];  // 2 float4 per lane (target pairs)
   __shared__ int2 shr[P2P_WARPS][P2P_RANGES];
-  constexpr int NP = P2P_NP, TPL = 2 * NP;  // target pairs / targets per lane
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float4 *tq = shq[wib];
   int2 *rng = shr[wib];
   for (;;) {
     int li = 0;
@@ -257,34 +216,33 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
     // ancestors of the leaf (each may carry a P2P list)
     int anc[FMM_LEVELS + 1], na = 0;
     for (int a = leaf; a >= 0 && na <= FMM_LEVELS; a = C.parent[a]) anc[na++] = a;
-    for (int c0 = 0; c0 < tn; c0 += 32 * TPL) {
-      // G = ceil(nt / TPL) target groups x S = min(8, 32 / G) source slices (lanes with h >= S
+    for (int c0 = 0; c0 < tn; c0 += 32) {
+      // G = ceil(nt / 2) target pairs x S = min(8, 32 / G) source slices (lanes with h >= S
       // idle): no padding of the target count to a power of two (a 17-target leaf keeps 27 of
       // 32 lanes busy instead of 17 of 32 target slots)
-      const int nt = min(32 * TPL, tn - c0);
-      const int G = (nt + TPL - 1) / TPL;
+      const int nt = min(32, tn - c0);
+      const int G = (nt + 1) >> 1;
       const int S = min(8, 32 / G);
       const int grp = lane % G, h = lane / G;
       const bool active = h < S;
-      const int i0 = c0 + TPL * grp;
-      f2x tx[NP], ty[NP], tz[NP], acc[4 * NP];
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        const int ia = i0 + 2 * k, ib = ia + 1;
-        const float4 t0 = ia < tn ? pos[tb + ia] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 t1 = ib < tn ? pos[tb + ib] : t0;
-        tx[k] = pk(m1 * t0.x, m1 * t1.x);
-        ty[k] = pk(m1 * t0.y, m1 * t1.y);
-        tz[k] = pk(m1 * t0.z, m1 * t1.z);
-        acc[4 * k] = acc[4 * k + 1] = acc[4 * k + 2] = acc[4 * k + 3] = 0ull;
-      }
+      const int i0 = c0 + 2 * grp, i1 = i0 + 1;
+      const float4 t0 = i0 < tn ? pos[tb + i0] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 t1 = i1 < tn ? pos[tb + i1] : t0;
+      __syncwarp();
+      tq[2 * lane] = make_float4(m1 * t0.x, m1 * t1.x, m1 * t0.y, m1 * t1.y);
+      tq[2 * lane + 1] = make_float4(m1 * t0.z, m1 * t1.z, 0.f, 0.f);
+      __syncwarp();
+      const ulonglong2 ta = *reinterpret_cast<const ulonglong2 *>(&tq[2 * lane]);
+      const ulonglong2 tb2 = *reinterpret_cast<const ulonglong2 *>(&tq[2 * lane + 1]);
+      const f2x tx = ta.x, ty = ta.y, tz = tb2.x;
+      f2x acc[4] = {0ull, 0ull, 0ull, 0ull};
       // (1) the leaf itself, masked (r = 0 pairs)
       for (int j0 = 0; j0 < tn; j0 += P2P_TILE) {
         const int n = min(P2P_TILE, tn - j0);
         __syncwarp();
         for (int j = lane; j < n; j += 32) sh[wib][0][j] = pos[tb + j0 + j];
         __syncwarp();
-        p2p_tile_raw<true, NP>(sh[wib][0], active ? n : 0, h, S, tx, ty, tz, acc);
+        p2p_tile_raw<true>(sh[wib][0], active ? n : 0, h, S, tx, ty, tz, acc);
       }
       // (2) all other source cells of the P2P lists of the leaf and its ancestors, as particle
       // ranges collected into shared memory (batches of P2P_RANGES), streamed by cp.async into a
@@ -335,7 +293,7 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
           const int nxt = issue(buf ^ 1);
           cp_async_wait1();  // tile `buf` has landed
           __syncwarp();
-          p2p_tile_raw<false, NP>(sh[wib][buf], active ? cur : 0, h, S, tx, ty, tz, acc);
+          p2p_tile_raw<false>(sh[wib][buf], active ? cur : 0, h, S, tx, ty, tz, acc);
           __syncwarp();
           buf ^= 1;
           cur = nxt;
@@ -344,28 +302,23 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
         __syncwarp();
       }
       // reduce the S source slices (lanes grp, grp + G, ...) in slice order
-      float2 r[4 * NP];
+      float2 r[4];
 #pragma unroll
-      for (int k = 0; k < 4 * NP; ++k) r[k] = upk(acc[k]);
-      float2 tot[4 * NP];
-#pragma unroll
-      for (int k = 0; k < 4 * NP; ++k) tot[k] = r[k];
+      for (int k = 0; k < 4; ++k) r[k] = upk(acc[k]);
+      float2 tot[4] = {r[0], r[1], r[2], r[3]};
       for (int sl = 1; sl < S; ++sl) {  // slice order: deterministic
         const int from = grp + sl * G;
 #pragma unroll
-        for (int k = 0; k < 4 * NP; ++k) {
+        for (int k = 0; k < 4; ++k) {
           tot[k].x += __shfl_sync(0xffffffffu, r[k].x, from);
           tot[k].y += __shfl_sync(0xffffffffu, r[k].y, from);
         }
       }
-      if (h == 0) {
 #pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const int ia = i0 + 2 * k, ib = ia + 1;
-          const float2 *t = tot + 4 * k;
-          if (ia < tn) acc_out[tb + ia] = make_float4(t[0].x, t[1].x, t[2].x, t[3].x);
-          if (ib < tn) acc_out[tb + ib] = make_float4(t[0].y, t[1].y, t[2].y, t[3].y);
-        }
+      for (int k = 0; k < 4; ++k) r[k] = tot[k];
+      if (h == 0) {
+        if (i0 < tn) acc_out[tb + i0] = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
+        if (i1 < tn) acc_out[tb + i1] = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
       }
       __syncwarp();
     }
