@@ -213,6 +213,7 @@ def run_ours(args):
                           "ms_upward": 0.0, "ms_traverse": 0.0, "ms_downward": 0.0}
     launches = 0
     with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/": the launch list
         for _ in range(args.steps):
             flush.fill_(1.0)
             barrier()
@@ -226,6 +227,7 @@ def run_ours(args):
             for k in phase:
                 phase[k] += s[k]
             launches += s["launches"]
+        torch.cuda.nvtx.range_pop()
         barrier()
     stats = f.stats()
     total_ms = sum(step_ms)

@@ -1,5 +1,6 @@
-"""One warm-up + one profiled fmm_evaluate (NVTX range "profiled") of a config for ncu captures;
-the cost model is measured at create like bench.py (FMM_COST=t_pp,t_mp,t_ml fixes it instead)."""
+"""One warm-up + one profiled fmm_evaluate (NVTX range "profiled") of a config for ncu captures,
+in bench.py's launch configuration: cost model measured at create (FMM_COST=t_pp,t_mp,t_ml fixes
+it instead) and the M2L summed by L2 vector reductions (FMM_DET=1: the deterministic order)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -12,6 +13,7 @@ X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
 f = FMM(p=cfg["p"], theta=cfg["theta"], ncrit=cfg["ncrit"], mode=mode, tune="FMM_COST" not in os.environ)
 if "FMM_COST" in os.environ:  # a fixed cost model (else the one measured at create, as bench.py)
     f.set_cost_model(*map(float, os.environ["FMM_COST"].split(",")))
+f.set_deterministic(os.environ.get("FMM_DET", "0") == "1")
 f.evaluate(X, Q); torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("profiled")
 f.evaluate(X, Q); torch.cuda.synchronize()
