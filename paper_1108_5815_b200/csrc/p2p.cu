@@ -20,6 +20,9 @@
 #define P2P_TILE 256  // 16 KiB per warp double buffer; 256 beats 128 by ~2% at C2
 #endif
 #define P2P_WARPS 4
+#ifndef P2P_SMAX
+#define P2P_SMAX 32  // most source slices per warp (32 / G for G target pairs)
+#endif
 #ifndef P2P_MINB
 #define P2P_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
@@ -151,7 +154,9 @@ __device__ __forceinline__ void p2p_tile_rawS(const float4 *__restrict__ sp, int
                                               f2x tx, f2x ty, f2x tz, f2x acc[4]) {
   f2x ph = 0ull, gx = 0ull, gy = 0ull, gz = 0ull;
   const float4 *q = sp + h;
-  const float4 *end4 = sp + ns - 3 * S;  // q + 3S < sp + ns
+  // q + 3S < sp + ns; clamped so that the bound never lies below the buffer (as a 32-bit shared
+  // address sp + ns - 3S would wrap around when the buffer starts near address 0)
+  const float4 *end4 = ns > 3 * S ? sp + ns - 3 * S : sp;
   for (; q < end4; q += 4 * S) {
     const float4 s0 = q[0], s1 = q[S], s2 = q[2 * S], s3 = q[3 * S];
     p2p_raw<MASK>(s0, tx, ty, tz, ph, gx, gy, gz);
@@ -176,7 +181,10 @@ __device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int 
     case 5: p2p_tile_rawS<MASK, 5>(sp, ns, h, tx, ty, tz, acc); break;
     case 6: p2p_tile_rawS<MASK, 6>(sp, ns, h, tx, ty, tz, acc); break;
     case 7: p2p_tile_rawS<MASK, 7>(sp, ns, h, tx, ty, tz, acc); break;
-    default: p2p_tile_rawS<MASK, 8>(sp, ns, h, tx, ty, tz, acc); break;
+    case 8: p2p_tile_rawS<MASK, 8>(sp, ns, h, tx, ty, tz, acc); break;
+    case 10: p2p_tile_rawS<MASK, 10>(sp, ns, h, tx, ty, tz, acc); break;
+    case 16: p2p_tile_rawS<MASK, 16>(sp, ns, h, tx, ty, tz, acc); break;
+    default: p2p_tile_rawS<MASK, 32>(sp, ns, h, tx, ty, tz, acc); break;
   }
 }
 
@@ -217,12 +225,13 @@ __global__ void __launch_bounds__(P2P_WARPS * 32, P2P_MINB) k_p2p_leaves(const i
     int anc[FMM_LEVELS + 1], na = 0;
     for (int a = leaf; a >= 0 && na <= FMM_LEVELS; a = C.parent[a]) anc[na++] = a;
     for (int c0 = 0; c0 < tn; c0 += 32) {
-      // G = ceil(nt / 2) target pairs x S = min(8, 32 / G) source slices (lanes with h >= S
-      // idle): no padding of the target count to a power of two (a 17-target leaf keeps 27 of
-      // 32 lanes busy instead of 17 of 32 target slots)
+      // G = ceil(nt / 2) target pairs x S = 32 / G source slices (lanes with h >= S idle): no
+      // padding of the target count to a power of two (a 17-target leaf keeps 27 of 32 lanes
+      // busy instead of 17 of 32 target slots), and the 1-10 targets left over by a 33-42
+      // target leaf still spread the sources over all 32 lanes (S up to 32)
       const int nt = min(32, tn - c0);
       const int G = (nt + 1) >> 1;
-      const int S = min(8, 32 / G);
+      const int S = P2P_SMAX < 32 / G ? P2P_SMAX : 32 / G;
       const int grp = lane % G, h = lane / G;
       const bool active = h < S;
       const int i0 = c0 + 2 * grp, i1 = i0 + 1;
