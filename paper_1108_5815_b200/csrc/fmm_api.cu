@@ -1162,7 +1162,9 @@ static void read_phase_times(fmm_ctx *h) {
   h->stats.ms_tree = el(EV_START, EV_TREE);
   // the upward sweep (aux stream) overlaps the traversal: both are measured from EV_TREE
   h->stats.ms_upward = el(EV_TREE, EV_UP);
-  h->stats.ms_traverse = el(EV_TREE, EV_TRAV) + el(EV_TRAV, EV_M2L_PREP);  // + the class sort
+  // traversal (+ the class sort when P2P does not overlap it; overlapped, the sort's time is
+  // hidden under P2P and not attributed to any phase)
+  h->stats.ms_traverse = el(EV_TREE, EV_TRAV) + (h->overlap ? 0.0 : el(EV_TRAV, EV_M2L_PREP));
   h->stats.ms_m2l = el(EV_M2L_PREP, EV_M2L);
   // P2P / M2P: their own events (on aux when overlapping the M2L, which the phases then do)
   h->stats.ms_p2p = el(EV_P2P0, EV_P2P);

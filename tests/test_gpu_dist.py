@@ -148,3 +148,27 @@ def test_dist_repeated_and_single_rank():
     assert O.rel_l2(out[0]["phi"], ref["phi"]) < 1e-6
     out = run_group(3, xyz, q, shards(6000, 3, 1), 6, 0.5, 32, "hybrid", evals=3)
     assert out[0]["stats"]["n_global"] == 6000
+
+
+def test_dist_bench_workload_shape():
+    # bench.py at N > 1: rank r contributes one uniform instance shifted into unit cube r (one
+    # global problem, weak scaling); p = 10, theta = 0.4, ncrit = 64 as C2, at 2 x 200k here
+    R, n_local = 2, 200_000
+    parts_xyz, parts_q = [], []
+    for r in range(R):
+        x, q = make_particles(n_local, "uniform", 2 + 100 * r)
+        parts_xyz.append((x + np.array([r % 2, (r // 2) % 2, r // 4], np.float32)).astype(np.float32))
+        parts_q.append(q)
+    xyz = np.concatenate(parts_xyz)
+    q = np.concatenate(parts_q)
+    parts = [np.arange(r * n_local, (r + 1) * n_local) for r in range(R)]
+    ref = single(xyz, q, 10, 0.4, 64, "hybrid")
+    out = run_group(R, xyz, q, parts, 10, 0.4, 64, "hybrid")
+    phi = np.concatenate([o["phi"] for o in out])
+    grad = np.concatenate([o["grad"] for o in out])
+    assert O.rel_l2(phi, ref["phi"]) < 1e-6 and O.rel_l2(grad, ref["grad"]) < 1e-6
+    s = np.random.default_rng(3).choice(len(q), 512, replace=False)
+    d = O.direct(xyz, q, s)
+    assert O.rel_l2(phi[s], d[0]) < 1e-4 and O.rel_l2(grad[s], d[1]) < 1e-3
+    st = [o["stats"] for o in out]
+    assert all(x["let_cells"] > 0 and x["let_particles"] > 0 for x in st)
