@@ -72,6 +72,11 @@ struct fmm_ctx {
   cudaStream_t own_stream = nullptr, stream = nullptr;
   // the upward sweep runs on `aux`, concurrently with the traversal and the M2L class sort
   cudaStream_t aux = nullptr;
+  // the pipeline itself runs on `hi` (highest stream priority; joined with the caller's stream at
+  // entry and exit) and the near field on `aux` (lowest), so that the latency-bound M2L class sort
+  // gets SMs as soon as P2P blocks retire instead of queueing behind the whole P2P grid
+  cudaStream_t hi = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_up = nullptr, ev_trav = nullptr, ev_near = nullptr;
   // P2P / M2P run on `aux` after the traversal, overlapping the M2L class preparation and GEMM
   // on the main stream (off while the kernel pre-calculation times the kernels in isolation)
@@ -1089,8 +1094,25 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
 }
 
 static void read_phase_times(fmm_ctx *h);
+static int evaluate_run(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
+                        float *grad);
+// One evaluation: the work runs on the handle's high-priority stream, ordered after everything
+// already queued on the caller's stream, and the caller's stream waits for it at the end.
 static int evaluate_impl(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
                          float *grad) {
+  cudaStream_t user = h->stream;
+  CK(cudaEventRecord(h->ev_in, user));
+  CK(cudaStreamWaitEvent(h->hi, h->ev_in, 0));
+  h->stream = h->hi;
+  const int rc = evaluate_run(h, xyz, q, n, phi, grad);
+  h->stream = user;
+  CK(cudaEventRecord(h->ev_out, h->hi));
+  CK(cudaStreamWaitEvent(user, h->ev_out, 0));
+  return rc;
+}
+
+static int evaluate_run(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
+                        float *grad) {
   cudaStream_t st = h->stream;
   memset(&h->stats, 0, sizeof h->stats);
   h->stats.n = n;
@@ -1246,7 +1268,12 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
     if ((e = cudaGetDevice(&h->device)) != cudaSuccess) { rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e)); break; }
     if ((e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking)) != cudaSuccess) { rc = fail(h, FMM_E_CUDA, "%s", cudaGetErrorString(e)); break; }
     h->stream = h->own_stream;
-    if ((e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking)) != cudaSuccess ||
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if ((e = cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, prio_lo)) != cudaSuccess ||
+        (e = cudaStreamCreateWithPriority(&h->hi, cudaStreamNonBlocking, prio_hi)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&h->ev_trav, cudaEventDisableTiming)) != cudaSuccess ||
@@ -1326,6 +1353,9 @@ int fmm_destroy(fmm_t h) {
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->hi) cudaStreamDestroy(h->hi);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_out) cudaEventDestroy(h->ev_out);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_up) cudaEventDestroy(h->ev_up);
   if (h->ev_trav) cudaEventDestroy(h->ev_trav);

@@ -388,8 +388,10 @@ void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     resident = (per_sm > 0 ? per_sm : 1) * nsm;
   }
+  // up to 8 waves of blocks (not a persistent grid): blocks retire continually, so that kernels of
+  // a higher-priority stream (the M2L class sort running beside P2P) get SMs early
   const int need = (nleaves + P2P_WARPS - 1) / P2P_WARPS;
-  const int b = need < resident ? (need > 0 ? need : 1) : resident;
+  const int b = need < 8 * resident ? (need > 0 ? need : 1) : 8 * resident;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   k_p2p_leaves<<<b, P2P_WARPS * 32, 0, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f, counter);
 }

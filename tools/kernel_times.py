@@ -17,6 +17,7 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 xyz, q = make_particles(cfg["n"], cfg["dist"], cfg["seed"])
 X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
 f = FMM(p=cfg["p"], theta=cfg["theta"], ncrit=cfg["ncrit"], mode=mode)
+f.set_deterministic(os.environ.get("FMM_DET", "0") == "1")
 for _ in range(3):
     f.evaluate(X, Q)
 torch.cuda.synchronize()
