@@ -325,6 +325,12 @@ def run_ours(args):
         "counts": {k: stats[k] for k in ("ncells", "nleaves", "depth", "n_m2l", "n_m2p", "n_p2p",
                                           "p2p_pairs", "m2p_evals")},
         "cost_model": dict(zip(("t_pp", "t_mp", "t_ml"), f.cost_model())),
+        # SURVEY §8(d) interaction rates: kernel-only P2P pairs/s and M2L translations/s, and the
+        # direct-sum-equivalent N(N-1)/T of the whole evaluation
+        "interactions": {
+            "p2p_pairs_per_s": stats["p2p_pairs"] / (p2p_ms * 1e-3) if p2p_ms > 0 else None,
+            "m2l_per_s": stats["n_m2l"] / (m2l_ms * 1e-3) if m2l_ms > 0 else None,
+            "effective_pairs_per_s": float(n_all) * (n_all - 1) / (ms_step * 1e-3)},
         "tune_s": tune_s,
         "gpu_launches": launches,
         "roofline": roofline,

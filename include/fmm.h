@@ -104,6 +104,17 @@ int fmm_destroy(fmm_t h);
 int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float *d_phi,
                  float *d_grad);
 
+/* Distinct target and source sets (the dual tree traversal pairs target cells with
+ * source cells): phi / grad at the n_t target points d_xyz_t [3 n_t] due to the n_s charges
+ * d_q_s [n_s] at d_xyz_s [3 n_s] (all device, AoS as in fmm_evaluate). One octree is built over
+ * the union (targets carry zero charge, so they are not sources); only cells holding targets are
+ * traversed as targets and only leaves holding targets are evaluated. A target coincident with a
+ * source gets no contribution from it (r = 0 rule). Outputs are written for the n_t targets in
+ * their order. n_s = 0 gives zero fields. Not available on distributed handles or in FMM_DIRECT
+ * mode. Errors: as fmm_evaluate. */
+int fmm_evaluate_ts(fmm_t h, const float *d_xyz_t, int64_t n_t, const float *d_xyz_s,
+                    const float *d_q_s, int64_t n_s, float *d_phi_t, float *d_grad_t);
+
 /* Same with HOST buffers (pinned or pageable): copies in, evaluates, copies out (end-to-end path). */
 int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, float *h_phi,
                       float *h_grad);

@@ -150,6 +150,12 @@ struct fmm_ctx {
   int64_t last_n = 0;
   RootInfo h_root{};
 
+  // ---- distinct target / source sets (fmm_evaluate_ts): the first ts_nt particles of the union
+  // are the targets (zero charge); 0 = ordinary evaluation ----
+  int64_t ts_nt = 0;
+  DBuf<int> ntgt;
+  DBuf<float> ts_stage;
+
   // ---- multi-GPU; comm == nullptr: single GPU ----
   FmmComm *comm = nullptr;
   int64_t n_glob = 0;
@@ -355,7 +361,25 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
   h->part_lo = 0;
   h->part_hi = (int)n;
   h->tleaves_n = h->nleaves;
-  if (h->nparts > 1) {
+  if (h->ts_nt > 0) {  // target cells / leaves: the ones holding at least one target particle
+    CK(h->ntgt.ensure(total));
+    CK(h->tleaves.ensure(total));
+    CK(h->excl.ensure(std::max<int64_t>(n, total)));
+    int *flag = reinterpret_cast<int *>(h->acc.p);  // scratch (acc is written later by P2P)
+    launch_target_flags(h->perm.p, (int)n, (int)h->ts_nt, flag, st);
+    CKL();
+    if (int rc = cub_scan(h, flag, h->excl.p, (int)n)) return rc;
+    launch_cell_targets(total, h->cells(), h->excl.p, flag, (int)n, h->ntgt.p, h->leafflag.p, st);
+    CKL();
+    if (int rc = cub_scan(h, h->leafflag.p, h->excl.p, total)) return rc;
+    launch_leaf_scatter(total, h->leafflag.p, h->excl.p, h->tleaves.p, st);
+    CKL();
+    launch_level_total(h->leafflag.p, h->excl.p, total, h->d_small, st);
+    CKL();
+    CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h->tleaves_n = h->h_small[0];
+  } else if (h->nparts > 1) {
     CK(h->tleaves.ensure(total));
     launch_part_flags(total, h->cells(), n, h->nparts, h->part, h->leafflag.p, h->d_small + 8, st);
     h->stats.launches += 1;
@@ -779,6 +803,7 @@ static int traverse(fmm_ctx *h) {
       A.stack_cap = h->stack_cap;
       A.grid_blocks = std::min(grid_blocks, (nt + warps_per_block - 1) / warps_per_block);
       A.tlo = h->part_lo;
+      A.tmask = h->ts_nt > 0 ? h->ntgt.p : nullptr;
       A.thi = h->part_hi;
       A.theta = h->theta;
       A.t_pp = h->cost.t_pp;
@@ -925,7 +950,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   record(h, EV_TRAV);
   // a12 P2P (writes acc), a11 M2P (adds): on the aux stream (after the upward sweep there) when
   // overlapping, so that they run while the main stream sorts the M2L pairs into classes
-  const int *tl = (h->nparts > 1 || h->comm) ? h->tleaves.p : h->leaves.p;
+  const int *tl = (h->nparts > 1 || h->comm || h->ts_nt > 0) ? h->tleaves.p : h->leaves.p;
   const int ntl = h->tleaves_n;
   auto near_field = [&](cudaStream_t ns) -> int {
     record_on(h, EV_P2P0, ns);
@@ -1313,6 +1338,7 @@ int fmm_destroy(fmm_t h) {
   h->tleaves.release();
   h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
+  h->ntgt.release(); h->ts_stage.release();
   h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
@@ -1384,6 +1410,52 @@ int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float
     if (!rc) rc = check_device_ptr(h, d_grad, "grad");
   }
   if (!rc) rc = evaluate_impl(h, d_xyz, d_q, n, d_phi, d_grad);
+  if (cur != h->device && cur >= 0) cudaSetDevice(cur);
+  return rc;
+}
+
+int fmm_evaluate_ts(fmm_t h, const float *d_xyz_t, int64_t n_t, const float *d_xyz_s,
+                    const float *d_q_s, int64_t n_s, float *d_phi_t, float *d_grad_t) {
+  if (!h) return FMM_E_INVALID;
+  if (h->comm) return fail(h, FMM_E_INVALID, "fmm_evaluate_ts: not available on distributed handles");
+  if (h->mode == FMM_DIRECT) return fail(h, FMM_E_INVALID, "fmm_evaluate_ts: not in FMM_DIRECT mode");
+  if (n_t < 0 || n_s < 0) return fail(h, FMM_E_INVALID, "n < 0");
+  if (n_t == 0) {
+    memset(&h->stats, 0, sizeof h->stats);
+    return FMM_OK;
+  }
+  if (!d_xyz_t || !d_phi_t || !d_grad_t || (n_s > 0 && (!d_xyz_s || !d_q_s)))
+    return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
+  const int64_t n = n_t + n_s;
+  if (n > (int64_t)1 << 28) return fail(h, FMM_E_INVALID, "n_t + n_s = %lld exceeds 2^28", (long long)n);
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != h->device) cudaSetDevice(h->device);
+  int rc = check_device_ptr(h, d_xyz_t, "xyz_t");
+  if (!rc && n_s > 0) rc = check_device_ptr(h, d_xyz_s, "xyz_s");
+  if (!rc && n_s > 0) rc = check_device_ptr(h, d_q_s, "q_s");
+  if (!rc) rc = check_device_ptr(h, d_phi_t, "phi_t");
+  if (!rc) rc = check_device_ptr(h, d_grad_t, "grad_t");
+  if (!rc) {
+    // the union [targets (charge 0) | sources] and its full-size outputs, in handle scratch
+    cudaStream_t st = h->stream;
+    CK(h->ts_stage.ensure(8 * (size_t)n));
+    float *xyz = h->ts_stage.p, *q = xyz + 3 * n, *phi = q + n, *grad = phi + n;
+    CK(cudaMemcpyAsync(xyz, d_xyz_t, sizeof(float) * 3 * n_t, cudaMemcpyDeviceToDevice, st));
+    if (n_s > 0) {
+      CK(cudaMemcpyAsync(xyz + 3 * n_t, d_xyz_s, sizeof(float) * 3 * n_s, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(q + n_t, d_q_s, sizeof(float) * n_s, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaMemsetAsync(q, 0, sizeof(float) * n_t, st));
+    h->ts_nt = n_t;
+    rc = evaluate_impl(h, xyz, q, n, phi, grad);
+    h->ts_nt = 0;
+    if (!rc) {
+      CK(cudaMemcpyAsync(d_phi_t, phi, sizeof(float) * n_t, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(d_grad_t, grad, sizeof(float) * 3 * n_t, cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  }
   if (cur != h->device && cur >= 0) cudaSetDevice(cur);
   return rc;
 }

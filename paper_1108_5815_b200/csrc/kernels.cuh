@@ -37,6 +37,11 @@ void launch_part_flags(int ncells, CellsView C, int64_t n, int nparts, int part,
 void launch_part_indices(int lo, int cnt, const unsigned *perm, int64_t *out, cudaStream_t st);
 void launch_leaf_scatter(int ncells, const int *flag, const int *excl, int *leaves,
                          cudaStream_t st);
+// distinct target / source sets: flag[i] = (perm[i] < nt) over sorted particles; per cell target
+// counts from the exclusive scan of the flags; leaf flags of the leaves holding targets
+void launch_target_flags(const unsigned *perm, int n, int nt, int *flag, cudaStream_t st);
+void launch_cell_targets(int ncells, CellsView C, const int *excl, const int *flag, int n,
+                         int *ntgt, int *leafflag, cudaStream_t st);
 
 // ---- traverse.cu ----
 struct TravArgs {
@@ -44,6 +49,7 @@ struct TravArgs {
   const int4 *pk;  // packed cell records (k_pack_cells): [2c] = grid, [2c+1] = beg, cnt, child0, nchild
   int t0, nt, level, mode, stack_cap, grid_blocks;
   int tlo, thi;  // targets restricted to cells intersecting sorted particle range [tlo, thi)
+  const int *tmask;  // or null: per cell, number of target particles (0: not a target cell)
   double theta, t_pp, t_mp, t_ml;
   const unsigned *in_src;
   const int *in_off, *in_cnt;

@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
     const CellRec rt = load_rec(A.pk, t);
     const int4 gt = rt.g;
     const int tcnt = rt.b.y;
-    if (!(rt.b.x < A.thi && rt.b.x + tcnt > A.tlo)) {  // outside this rank's target partition
+    // outside this rank's target partition, or (distinct target / source sets) no target inside
+    if (!(rt.b.x < A.thi && rt.b.x + tcnt > A.tlo) || (A.tmask && A.tmask[t] == 0)) {
       if (lane == 0) {
         if (WRITE) {
           for (int c = 0; c < 3; ++c) {

@@ -392,3 +392,26 @@ void launch_leaf_scatter(int ncells, const int *flag, const int *excl, int *leav
                          cudaStream_t st) {
   k_leaf_scatter<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, flag, excl, leaves);
 }
+
+// ---- distinct target / source sets --------------------------------------------
+__global__ void k_target_flags(const unsigned *__restrict__ perm, int n, int nt, int *flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    flag[i] = perm[i] < (unsigned)nt;
+}
+__global__ void k_cell_targets(int ncells, CellsView C, const int *__restrict__ excl,
+                               const int *__restrict__ flag, int n, int *ntgt, int *leafflag) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const int b = C.beg[c], e = b + C.cnt[c];
+  const int hi = e < n ? excl[e] : excl[n - 1] + flag[n - 1];
+  const int k = hi - excl[b];
+  ntgt[c] = k;
+  leafflag[c] = C.nchild[c] == 0 && k > 0;
+}
+void launch_target_flags(const unsigned *perm, int n, int nt, int *flag, cudaStream_t st) {
+  k_target_flags<<<grid_for(n, 256), 256, 0, st>>>(perm, n, nt, flag);
+}
+void launch_cell_targets(int ncells, CellsView C, const int *excl, const int *flag, int n,
+                         int *ntgt, int *leafflag, cudaStream_t st) {
+  k_cell_targets<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, C, excl, flag, n, ntgt, leafflag);
+}

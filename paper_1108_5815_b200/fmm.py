@@ -11,7 +11,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 HYBRID, FMM_MODE, TREECODE, DIRECT = 0, 1, 2, 3
 MODES = {"hybrid": HYBRID, "fmm": FMM_MODE, "treecode": TREECODE, "direct": DIRECT}
-SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_host", "fmm_set_stream",
+SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_ts", "fmm_evaluate_host",
+           "fmm_set_stream",
            "fmm_set_mode", "fmm_set_timing", "fmm_set_deterministic", "fmm_tune", "fmm_get_cost_model",
            "fmm_set_cost_model", "fmm_get_stats", "fmm_export_tree", "fmm_export_lists",
            "fmm_export_perm", "fmm_set_partition", "fmm_get_partition", "fmm_partition_indices",
@@ -67,6 +68,7 @@ def load_library():
     L.fmm_destroy.argtypes = [vp]
     L.fmm_evaluate.argtypes = [vp, vp, vp, i64, vp, vp]
     L.fmm_evaluate_host.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.fmm_evaluate_ts.argtypes = [vp, vp, i64, vp, vp, i64, vp, vp]
     L.fmm_set_stream.argtypes = [vp, vp]
     L.fmm_set_mode.argtypes = [vp, C.c_int]
     L.fmm_set_timing.argtypes = [vp, C.c_int]
@@ -231,6 +233,25 @@ class FMM:
                     "fmm_set_stream")
         self._check(self.L.fmm_evaluate(self.h, xyz.data_ptr(), q.data_ptr(), n, phi.data_ptr(),
                                         grad.data_ptr()), "fmm_evaluate")
+        return phi, grad
+
+    def evaluate_ts(self, xyz_t, xyz_s, q_s):
+        """Distinct targets and sources (fmm_evaluate_ts): CUDA float32 xyz_t [Nt,3], xyz_s [Ns,3],
+        q_s [Ns]. Returns (phi [Nt], grad [Nt,3]) at the targets due to the sources."""
+        import torch
+
+        for a in (xyz_t, xyz_s, q_s):
+            assert a.is_cuda and a.dtype == torch.float32 and a.is_contiguous()
+        nt, ns = xyz_t.shape[0], q_s.numel()
+        phi = torch.empty(nt, dtype=torch.float32, device=xyz_t.device)
+        grad = torch.empty((nt, 3), dtype=torch.float32, device=xyz_t.device)
+        if nt == 0:
+            return phi, grad
+        self._check(self.L.fmm_set_stream(self.h, C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                    "fmm_set_stream")
+        self._check(self.L.fmm_evaluate_ts(self.h, xyz_t.data_ptr(), nt, xyz_s.data_ptr() if ns else None,
+                                           q_s.data_ptr() if ns else None, ns, phi.data_ptr(),
+                                           grad.data_ptr()), "fmm_evaluate_ts")
         return phi, grad
 
     def evaluate_host(self, xyz: np.ndarray, q: np.ndarray, phi=None, grad=None):

@@ -255,3 +255,41 @@ def test_m2l_block_order(O, handles, monkeypatch, blk, deterministic):
     ref = O.fmm(xyz, q, 8, 0.45, 32, O.HYBRID, cost=COST)
     assert np.array_equal(lists, O.canonical_tasks(ref.tasks))
     assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
+
+
+@pytest.mark.parametrize("nt,ns,dist", [(3000, 20000, "uniform"), (15000, 4000, "plummer"),
+                                        (500, 30000, "shell")])
+def test_distinct_targets_and_sources(O, handles, nt, ns, dist):
+    # PAPER.md:145 distinct target and source sets (fmm_evaluate_ts) against the oracle run on the
+    # union with zero target charges: same fields at the targets; the lists are the oracle's lists
+    # of the target cells that hold targets
+    xt, _ = make_particles(nt, dist, 61)
+    xs, qs = make_particles(ns, "mixed" if dist == "uniform" else dist, 62)
+    f = handles(8, 0.45, 32, "hybrid")
+    phi, grad = f.evaluate_ts(dev(xt), dev(xs), dev(qs))
+    torch.cuda.synchronize()
+    lists = O.canonical_tasks(f.export_lists())
+    xu = np.concatenate([xt, xs]).astype(np.float32)
+    qu = np.concatenate([np.zeros(nt, np.float32), qs]).astype(np.float32)
+    ref = O.fmm(xu, qu, 8, 0.45, 32, O.HYBRID, cost=COST)
+    assert O.rel_l2(phi.cpu().numpy(), ref.phi[:nt]) < 1e-5
+    assert O.rel_l2(grad.cpu().numpy(), ref.grad[:nt]) < 1e-5
+    tr = ref.tree
+    has_t = {(int(l), int(p)) for l, p, b, c in zip(tr["level"], tr["prefix"], tr["begin"], tr["count"])
+             if np.any(ref.perm[int(b):int(b) + int(c)] < nt)}
+    want = O.canonical_tasks(ref.tasks)
+    keep = np.array([(int(r["tlevel"]), int(r["tprefix"])) in has_t for r in want], bool)
+    assert np.array_equal(lists, want[keep])
+    d = O.direct(xu, qu, np.arange(0, nt, max(1, nt // 300)))
+    assert O.rel_l2(phi.cpu().numpy()[::max(1, nt // 300)], d[0]) < 1e-4
+
+
+def test_distinct_sets_edge_cases(handles):
+    f = handles(4, 0.5, 16, "hybrid")
+    xt = dev(np.random.default_rng(1).random((100, 3), dtype=np.float32))
+    e3 = torch.empty((0, 3), dtype=torch.float32, device="cuda")
+    e1 = torch.empty(0, dtype=torch.float32, device="cuda")
+    phi, grad = f.evaluate_ts(xt, e3, e1)  # no sources: zero fields
+    assert float(phi.abs().max()) == 0.0 and float(grad.abs().max()) == 0.0
+    phi, grad = f.evaluate_ts(e3, xt, dev(np.ones(100, np.float32)))  # no targets
+    assert phi.numel() == 0
