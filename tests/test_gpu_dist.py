@@ -172,3 +172,35 @@ def test_dist_bench_workload_shape():
     assert O.rel_l2(phi[s], d[0]) < 1e-4 and O.rel_l2(grad[s], d[1]) < 1e-3
     st = [o["stats"] for o in out]
     assert all(x["let_cells"] > 0 and x["let_particles"] > 0 for x in st)
+
+
+def test_nccl_transport_world1(tmp_path):
+    # the NCCL transport (fmm_comm_unique_id / fmm_create_dist, libnccl dlopen'ed) end to end
+    # through paper_1108_5815_b200.dist.DistFMM on a 1-rank torch.distributed NCCL group: the
+    # distributed pipeline with its exchanges against the plain handle
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1108_5815_b200.dist import DistFMM
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        xyz, q = make_particles(30000, "plummer", 91)
+        ref = single(xyz, q, 8, 0.45, 32, "hybrid")
+        f = DistFMM(p=8, theta=0.45, ncrit=32, mode="hybrid", tune=False)
+        f.set_cost_model(*COST)
+        phi, grad = f.evaluate(torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda())
+        torch.cuda.synchronize()
+        st = f.stats()
+        f.close()
+    finally:
+        dist.destroy_process_group()
+    assert O.rel_l2(phi.cpu().numpy(), ref["phi"]) < 1e-6
+    assert O.rel_l2(grad.cpu().numpy(), ref["grad"]) < 1e-6
+    assert st["n_global"] == 30000 and st["rank_lo"] == 0 and st["rank_hi"] == 30000
