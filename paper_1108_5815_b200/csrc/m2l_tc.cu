@@ -253,8 +253,10 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
   extern __shared__ __align__(1024) unsigned char sh_tc[];
   unsigned *Bimg = reinterpret_cast<unsigned *>(sh_tc);                      // Th | Tl
   float *Xst = reinterpret_cast<float *>(sh_tc + TBYTES);                     // [128][MROW]
+  // the epilogue's transpose buffer exists only for the Y-slot epilogue: in accumulate mode the
+  // CTA is 18 KB smaller, so that a P2P block fits on the same SM beside it
   float *Ep = Xst + 128 * MROW;                                                // [4][32][36]
-  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Ep + 4 * 32 * 36);
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(Ep + (Lacc ? 0 : 4 * 32 * 36));
   unsigned *tmem_base_slot = reinterpret_cast<unsigned *>(bars + 6);
   volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 7);
   unsigned long long *t_full = &bars[0], *mma_done = &bars[1], *x_full = &bars[2];
@@ -506,10 +508,12 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
   cudaMemsetAsync(queue, 0, sizeof(int), st);
 #define M2L_TC_CASE(PP)                                                                        \
   case PP: {                                                                                 \
-    const size_t smem = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + 4 * 32 * 36 * 4 + 128; \
+    const size_t ep_bytes = 4 * 32 * 36 * 4;                                                 \
+    const size_t smem_full = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + ep_bytes + 128; \
+    const size_t smem = Lacc ? smem_full - ep_bytes : smem_full;                             \
     static bool cfg = false;                                                                 \
     if (!cfg) {                                                                              \
-      cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full); \
       cfg = true;                                                                            \
     }                                                                                        \
     k_m2l_tc<PP><<<grid, 160, smem, st>>>(items, counters, sidx, ssrc, Timg,                 \
