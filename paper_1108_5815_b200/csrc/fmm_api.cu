@@ -140,7 +140,10 @@ struct fmm_ctx {
   DBuf<int> loff[3], lcnt[3];
   DBuf<unsigned> lsrc[3];
   DBuf<int2> p2p_rng;
-  DBuf<int> out_off, out_cnt, cnt4, excl4;
+  DBuf<int> out_off, out_cnt;
+  DBuf<unsigned> trav_osc;
+  DBuf<int2> trav_rsc;
+  int trav_ocap = 2048;  // per-warp list scratch (entries per list), doubled on overflow
   DBuf<unsigned> outA, outB, stack;
   int stack_cap = 2048;
   size_t trav_cap[4] = {0, 0, 0, 0};  // list buffer sizes seen so far (traverse)
@@ -747,10 +750,11 @@ static int dist_return(fmm_ctx *h, float *phi, float *grad) {
 
 // ---- a9: traversal ----------------------------------------------------------------------------
 static int traverse(fmm_ctx *h) {
-  // Level-synchronous target-centric traversal (traverse.cu). All bookkeeping stays on the
-  // device: list buffers are sized from the previous evaluation (or an estimate), the write pass
-  // of a level whose lists would not fit does nothing, and one read-back at the end decides
-  // whether to re-run with larger buffers (stack or lists) -- no host round trip per level.
+  // Level-synchronous target-centric traversal (traverse.cu), one kernel per level. All
+  // bookkeeping stays on the device: list buffers are sized from the previous evaluation (or an
+  // estimate), a target whose lists would not fit writes nothing, and one read-back at the end
+  // decides whether to re-run with larger buffers (stack, scratch or lists) -- no host round trip
+  // per level.
   cudaStream_t st = h->stream;
   const int nc = h->ncells;
   for (int k = 0; k < 3; ++k) {
@@ -767,10 +771,6 @@ static int traverse(fmm_ctx *h) {
   const int warps_per_block = 4;
   const int grid_blocks = 148 * 8;
   const size_t nwarps = (size_t)grid_blocks * warps_per_block;
-  int maxnt = 1;
-  for (int level = 0; level <= h->depth; ++level) maxnt = std::max(maxnt, h->level_cnt[level]);
-  CK(h->cnt4.ensure((size_t)4 * maxnt));
-  CK(h->excl4.ensure((size_t)4 * maxnt));
   // capacities: at least the previous evaluation's totals, else an estimate per target cell
   size_t cap[4];
   for (int k = 0; k < 4; ++k) {
@@ -780,11 +780,13 @@ static int traverse(fmm_ctx *h) {
   }
   for (int attempt = 0;; ++attempt) {
     CK(h->stack.ensure(nwarps * h->stack_cap));
+    CK(h->trav_osc.ensure(nwarps * 4 * (size_t)h->trav_ocap));
+    CK(h->trav_rsc.ensure(nwarps * (size_t)h->trav_ocap));
     for (int k = 0; k < 3; ++k) CK(h->lsrc[k].ensure(cap[k]));
     CK(h->p2p_rng.ensure(cap[2]));
     CK(h->outA.ensure(cap[3]));
     CK(h->outB.ensure(cap[3]));
-    int hb[20] = {0};
+    int hb[TRAV_BK_INTS] = {0};
     for (int k = 0; k < 4; ++k) hb[8 + k] = (int)cap[k];
     CK(cudaMemcpyAsync(h->d_bk, hb, sizeof hb, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(h->d_overflow, 0, sizeof(unsigned), st));
@@ -814,8 +816,9 @@ static int traverse(fmm_ctx *h) {
       A.in_cnt = h->out_cnt.p;
       A.scratch = h->stack.p;
       A.overflow = h->d_overflow;
-      A.cnt4 = h->cnt4.p;
-      A.excl = h->excl4.p;
+      A.oscratch = h->trav_osc.p;
+      A.rscratch = h->trav_rsc.p;
+      A.ocap = h->trav_ocap;
       A.stats = h->d_stats;
       A.bk = h->d_bk;
       for (int k = 0; k < 3; ++k) {
@@ -828,39 +831,37 @@ static int traverse(fmm_ctx *h) {
       A.out_src = ob->p;
       A.out_off = h->out_off.p;
       A.out_cnt = h->out_cnt.p;
-      launch_traverse(A, false, st);
-      CKL();
-      if (int rc = cub_scan(h, h->cnt4.p, h->excl4.p, 4 * nt)) return rc;
-      launch_trav_totals(h->excl4.p, h->cnt4.p, nt, h->d_bk, st);
-      CKL();
-      launch_traverse(A, true, st);
+      CK(cudaMemsetAsync(h->d_bk + TRAV_CNT(3), 0, sizeof(int), st));  // this level's deferred pairs
+      launch_traverse(A, st);
       CKL();
       in_src = ob->p;
     }
-    int hb2[20];
+    int hb2[TRAV_BK_INTS];
     unsigned ovf = 0;
     unsigned long long hs[2];
     CK(cudaMemcpyAsync(hb2, h->d_bk, sizeof hb2, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&ovf, h->d_overflow, sizeof ovf, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hs, h->d_stats, sizeof hs, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (ovf) {  // a warp's traversal stack overflowed: larger stacks, again
-      h->stack_cap *= 2;
-      if ((size_t)h->stack_cap * nwarps > ((size_t)1 << 31))
-        return fail(h, FMM_E_OOM, "traversal stack exceeds 8 GiB");
+    if (ovf) {  // a warp's stack (bit 1) or list scratch (bit 2) overflowed: larger ones, again
+      if (ovf & 1u) h->stack_cap *= 2;
+      if (ovf & 2u) h->trav_ocap *= 2;
+      if ((size_t)h->stack_cap * nwarps > ((size_t)1 << 31) ||
+          (size_t)h->trav_ocap * nwarps * 4 > ((size_t)1 << 31))
+        return fail(h, FMM_E_OOM, "traversal scratch exceeds 8 GiB");
       continue;
     }
     if (hb2[12]) {  // a list buffer was too small: grow to what the count passes have seen so far
       if (attempt > 8) return fail(h, FMM_E_OOM, "interaction lists do not fit");
       for (int k = 0; k < 4; ++k) {
-        const size_t need = (size_t)(k < 3 ? hb2[16 + k] : 0);
+        const size_t need = (size_t)(k < 3 ? hb2[TRAV_CNT(k)] : 0);
         cap[k] = std::min((size_t)INT32_MAX - 1, std::max(cap[k] * 2, need + need / 4 + 1024));
       }
       continue;
     }
     for (int k = 0; k < 3; ++k) {
-      h->ntask[k] = hb2[16 + k];
-      h->trav_cap[k] = std::max(h->trav_cap[k], (size_t)hb2[16 + k] + 1);
+      h->ntask[k] = hb2[TRAV_CNT(k)];
+      h->trav_cap[k] = std::max(h->trav_cap[k], (size_t)hb2[TRAV_CNT(k)] + 1);
     }
     h->trav_cap[3] = std::max(h->trav_cap[3], cap[3]);
     h->stats.p2p_pairs = (int64_t)hs[0];
@@ -1310,7 +1311,7 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
     if (cudaMalloc(&h->d_root, sizeof(RootInfo)) || cudaMalloc(&h->d_mm, 8 * sizeof(unsigned)) ||
         cudaMalloc(&h->d_small, 16 * sizeof(int)) || cudaMalloc(&h->d_overflow, sizeof(unsigned)) ||
         cudaMalloc(&h->d_stats, 4 * sizeof(unsigned long long)) ||
-        cudaMalloc(&h->d_bk, 32 * sizeof(int)) ||
+        cudaMalloc(&h->d_bk, TRAV_BK_INTS * sizeof(int)) ||
         cudaMallocHost(&h->h_small, 16 * sizeof(int))) {
       rc = fail(h, FMM_E_OOM, "small device allocations failed");
       break;
@@ -1349,7 +1350,8 @@ int fmm_destroy(fmm_t h) {
   h->sh_src.release(); h->sh_T.release(); h->sh_items.release(); h->sh_counters.release();
   h->m2l_Y.release(); h->sh_Y.release(); h->cub_tmp_aux.release(); h->m2l_Ttc.release(); h->m2l_class_rep.release(); h->m2l_ssrc.release(); h->m2l_stgt.release(); h->m2l_T.release();
   for (int k = 0; k < 3; ++k) { h->loff[k].release(); h->lcnt[k].release(); h->lsrc[k].release(); }
-  h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release(); h->cnt4.release(); h->excl4.release();
+  h->p2p_rng.release(); h->out_off.release(); h->out_cnt.release();
+  h->trav_osc.release(); h->trav_rsc.release();
   h->outA.release(); h->outB.release(); h->stack.release();
   for (auto *b : {&h->d_off, &h->d_lb, &h->d_cnt, &h->strad_flag, &h->strad_excl, &h->need_m,
                   &h->need_p, &h->dexcl, &h->psize, &h->pexcl, &h->prsize, &h->prexcl, &h->psz2,

@@ -44,6 +44,10 @@ void launch_cell_targets(int ncells, CellsView C, const int *excl, const int *fl
                          int *ntgt, int *leafflag, cudaStream_t st);
 
 // ---- traverse.cu ----
+// the four list counters of the traversal, one per 128-byte line (every target does one atomic
+// on each: on a shared line they would serialise in one L2 slice)
+#define TRAV_CNT(c) (32 + 32 * (c))
+#define TRAV_BK_INTS 160
 struct TravArgs {
   CellsView C;
   const int4 *pk;  // packed cell records (k_pack_cells): [2c] = grid, [2c+1] = beg, cnt, child0, nchild
@@ -53,24 +57,23 @@ struct TravArgs {
   double theta, t_pp, t_mp, t_ml;
   const unsigned *in_src;
   const int *in_off, *in_cnt;
-  unsigned *scratch, *overflow;
-  int *cnt4;
-  const int *excl;
-  // device-resident bookkeeping (no host round trip per level), see k_trav_totals:
-  //   [0..3] this level's scan value at the first target of each category, [4..7] where this
-  //   level's lists start in lsrc[k] / the out buffer, [8..11] capacities, [12] overflow flag,
-  //   [16..18] running list sizes
+  unsigned *scratch, *overflow;  // per-warp stack; overflow bits: 1 stack, 2 list scratch
+  unsigned *oscratch;            // per-warp [4][ocap] lists of the current target
+  int2 *rscratch;                // per-warp [ocap] P2P source ranges
+  int ocap;
+  // device-resident bookkeeping (no host round trip per level): [8..11] capacities of the three
+  // lists and of the deferred-pair buffer, [12] overflow flag, [TRAV_CNT(0..2)] running list
+  // sizes, [TRAV_CNT(3)] this level's deferred pairs (reset per level)
   int *bk;
   unsigned *lsrc[3];
   int *loff[3], *lcnt[3];
   unsigned *out_src;
   int *out_off, *out_cnt;
-  int2 *p2p_rng;  // WRITE pass: (begin, count) of each P2P source cell, parallel to lsrc[2]
+  int2 *p2p_rng;  // (begin, count) of each P2P source cell, parallel to lsrc[2]
   unsigned long long *stats;  // [0] P2P particle pairs, [1] M2P target evaluations
 };
-void launch_traverse(const TravArgs &A, bool write, cudaStream_t st);
+void launch_traverse(const TravArgs &A, cudaStream_t st);
 void launch_pack_cells(int ncells, CellsView C, int4 *pk, cudaStream_t st);
-void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *bk, cudaStream_t st);
 
 // ---- expansions.cu ----
 struct M2LTiles {

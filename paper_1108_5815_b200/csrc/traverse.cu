@@ -10,9 +10,12 @@
 // their parents"). Each target's interaction lists therefore come out contiguous and in
 // a deterministic order, with no global sort.
 //
-// Two passes per level: COUNT (sizes per target) -> one exclusive scan -> WRITE (same logic,
-// writing at the scanned offsets). The MAC is the exact integer/FP64 test of DESIGN.md §3 (R4, R5)
-// and the kind choice the linear cost model with ties M2L > M2P > P2P (R8).
+// One pass per level: a warp collects its target's four lists (M2L, M2P, P2P, deferred) in its own
+// scratch, then claims their final space with one atomic per list and copies them there. Each
+// target's lists are contiguous and in a deterministic order (ballot order); only where a target's
+// segment lands in the global arrays depends on the schedule, and every consumer addresses the
+// lists through the per-target (offset, count). The MAC is the exact integer/FP64 test of
+// DESIGN.md §3 (R4, R5) and the kind choice the linear cost model with ties M2L > M2P > P2P (R8).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -60,7 +63,6 @@ void launch_pack_cells(int ncells, CellsView C, int4 *pk, cudaStream_t st) {
   if (ncells > 0) k_pack_cells<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, C, pk);
 }
 
-template <bool WRITE>
 __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
   const CellsView C = A.C;
   const int lane = threadIdx.x & 31;
@@ -68,16 +70,9 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   unsigned *stack = A.scratch + (size_t)gw * A.stack_cap;
+  unsigned *osc = A.oscratch + (size_t)gw * 4 * A.ocap;  // [4][ocap] this target's lists
+  int2 *rsc = A.rscratch + (size_t)gw * A.ocap;          // P2P source ranges, parallel to [2]
 
-  int bk_excl[4] = {0, 0, 0, 0}, bk_base[4] = {0, 0, 0, 0};
-  if (WRITE) {
-    if (A.bk[12]) return;  // a list would overflow its buffer: the host re-runs with larger ones
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      bk_excl[c] = A.bk[c];
-      bk_base[c] = A.bk[4 + c];
-    }
-  }
   unsigned long long warp_pp = 0, warp_mp = 0;
   for (int k = gw; k < A.nt; k += nw) {
     const int t = A.t0 + k;
@@ -87,41 +82,20 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
     // outside this rank's target partition, or (distinct target / source sets) no target inside
     if (!(rt.b.x < A.thi && rt.b.x + tcnt > A.tlo) || (A.tmask && A.tmask[t] == 0)) {
       if (lane == 0) {
-        if (WRITE) {
-          for (int c = 0; c < 3; ++c) {
-            A.loff[c][t] = 0;
-            A.lcnt[c][t] = 0;
-          }
-          A.out_off[t] = 0;
-          A.out_cnt[t] = 0;
-        } else {
-          for (int c = 0; c < 4; ++c) A.cnt4[c * A.nt + k] = 0;
+        for (int c = 0; c < 3; ++c) {
+          A.loff[c][t] = 0;
+          A.lcnt[c][t] = 0;
         }
+        A.out_off[t] = 0;
+        A.out_cnt[t] = 0;
       }
       continue;
     }
     const bool tleaf = rt.b.w == 0;
     int n[4] = {0, 0, 0, 0};
-    unsigned *dst[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (WRITE) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int o = bk_base[c] + A.excl[c * A.nt + k] - bk_excl[c];
-        dst[c] = (c < 3 ? A.lsrc[c] : A.out_src) + o;
-        if (lane == 0) {
-          if (c < 3) {
-            A.loff[c][t] = o;
-            A.lcnt[c][t] = A.cnt4[c * A.nt + k];
-          } else {
-            A.out_off[t] = o;
-            A.out_cnt[t] = A.cnt4[c * A.nt + k];
-          }
-        }
-      }
-    }
     unsigned long long pp_pairs = 0, mp_evals = 0;  // this target's lane partials
     int top = 0;
-    bool overflow = false;
+    bool overflow = false, ovf_out = false;
 
     // classify (t, s) and append it to its category with ballots (deterministic order)
     auto consider_and_put = [&](bool valid, unsigned s, int forced_cat) {
@@ -142,10 +116,8 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
             cat = CAT_PUSH;
         }
       }
-      if (!WRITE) {
-        if (cat == CAT_P2P) pp_pairs += (unsigned long long)tcnt * (unsigned long long)scnt;
-        if (cat == CAT_M2P) mp_evals += (unsigned long long)tcnt;
-      }
+      if (cat == CAT_P2P) pp_pairs += (unsigned long long)tcnt * (unsigned long long)scnt;
+      if (cat == CAT_M2P) mp_evals += (unsigned long long)tcnt;
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         const unsigned b = __ballot_sync(0xffffffffu, cat == c);
@@ -156,15 +128,15 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
           top += __popc(b);
           if (top > A.stack_cap) overflow = true;
         } else {
-          if (WRITE && cat == c) {
-            dst[c][n[c] + pos] = s;
-            if (c == CAT_P2P) A.p2p_rng[(dst[c] - A.lsrc[2]) + n[c] + pos] = make_int2(sbeg, scnt);
+          if (cat == c && n[c] + pos < A.ocap) {
+            osc[(size_t)c * A.ocap + n[c] + pos] = s;
+            if (c == CAT_P2P) rsc[n[c] + pos] = make_int2(sbeg, scnt);
           }
           n[c] += __popc(b);
+          if (n[c] > A.ocap) ovf_out = true;
         }
       }
     };
-
     // 1) inherited pairs (parent(t), s) split on the target side: test (t, s)
     int in_off = 0, in_cnt = 1;
     if (A.level > 0) {
@@ -180,7 +152,7 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
     }
     __syncwarp();
     // 2) the paper's stack: pop, split the larger cell (ties and leaf targets split the source)
-    while (top > 0 && !overflow) {
+    while (top > 0 && !overflow && !ovf_out) {
       const int nb = min(top, 32);
       top -= nb;
       const bool valid = lane < nb;
@@ -202,54 +174,54 @@ __global__ void __launch_bounds__(128) k_traverse(TravArgs A) {
       for (int j = 0; j < mmax; ++j) consider_and_put(j < m, (unsigned)(c0 + j), -1);
       __syncwarp();
     }
-    if (overflow) {
-      if (lane == 0) atomicOr(A.overflow, 1u);
+    if (overflow || ovf_out) {  // the host re-runs the traversal with larger scratch
+      if (lane == 0) atomicOr(A.overflow, overflow ? 1u : 2u);
       continue;
     }
-    if (!WRITE) {
-      if (lane == 0) {
+    // claim the final space of the four lists (running list sizes, this level's deferred pairs:
+    // counters in separate 128-byte lines, see TRAV_CNT) and copy them there
+    int base[4];
+    if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) A.cnt4[c * A.nt + k] = n[c];
+      for (int c = 0; c < 4; ++c) {
+        base[c] = n[c] ? atomicAdd(&A.bk[TRAV_CNT(c)], n[c]) : 0;
+        if ((long long)base[c] + n[c] + 1 > A.bk[8 + c]) A.bk[12] = 1;
       }
-      warp_pp += pp_pairs;  // one atomic per warp at the end, not two per target
-      warp_mp += mp_evals;
     }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) base[c] = __shfl_sync(0xffffffffu, base[c], 0);
+    const bool fits = *(volatile int *)&A.bk[12] == 0;
+    if (lane == 0) {
+      for (int c = 0; c < 3; ++c) {
+        A.loff[c][t] = base[c];
+        A.lcnt[c][t] = n[c];
+      }
+      A.out_off[t] = base[3];
+      A.out_cnt[t] = n[3];
+    }
+    if (fits) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        unsigned *dst = (c < 3 ? A.lsrc[c] : A.out_src) + base[c];
+        const unsigned *src = osc + (size_t)c * A.ocap;
+        for (int e = lane; e < n[c]; e += 32) dst[e] = src[e];
+      }
+      for (int e = lane; e < n[2]; e += 32) A.p2p_rng[base[2] + e] = rsc[e];
+    }
+    __syncwarp();
+    warp_pp += pp_pairs;  // one atomic per warp at the end, not two per target
+    warp_mp += mp_evals;
   }
-  if (!WRITE) {
-    for (int o = 16; o > 0; o >>= 1) {
-      warp_pp += __shfl_xor_sync(0xffffffffu, warp_pp, o);
-      warp_mp += __shfl_xor_sync(0xffffffffu, warp_mp, o);
-    }
-    if (lane == 0 && (warp_pp | warp_mp)) {
-      atomicAdd(&A.stats[0], warp_pp);
-      atomicAdd(&A.stats[1], warp_mp);
-    }
+  for (int o = 16; o > 0; o >>= 1) {
+    warp_pp += __shfl_xor_sync(0xffffffffu, warp_pp, o);
+    warp_mp += __shfl_xor_sync(0xffffffffu, warp_mp, o);
+  }
+  if (lane == 0 && (warp_pp | warp_mp)) {
+    atomicAdd(&A.stats[0], warp_pp);
+    atomicAdd(&A.stats[1], warp_mp);
   }
 }
 
-// level totals from the one exclusive scan over the four categories: where each category's
-// scan starts, where this level's lists go (running sizes) and an overflow flag when a buffer
-// is too small (the write pass then does nothing and the host re-runs the traversal)
-__global__ void k_trav_totals(const int *excl, const int *cnt4, int nt, int *bk) {
-  for (int c = 0; c < 4; ++c) {
-    const int e0 = excl[c * nt];
-    const int last = (c + 1) * nt - 1;
-    const long long tot = (long long)excl[last] + cnt4[last] - e0;
-    bk[c] = e0;
-    const long long start = c < 3 ? bk[16 + c] : 0;
-    bk[4 + c] = (int)start;
-    if (start + tot + 1 > bk[8 + c]) bk[12] = 1;
-    if (c < 3) bk[16 + c] = (int)min(start + tot, (long long)INT32_MAX);
-  }
-}
-
-void launch_traverse(const TravArgs &A, bool write, cudaStream_t st) {
-  const int blocks = A.grid_blocks;
-  if (write)
-    k_traverse<true><<<blocks, 128, 0, st>>>(A);
-  else
-    k_traverse<false><<<blocks, 128, 0, st>>>(A);
-}
-void launch_trav_totals(const int *excl, const int *cnt4, int nt, int *bk, cudaStream_t st) {
-  k_trav_totals<<<1, 1, 0, st>>>(excl, cnt4, nt, bk);
+void launch_traverse(const TravArgs &A, cudaStream_t st) {
+  k_traverse<<<A.grid_blocks, 128, 0, st>>>(A);
 }
