@@ -236,6 +236,12 @@ __device__ __forceinline__ void cp_async_wait_all_tc() { asm volatile("cp.async.
 // issuer never waits for the epilogue, so MMA(i+1) overlaps the epilogue of tile i and the X
 // gather of tile i+2.
 // TMEM columns: Xh [0,NT) | Xl [NT,2NT) | D0 [2NT,3NT) | D1 [3NT,4NT)  (4 NT <= 512 -> p <= 10)
+// The per-item hand-off between the issuer warp and the row warps: they reach it from their own
+// code paths (and the issuer warp right after one lane's atomicAdd), so it is a named, non-aligned
+// barrier with an explicit count (barrier.sync 1, 160) instead of __syncthreads (= the aligned
+// bar.sync 0, which expects every warp converged on one barrier instruction).
+__device__ __forceinline__ void item_bar() { asm volatile("barrier.sync 1, 160;" ::: "memory"); }
+
 template <int p>
 __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ items,
                                                    const int *__restrict__ counters,
@@ -294,9 +300,9 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
     const unsigned bh_addr = smem_addr(Bimg), bl_addr = bh_addr + (unsigned)(NT * NT * 4);
     for (;;) {
       if (tid == 128) item_sh[0] = atomicAdd(queue, 1);
-      __syncthreads();
+      item_bar();
       const int it = item_sh[0];
-      __syncthreads();  // item_sh is rewritten for the next item only after everyone read it
+      item_bar();  // item_sh is rewritten for the next item only after everyone read it
       if (it >= nitems) break;
       const int4 item = items[it];
       const int ntile = (item.y + 127) / 128;
@@ -407,9 +413,9 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
       }
     };
     for (;;) {
-      __syncthreads();  // the issuer fetched the next item
+      item_bar();  // the issuer fetched the next item
       const int it = item_sh[0];
-      __syncthreads();
+      item_bar();
       if (it >= nitems) break;
       const int4 item = items[it];
       const int pos0 = item.x, cnt = item.y;

@@ -1,0 +1,31 @@
+"""compute-sanitizer over small evaluations that reach every kernel:
+memcheck (out-of-bounds / misaligned accesses) and synccheck (barrier misuse) must report no
+error. tools/sanitize_run.py covers all modes, the three M2L paths, both M2L summation modes,
+distinct target/source sets and a 2-rank in-process distributed evaluation."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "3", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_run.py")],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert "SANITIZE_DONE" in out, out[-3000:]
+    assert r.returncode == 0 and "ERROR SUMMARY: 0 errors" in out, out[-3000:]

@@ -100,3 +100,45 @@ def test_theta_monotonicity(O):
     errs = [O.rel_l2(O.fmm(xyz, q, 4, th, 16, O.FMM, want_structure=False).phi, d[0])
             for th in (0.7, 0.5, 0.35, 0.25)]
     assert all(b < a for a, b in zip(errs, errs[1:])), errs
+
+
+def test_coverage_check_detects_mutations(O):
+    # SURVEY §4.2 mutation test: the exact-coverage check must fail when the task set is wrong --
+    # a dropped task leaves pairs uncovered, a duplicated task covers pairs twice
+    xyz, q = make_particles(300, "uniform", 9)
+    res = O.fmm(xyz, q, 2, 0.5, 16, O.HYBRID, cost=(2e-12, 6e-11, 2.5e-9))
+    assert np.all(coverage(O, res, len(q)) == 1)
+    t = res.tasks
+    for mutate in ("drop", "dup"):
+        idx = np.arange(len(t["kind"]))
+        idx = idx[1:] if mutate == "drop" else np.concatenate([idx, idx[:1]])
+        res.tasks = {k: np.asarray(v)[idx] for k, v in t.items()}
+        assert not np.all(coverage(O, res, len(q)) == 1), mutate
+    res.tasks = t
+
+
+def test_work_count_scaling(O):
+    # the FMM is O(N) (cell-cell interactions per particle constant), the treecode
+    # O(N log N) (cell-particle evaluations per particle grow with log N). Counts from the
+    # oracle's lists on uniform cubes at a fixed occupancy (ncrit) over a 64x range of N.
+    Ns = [2000, 16000, 128000]
+    fmm_work, tree_work = [], []
+    for n in Ns:
+        xyz, q = make_particles(n, "uniform", 11)
+        r = O.fmm(xyz, q, 1, 0.5, 16, O.FMM)
+        fmm_work.append(np.sum(r.tasks["kind"] == O.K_M2L))
+        r = O.fmm(xyz, q, 1, 0.5, 16, O.TREECODE)
+        rng = O.task_ranges(r)
+        tree_work.append(int(np.sum(rng[rng[:, 0] == O.K_M2P, 2])))  # target particles x cells
+    s_fmm = np.polyfit(np.log(Ns), np.log(fmm_work), 1)[0]
+    s_tree = np.polyfit(np.log(Ns), np.log(tree_work), 1)[0]
+    # per-particle work: the FMM's converges to a constant (its growth at these sizes is the
+    # shrinking share of boundary cells, and its increments per 8x in N shrink); the treecode's
+    # grows like log N (increments per 8x in N do not shrink)
+    f_pp = np.array(fmm_work) / np.array(Ns)
+    t_pp = np.array(tree_work) / np.array(Ns)
+    df, dt = np.diff(f_pp), np.diff(t_pp)
+    assert df[1] < 0.8 * df[0], f_pp
+    assert dt[1] > 0.9 * dt[0], t_pp
+    assert s_tree > s_fmm + 0.15, (s_tree, s_fmm)
+    assert 0.9 < s_fmm < 1.2 and s_tree < 1.5, (s_fmm, s_tree)
