@@ -6,7 +6,9 @@ Timing: CUDA events around fmm_evaluate on resident inputs, L2 flushed before ev
 of `--steps` after 3 warm-ups, the handle auto-tuned on the device. Accuracy in the sweep
 is measured on the GPU against a tighter FMM of the same points (p = 12, theta = 0.3; its own
 error vs the direct sum is pinned by tests/test_gpu_parity.py), on 65,536 sampled particles.
-Usage: config_sweep.py [configs|modes|pladder|sweep|all] [--steps K]
+Also the paper's own GPU experiments as B200 analogs: E7 interaction mix on a spherical
+shell, E10 time vs N of treecode / FMM / hybrid at N_crit = 100, p = 8.
+Usage: config_sweep.py [configs|modes|pladder|sweep|mix|nsweep|paper|all] [--steps K]
 """
 import argparse
 import json
@@ -100,6 +102,35 @@ def main():
     if what in ("pladder", "all"):
         for p in (4, 6, 8, 12):
             run_cfg("C2", p=p)
+    if what in ("mix", "paper", "all"):
+        # E7: spherical shell, N = 1e5, N_crit = 20: interaction mix per mode
+        xyz, q = make_particles(100_000, "shell", 7)
+        X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
+        for mode in ("treecode", "fmm", "hybrid"):
+            f = FMM(p=10, theta=0.4, ncrit=20, mode=mode, tune=False)
+            f.set_deterministic(False)
+            f.tune()
+            ms, s, _, _ = timed(f, X, Q, a.steps, flush)
+            c = s
+            record("E7-shell-mix", "shell", 100_000, mode, 10, 0.4, 20, ms, s, f,
+                   {"mix": {"m2p_per_p2p": c["n_m2p"] / max(1, c["n_p2p"]),
+                            "m2l_per_p2p": c["n_m2l"] / max(1, c["n_p2p"]),
+                            "p2p_per_m2l": c["n_p2p"] / max(1, c["n_m2l"])}})
+            f.close()
+    if what in ("nsweep", "paper", "all"):
+        # E10: time vs N of the three methods at N_crit = 100, p = 8, uniform cube
+        for n in (100_000, 300_000, 1_000_000, 3_000_000, 10_000_000):
+            xyz, q = make_particles(n, "uniform", 10)
+            X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
+            for mode in ("treecode", "fmm", "hybrid"):
+                if mode == "treecode" and n > 3_000_000:
+                    continue
+                f = FMM(p=8, theta=0.4, ncrit=100, mode=mode, tune=False)
+                f.set_deterministic(False)
+                f.tune()
+                ms, s, _, _ = timed(f, X, Q, max(3, a.steps // 2), flush)
+                record("E10-nsweep", "uniform", n, mode, 8, 0.4, 100, ms, s, f)
+                f.close()
     if what in ("sweep", "all"):
         c = CONFIGS["C5"]
         xyz, q = make_particles(c["n"], c["dist"], c["seed"])
