@@ -204,3 +204,47 @@ def test_nccl_transport_world1(tmp_path):
     assert O.rel_l2(phi.cpu().numpy(), ref["phi"]) < 1e-6
     assert O.rel_l2(grad.cpu().numpy(), ref["grad"]) < 1e-6
     assert st["n_global"] == 30000 and st["rank_lo"] == 0 and st["rank_hi"] == 30000
+
+
+def test_dist_nonfinite_fails_on_every_rank():
+    # a NaN on one rank: the non-finite flag travels with the bbox allreduce, so every rank
+    # returns FMM_E_NONFINITE at the same point (no rank is left waiting in a collective), and
+    # the group is usable again afterwards
+    from paper_1108_5815_b200 import FmmError
+
+    R = 3
+    xyz, q = make_particles(9000, "uniform", 3)
+    parts = shards(9000, R, 4)
+    bad = xyz.copy()
+    bad[parts[1][5], 2] = np.nan
+    grp = LocalGroup(R)
+    errs, ok = [None] * R, [None] * R
+
+    def worker(r):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            f = FMM(p=4, theta=0.5, ncrit=16, tune=False, group=(grp, r))
+            f.set_cost_model(*COST)
+            try:
+                f.evaluate(torch.from_numpy(bad[parts[r]]).cuda(), torch.from_numpy(q[parts[r]]).cuda())
+            except FmmError as e:
+                errs[r] = str(e)
+            phi, _ = f.evaluate(torch.from_numpy(xyz[parts[r]]).cuda(), torch.from_numpy(q[parts[r]]).cuda())
+            s.synchronize()
+            ok[r] = phi.cpu().numpy()
+            f.close()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th), "a rank hung"
+    grp.close()
+    assert all(e is not None and "non-finite" in e for e in errs), errs
+    ref = single(xyz, q, 4, 0.5, 16, "hybrid")
+    phi = np.zeros(9000)
+    for r in range(R):
+        phi[parts[r]] = ok[r]
+    assert O.rel_l2(phi, ref["phi"]) < 1e-6
