@@ -120,10 +120,36 @@ def cpu_baseline(cost, p, theta, ncrit, mode_name):
     dt = time.perf_counter() - t
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     return {"value": CPU_SAMPLE_N / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "seconds": dt,
+            "seconds": dt, "single_thread": single_thread_oracle(cost),
             "sample": f"full oracle FMM (FP64, OpenMP) of the {CPU_SAMPLE_N}-particle C2 instance "
                       f"(same seed as the GPU workload (uniform cube, q=1/N, p={p}, theta={theta}, ncrit={ncrit}, "
                       f"{mode_name}, the GPU's measured cost model)"}
+
+
+def single_thread_oracle(cost):
+    """the oracle also on ONE thread (OMP_NUM_THREADS=1, a subprocess): C1 in full
+    and a 62,500-particle instance of the C2 recipe (1/16 of C2, same leaf occupancy)."""
+    code = (
+        "import sys, time, json; sys.path.insert(0, %r)\n"
+        "from fmm_inputs import CONFIGS, make_particles\n"
+        "from oracle import oracle as O\n"
+        "out = {}\n"
+        "c = CONFIGS['C1']; x, q = make_particles(c['n'], c['dist'], c['seed'])\n"
+        "t = time.perf_counter(); O.fmm(x, q, c['p'], c['theta'], c['ncrit'], O.HYBRID, cost=%r, want_structure=False)\n"
+        "out['C1'] = c['n'] / (time.perf_counter() - t)\n"
+        "x, q = make_particles(62500, 'uniform', 2)\n"
+        "t = time.perf_counter(); O.fmm(x, q, 10, 0.4, 64, O.HYBRID, cost=%r, want_structure=False)\n"
+        "out['C2_sample_62500'] = 62500 / (time.perf_counter() - t)\n"
+        "print(json.dumps(out))\n") % (ROOT, tuple(cost), tuple(cost))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           timeout=120)
+        vals = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 -- a reporting extra; never fail the bench on it
+        return {"error": str(e)[:200]}
+    return {"cores": 1, "unit": UNIT, "C1_particles_per_s": vals["C1"],
+            "C2_recipe_62500_particles_per_s": vals["C2_sample_62500"]}
 
 
 def run_reference(args):
