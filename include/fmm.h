@@ -99,8 +99,11 @@ int fmm_destroy(fmm_t h);
 /* Evaluate potential and gradient for n particles.
  *   d_xyz  [3n] float, AoS (x0,y0,z0,x1,...)     d_q [n] float
  *   d_phi  [n]  float (out)                       d_grad [3n] float, AoS (out)
- * n = 0 is a successful no-op. Errors: FMM_E_INVALID, FMM_E_NOT_DEVICE, FMM_E_NONFINITE,
- * FMM_E_CUDA, FMM_E_OOM. */
+ * Ordering: the work runs on the handle's internal streams, after everything already queued on
+ * the handle's stream (fmm_set_stream), and that stream waits for the results; the call also
+ * returns only when they are complete. n = 0 is a successful no-op (on a distributed handle it
+ * still takes part in the collective). Errors: FMM_E_INVALID, FMM_E_NOT_DEVICE, FMM_E_NONFINITE
+ * (outputs untouched), FMM_E_CUDA, FMM_E_OOM, FMM_E_NCCL. */
 int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float *d_phi,
                  float *d_grad);
 
@@ -119,7 +122,8 @@ int fmm_evaluate_ts(fmm_t h, const float *d_xyz_t, int64_t n_t, const float *d_x
 int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, float *h_phi,
                       float *h_grad);
 
-/* Use the caller's stream (a cudaStream_t passed as void*); NULL restores the handle's own. */
+/* The stream the evaluations are ordered with (a cudaStream_t passed as void*); NULL restores the
+ * handle's own. See fmm_evaluate for the ordering guarantees. */
 int fmm_set_stream(fmm_t h, void *stream);
 int fmm_set_mode(fmm_t h, int mode);
 /* 1 = record per-phase CUDA events (small overhead), 0 = off (default). */
@@ -130,11 +134,12 @@ int fmm_set_timing(fmm_t h, int enable);
  * the summation order then varies from run to run (differences at FP32 rounding level). */
 int fmm_set_deterministic(fmm_t h, int enable);
 
-/* Re-run the kernel pre-calculation on this device. */
+/* Re-run the kernel pre-calculation on this device (a single-GPU run on synthetic data).
+ * On a distributed handle it is collective and every rank then holds rank 0's table. */
 int fmm_tune(fmm_t h);
 int fmm_get_cost_model(fmm_t h, fmm_cost_t *out);
 /* Pin the cost model (reproducible lists; the oracle imports the same numbers). in->p must equal
- * the handle's p. */
+ * the handle's p. On distributed handles every rank must pin the same table. */
 int fmm_set_cost_model(fmm_t h, const fmm_cost_t *in);
 int fmm_get_stats(fmm_t h, fmm_stats_t *out);
 
