@@ -76,6 +76,7 @@ struct fmm_ctx {
   // entry and exit) and the near field on `aux` (lowest), so that the latency-bound M2L class sort
   // gets SMs as soon as P2P blocks retire instead of queueing behind the whole P2P grid
   cudaStream_t hi = nullptr;
+  cudaStream_t nf = nullptr;  // the near field (P2P, M2P): lowest priority, its own queue
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_up = nullptr, ev_trav = nullptr, ev_near = nullptr;
   // P2P / M2P run on `aux` after the traversal, overlapping the M2L class preparation and GEMM
@@ -968,9 +969,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   };
   if (h->overlap) {
     CK(cudaEventRecord(h->ev_trav, st));
-    CK(cudaStreamWaitEvent(h->aux, h->ev_trav, 0));
-    if (int rc = near_field(h->aux)) return rc;
-    CK(cudaEventRecord(h->ev_near, h->aux));
+    CK(cudaStreamWaitEvent(h->nf, h->ev_trav, 0));
+    if (int rc = near_field(h->nf)) return rc;
+    CK(cudaEventRecord(h->ev_near, h->nf));
   }
   record(h, EV_M2L_PREP);  // re-recorded after the class sort when there are M2L pairs
   // a10 M2L (writes every cell's local expansion, zero where no M2L)
@@ -1296,7 +1297,10 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
     h->stream = h->own_stream;
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-    if ((e = cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, prio_lo)) != cudaSuccess ||
+    // the upward sweep (aux) feeds the M2L GEMM: as urgent as the main pipeline; the near field
+    // (nf) only has to finish before L2P
+    if ((e = cudaStreamCreateWithPriority(&h->aux, cudaStreamNonBlocking, prio_hi)) != cudaSuccess ||
+        (e = cudaStreamCreateWithPriority(&h->nf, cudaStreamNonBlocking, prio_lo)) != cudaSuccess ||
         (e = cudaStreamCreateWithPriority(&h->hi, cudaStreamNonBlocking, prio_hi)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming)) != cudaSuccess ||
@@ -1381,6 +1385,7 @@ int fmm_destroy(fmm_t h) {
     if (h->ev[i]) cudaEventDestroy(h->ev[i]);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->nf) cudaStreamDestroy(h->nf);
   if (h->hi) cudaStreamDestroy(h->hi);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_out) cudaEventDestroy(h->ev_out);
