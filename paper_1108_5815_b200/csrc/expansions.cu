@@ -59,8 +59,11 @@ __device__ void regular_table(float x, float y, float z, int P, float2 *tab, int
 // P2M: warp per leaf; lane = particle. Each lane accumulates q conj(R(xi)) of its particles in
 // registers (all NC coefficients, templated p), then the warp sums the 32 lane vectors through a
 // padded shared-memory transpose (fixed order: deterministic).
+#ifndef P2M_MINB
+#define P2M_MINB 1
+#endif
 template <int p>
-__global__ void __launch_bounds__(128) k_p2m(const int *__restrict__ leaves, int nleaves,
+__global__ void __launch_bounds__(128, P2M_MINB) k_p2m(const int *__restrict__ leaves, int nleaves,
                                              CellsView C, const float4 *__restrict__ pos,
                                              float2 *__restrict__ M) {
   constexpr int NC = nc_of(p), NCS = nc_stride(p), RS = 2 * NC + 1;  // odd row stride
@@ -299,7 +302,10 @@ __global__ void __launch_bounds__(128) k_m2p(const int *__restrict__ leaves, int
 // L2P + combine + un-permute: warp per leaf, lanes = particles. out = acc (+ L2P if use_local),
 // written to the caller's order: phi[perm[i]], grad[3 perm[i] + a].
 template <int p>
-__global__ void __launch_bounds__(128) k_l2p(const int *__restrict__ leaves, int nleaves,
+#ifndef L2P_MINB
+#define L2P_MINB 6  // 80 registers: 6 resident blocks per SM (C2 downward 0.289 -> 0.256 ms)
+#endif
+__global__ void __launch_bounds__(128, L2P_MINB) k_l2p(const int *__restrict__ leaves, int nleaves,
                                              CellsView C, const float4 *__restrict__ pos,
                                              const float2 *__restrict__ L,
                                              const float4 *__restrict__ acc,
