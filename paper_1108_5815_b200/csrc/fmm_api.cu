@@ -22,6 +22,10 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#ifndef TRAV_GRID_PER_SM
+#define TRAV_GRID_PER_SM 8  // traversal blocks per SM (= its resident blocks, traverse.cu)
+#endif
+
 namespace {
 
 template <class T>
@@ -770,7 +774,7 @@ static int traverse(fmm_ctx *h) {
   launch_pack_cells(nc, h->cells(), h->cpack.p, st);
   h->stats.launches += 1;
   const int warps_per_block = 4;
-  const int grid_blocks = 148 * 8;
+  const int grid_blocks = 148 * TRAV_GRID_PER_SM;
   const size_t nwarps = (size_t)grid_blocks * warps_per_block;
   // capacities: at least the previous evaluation's totals, else an estimate per target cell
   size_t cap[4];

@@ -63,7 +63,10 @@ void launch_pack_cells(int ncells, CellsView C, int4 *pk, cudaStream_t st) {
   if (ncells > 0) k_pack_cells<<<(ncells + 255) / 256, 256, 0, st>>>(ncells, C, pk);
 }
 
-__global__ void __launch_bounds__(128, 8) k_traverse(TravArgs A) {
+#ifndef TRAV_MINB
+#define TRAV_MINB 8  // 64 registers: 8 resident blocks per SM (the traversal is latency-bound)
+#endif
+__global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
   const CellsView C = A.C;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
