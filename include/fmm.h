@@ -21,6 +21,10 @@
  *   - One handle = one CUDA device (the device current at fmm_create) and one stream; a handle is
  *     not thread-safe. Evaluations are stream-ordered and synchronous on return.
  *   - Results are written in the caller's particle order and overwrite the output buffers.
+ *   - Precision: the device arithmetic is FP32. Expansion centres and particle offsets
+ *     from them are formed in FP32, so a cloud whose distance from the origin is large compared
+ *     with its extent loses relative accuracy (e.g. a unit-sized cloud placed at 1e4); callers
+ *     should pass coordinates of the order of the cloud's own size (translate it first).
  */
 #ifndef FMM_B200_H
 #define FMM_B200_H

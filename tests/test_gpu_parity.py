@@ -318,3 +318,24 @@ def test_caller_stream_ordering(handles):
     o = out.cpu().numpy().astype(np.float64)
     from oracle.oracle import rel_l2
     assert rel_l2(o[:, 0], ref_phi) < 1e-6 and rel_l2(o[:, 1:], ref_grad) < 1e-6
+
+
+def test_degenerate_geometries(O, handles):
+    # every particle at one point (zero extent: root side 1, one level-21 leaf over ncrit, all
+    # pairs r = 0), and two tight clusters far apart (deep adaptive tree on both), against the
+    # oracle on the same FP32 input
+    f = handles(5, 0.5, 16, "hybrid")
+    xyz = np.full((300, 3), 0.375, np.float32)
+    q = np.linspace(-1, 1, 300).astype(np.float32)
+    phi, grad = run(f, xyz, q)
+    assert np.all(phi == 0) and np.all(grad == 0)
+    assert f.export_tree()["level"].max() == 21
+    rng = np.random.default_rng(8)
+    a = (0.1 + 1e-5 * rng.random((700, 3))).astype(np.float32)
+    b = (0.9 + 1e-3 * rng.random((900, 3))).astype(np.float32)
+    xyz = np.concatenate([a, b])
+    q = rng.uniform(-1, 1, len(xyz)).astype(np.float32)
+    phi, grad = run(f, xyz, q)
+    ref = O.fmm(xyz, q, 5, 0.5, 16, O.HYBRID, cost=COST)
+    assert np.array_equal(O.canonical_tasks(f.export_lists()), O.canonical_tasks(ref.tasks))
+    assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
