@@ -909,7 +909,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
       h->sh_T_p = p;
     }
     const int ns = h->ncells - 1;
-    S.items_per_level = 16 + h->ncells / 2048;
+    S.items_per_level = tc_shift_items_per_level(h->ncells);
     CK(h->sh_keys_in.ensure(ns));
     CK(h->sh_keys.ensure(ns));
     CK(h->sh_vals_in.ensure(ns));

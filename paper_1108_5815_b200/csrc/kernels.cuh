@@ -149,6 +149,7 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
                           const float2 *M, float *Y, int grid, cudaStream_t st,
                           float *Lacc = nullptr);
 cudaError_t tc_shift_build_ops(int p, unsigned *Tm2m, unsigned *Tl2l, cudaStream_t st);
+int tc_shift_items_per_level(int ncells);  // work-item capacity per level of the shift GEMMs
 size_t tc_shift_sort_bytes(int ncells);
 cudaError_t tc_shift_prepare(int ncells, int depth, const TcShiftWork &S, CellsView C,
                              cudaStream_t st);

@@ -641,7 +641,10 @@ __global__ void k_shift_basis(int p, unsigned *__restrict__ Tm2m, unsigned *__re
 // octant segments: the non-root cells sorted by (level << 3 | octant) give per level 8 contiguous
 // segments; a level's items are chunks of TC_SHIFT_ITEM cells of one segment (class = octant).
 // Output slots are the cell ids themselves (Y holds one row per cell).
-#define TC_SHIFT_ITEM 2048
+#ifndef TC_SHIFT_ITEM
+#define TC_SHIFT_ITEM 256  // children per M2M / L2L work item: enough items to spread a level over the SMs
+#endif
+int tc_shift_items_per_level(int ncells) { return 16 + ncells / TC_SHIFT_ITEM; }
 __global__ void k_shift_keys(int ncells, CellsView C, unsigned *keys, unsigned *vals) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncells - 1) return;
