@@ -22,7 +22,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
-#define M2L_ITEM 2048
+#ifndef M2L_ITEM
+#define M2L_ITEM 4096  // pairs per work item: fewer 128-KiB class-matrix loads; 8192 unbalances C2
+#endif
 #define M2L_PREF 12  // float4 per thread staged for the next chunk (= max over p <= 12 of ceil(Kpad/4*64/threads))
 #define M2L_CHUNK 64
 #define M2L_SMALL 16
