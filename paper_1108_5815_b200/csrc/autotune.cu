@@ -22,3 +22,48 @@ void launch_fill_random(float *dst, int64_t n, unsigned seed, float lo, float hi
   if (b > 148 * 32) b = 148 * 32;
   k_fill_random<<<(int)(b < 1 ? 1 : b), 256, 0, st>>>(dst, n, seed, lo, hi);
 }
+
+// ---- per-device one-time setup (common.cuh) ----------------------------------------------------
+#include <map>
+#include <mutex>
+#include <utility>
+
+static std::mutex g_once_mu;
+
+void fmm_smem_optin(const void *func, size_t bytes) {
+  if (bytes <= 48 * 1024) return;  // the default limit
+  static std::map<std::pair<const void *, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_once_mu);
+  size_t &have = done[{func, dev}];
+  if (have >= bytes) return;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
+      cudaSuccess)
+    have = bytes;
+}
+
+bool fmm_once_per_device(const void *key, bool (*fn)()) {
+  static std::map<std::pair<const void *, int>, bool> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_once_mu);
+  bool &ok = done[{key, dev}];
+  if (!ok) ok = fn();
+  return ok;
+}
+
+int fmm_resident_blocks(const void *func, int threads, size_t smem) {
+  static std::map<std::pair<const void *, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(g_once_mu);
+  int &r = cache[{func, dev}];
+  if (!r) {
+    int per_sm = 0, nsm = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    r = (per_sm > 0 ? per_sm : 1) * nsm;
+  }
+  return r;
+}

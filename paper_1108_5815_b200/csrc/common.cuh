@@ -83,3 +83,14 @@ __device__ __forceinline__ float2 sget(const float2 *A, int n, int m) {
 }
 
 #define CUDA_OK(x) ((x) == cudaSuccess)
+
+// Per-device, thread-safe one-time setup (host side). Function attributes and __constant__
+// tables belong to a device context, so a second handle on another device (or an in-process
+// group thread) must not see a process-wide "already configured" flag.
+// Raise the dynamic shared-memory limit of `func` on the current device to at least `bytes`.
+void fmm_smem_optin(const void *func, size_t bytes);
+// Run `fn` once per (key, current device); `fn` returns whether it succeeded (retried otherwise).
+bool fmm_once_per_device(const void *key, bool (*fn)());
+// Resident blocks per SM x SMs for `func` at `threads` threads and `smem` dynamic bytes on the
+// current device (cached per device).
+int fmm_resident_blocks(const void *func, int threads, size_t smem);

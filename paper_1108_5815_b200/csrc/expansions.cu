@@ -20,15 +20,14 @@
 
 __constant__ short2 c_nm[nc_of(FMM_PMAX)];  // coefficient index -> (n, m) (also used by m2l.cu)
 
-static bool g_nm_ready = false;
-void ensure_nm_table() {
-  if (g_nm_ready) return;
+static bool upload_nm_table() {
   short2 h[nc_of(FMM_PMAX)];
   for (int n = 0; n <= FMM_PMAX; ++n)
     for (int m = 0; m <= n; ++m) h[cidx(n, m)] = make_short2((short)n, (short)m);
-  cudaMemcpyToSymbol(c_nm, h, sizeof(h));
-  g_nm_ready = true;
+  return cudaMemcpyToSymbol(c_nm, h, sizeof(h)) == cudaSuccess;
 }
+// __constant__ memory is per device context: uploaded once per device (thread-safe)
+void ensure_nm_table() { fmm_once_per_device((const void *)&c_nm, upload_nm_table); }
 
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -438,11 +437,7 @@ void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4
   ensure_nm_table();
   FMM_DISPATCH_P(p, ({
     const size_t smem = 4 * 32 * (2 * nc_of(P_) + 1) * sizeof(float);
-    static bool cfg = false;
-    if (!cfg) {
-      cudaFuncSetAttribute(k_p2m<P_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cfg = true;
-    }
+    fmm_smem_optin((const void *)k_p2m<P_>, smem);
     k_p2m<P_><<<warp_grid(nleaves, 4), 128, smem, st>>>(leaves, nleaves, C, pos, M);
   }));
 }

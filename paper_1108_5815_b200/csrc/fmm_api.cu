@@ -151,6 +151,7 @@ struct fmm_ctx {
   int trav_ocap = 2048;  // per-warp list scratch (entries per list), doubled on overflow
   DBuf<unsigned> outA, outB, stack;
   int stack_cap = 2048;
+  int trav_list_est = 256;  // initial list capacity per target cell (entries), before any history
   size_t trav_cap[4] = {0, 0, 0, 0};  // list buffer sizes seen so far (traverse)
   int *d_bk = nullptr;                // device bookkeeping of the traversal (TravArgs::bk)
   int64_t ntask[3] = {0, 0, 0};
@@ -242,6 +243,19 @@ static void record(fmm_ctx *h, int e) {
 static void record_on(fmm_ctx *h, int e, cudaStream_t s) {
   if (h->timing) cudaEventRecord(h->ev[e], s);
 }
+
+// Every C-ABI entry point that touches the device runs on the handle's device and restores the
+// caller's current device on every return path.
+struct DeviceGuard {
+  int prev = -1, dev;
+  explicit DeviceGuard(int d) : dev(d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
 
 static int check_device_ptr(fmm_ctx *h, const void *ptr, const char *name) {
   cudaPointerAttributes a;
@@ -779,7 +793,7 @@ static int traverse(fmm_ctx *h) {
   // capacities: at least the previous evaluation's totals, else an estimate per target cell
   size_t cap[4];
   for (int k = 0; k < 4; ++k) {
-    const size_t est = (size_t)256 * nc + 1024;
+    const size_t est = (size_t)h->trav_list_est * nc + 1024;
     cap[k] = std::max(est, h->trav_cap[k]);
     cap[k] = std::min(cap[k], (size_t)INT32_MAX - 1);
   }
@@ -1324,6 +1338,10 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
       rc = fail(h, FMM_E_OOM, "small device allocations failed");
       break;
     }
+    // test hooks: small initial traversal scratch / list estimates force the overflow-and-retry
+    // paths of traverse() (tests/test_gpu_sanitize.py)
+    if (const char *v = getenv("FMM_TRAV_CAP")) h->stack_cap = h->trav_ocap = std::max(32, atoi(v));
+    if (const char *v = getenv("FMM_TRAV_LIST_EST")) h->trav_list_est = std::max(1, atoi(v));
     const char *no = getenv("FMM_NO_OVERLAP");
     h->overlap = !(no && no[0] && no[0] != '0');
     const char *nt = getenv("FMM_NO_TUNE");
@@ -1339,6 +1357,7 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
 
 int fmm_destroy(fmm_t h) {
   if (!h) return FMM_OK;
+  DeviceGuard dg(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->keys_in.release(); h->keys.release(); h->idx_in.release(); h->perm.release();
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
@@ -1410,9 +1429,7 @@ int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float
     return FMM_OK;
   }
   if (n > 0 && (!d_xyz || !d_q || !d_phi || !d_grad)) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
-  int cur = -1;
-  cudaGetDevice(&cur);
-  if (cur != h->device) cudaSetDevice(h->device);
+  DeviceGuard dg(h->device);
   int rc = FMM_OK;
   if (n > 0) {
     rc = check_device_ptr(h, d_xyz, "xyz");
@@ -1421,7 +1438,6 @@ int fmm_evaluate(fmm_t h, const float *d_xyz, const float *d_q, int64_t n, float
     if (!rc) rc = check_device_ptr(h, d_grad, "grad");
   }
   if (!rc) rc = evaluate_impl(h, d_xyz, d_q, n, d_phi, d_grad);
-  if (cur != h->device && cur >= 0) cudaSetDevice(cur);
   return rc;
 }
 
@@ -1439,9 +1455,7 @@ int fmm_evaluate_ts(fmm_t h, const float *d_xyz_t, int64_t n_t, const float *d_x
     return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
   const int64_t n = n_t + n_s;
   if (n > (int64_t)1 << 28) return fail(h, FMM_E_INVALID, "n_t + n_s = %lld exceeds 2^28", (long long)n);
-  int cur = -1;
-  cudaGetDevice(&cur);
-  if (cur != h->device) cudaSetDevice(h->device);
+  DeviceGuard dg(h->device);
   int rc = check_device_ptr(h, d_xyz_t, "xyz_t");
   if (!rc && n_s > 0) rc = check_device_ptr(h, d_xyz_s, "xyz_s");
   if (!rc && n_s > 0) rc = check_device_ptr(h, d_q_s, "q_s");
@@ -1467,13 +1481,13 @@ int fmm_evaluate_ts(fmm_t h, const float *d_xyz_t, int64_t n_t, const float *d_x
       CK(cudaStreamSynchronize(st));
     }
   }
-  if (cur != h->device && cur >= 0) cudaSetDevice(cur);
   return rc;
 }
 
 int fmm_evaluate_host(fmm_t h, const float *h_xyz, const float *h_q, int64_t n, float *h_phi,
                       float *h_grad) {
   if (!h) return FMM_E_INVALID;
+  DeviceGuard dg(h->device);
   if (n < 0) return fail(h, FMM_E_INVALID, "n < 0");
   if (n == 0 && !h->comm) return FMM_OK;
   if (n > 0 && (!h_xyz || !h_q || !h_phi || !h_grad)) return fail(h, FMM_E_INVALID, "NULL buffer with n > 0");
@@ -1524,6 +1538,7 @@ static int attach_comm(fmm_ctx *h, FmmComm *c);
 
 int fmm_tune(fmm_t h) {
   if (!h) return FMM_E_INVALID;
+  DeviceGuard dg(h->device);
   // the pre-calculation is a single-GPU run on synthetic data; a distributed handle then takes
   // rank 0's table again (collective)
   FmmComm *c = h->comm;
@@ -1559,6 +1574,7 @@ int fmm_get_stats(fmm_t h, fmm_stats_t *out) {
 int fmm_export_tree(fmm_t h, int64_t cap, int32_t *h_level, uint64_t *h_prefix, int64_t *h_begin,
                     int64_t *h_count, int64_t *count_out) {
   if (!h || !count_out) return FMM_E_INVALID;
+  DeviceGuard dg(h->device);
   if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
   const int nc = h->ncells;
   *count_out = nc;
@@ -1580,6 +1596,7 @@ int fmm_export_tree(fmm_t h, int64_t cap, int32_t *h_level, uint64_t *h_prefix, 
 int fmm_export_lists(fmm_t h, int64_t cap, int32_t *h_kind, int32_t *h_tlevel, uint64_t *h_tprefix,
                      int32_t *h_slevel, uint64_t *h_sprefix, int64_t *count_out) {
   if (!h || !count_out) return FMM_E_INVALID;
+  DeviceGuard dg(h->device);
   if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
   const int nc = h->ncells;
   const int64_t total = h->ntask[0] + h->ntask[1] + h->ntask[2];
@@ -1613,6 +1630,7 @@ int fmm_export_lists(fmm_t h, int64_t cap, int32_t *h_kind, int32_t *h_tlevel, u
 int fmm_export_perm(fmm_t h, int64_t cap, int64_t *h_perm, uint64_t *h_keys, double *h_origin3,
                     double *h_L) {
   if (!h) return FMM_E_INVALID;
+  DeviceGuard dg(h->device);
   if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
   if (h->comm) return fail(h, FMM_E_INVALID, "fmm_export_perm: not available on distributed handles");
   const int64_t n = h->last_n;
@@ -1646,6 +1664,7 @@ int fmm_get_partition(fmm_t h, int64_t *lo, int64_t *hi) {
 
 int fmm_partition_indices(fmm_t h, int64_t *d_out, int64_t cap, int64_t *count_out) {
   if (!h || !count_out) return FMM_E_INVALID;
+  DeviceGuard dg(h->device);
   if (!h->have_tree) return fail(h, FMM_E_STATE, "no tree evaluation yet");
   const int cnt = h->part_hi - h->part_lo;
   *count_out = cnt;

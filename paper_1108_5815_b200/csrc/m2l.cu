@@ -696,11 +696,7 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
     cudaMemsetAsync(W.counters + 4, 0, sizeof(int), st);
 #define M2L_GEMM_CASE(PP)                                                                    \
   case PP: {                                                                               \
-    static bool cfg = false;                                                               \
-    if (!cfg && smem > 48 * 1024) {                                                        \
-      cudaFuncSetAttribute(k_m2l_gemm<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      cfg = true;                                                                          \
-    }                                                                                      \
+    fmm_smem_optin((const void *)k_m2l_gemm<PP>, smem);                                    \
     k_m2l_gemm<PP><<<148 * per_sm, nthr, smem, st>>>(W.items, W.counters, W.sidx, W.ssrc, W.Tg, \
                                                     reinterpret_cast<const float *>(M), W.Y, \
                                                     W.counters + 4);                     \
@@ -716,11 +712,7 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
   {
     const int nI = (2 * p + 1) * (2 * p + 1), nM = (p + 1) * (p + 1);
     const size_t smem = (size_t)4 * (nI + nM) * sizeof(float2);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      cudaFuncSetAttribute(k_m2l_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      configured = smem;
-    }
+    fmm_smem_optin((const void *)k_m2l_pairs, smem);
     k_m2l_pairs<<<148 * 4, 128, smem, st>>>(p, W.small, W.counters, W.pair_t, W.src, W.C, M, W.Y,
                                             gemm_done ? 1 : 0,
                                             accum ? reinterpret_cast<float *>(L) : nullptr);

@@ -517,11 +517,7 @@ cudaError_t tc_class_gemm(int p, const int4 *items, const int *counters, int *qu
     const size_t ep_bytes = 4 * 32 * 36 * 4;                                                 \
     const size_t smem_full = (size_t)2 * tc_dim(PP) * tc_dim(PP) * 4 + (size_t)128 * 2 * nc_stride(PP) * 4 + ep_bytes + 128; \
     const size_t smem = Lacc ? smem_full - ep_bytes : smem_full;                             \
-    static bool cfg = false;                                                                 \
-    if (!cfg) {                                                                              \
-      cudaFuncSetAttribute(k_m2l_tc<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_full); \
-      cfg = true;                                                                            \
-    }                                                                                        \
+    fmm_smem_optin((const void *)k_m2l_tc<PP>, smem_full);                                   \
     k_m2l_tc<PP><<<grid, 160, smem, st>>>(items, counters, sidx, ssrc, Timg,                 \
                                          reinterpret_cast<const float *>(M), Y, queue, Lacc); \
   } break;

@@ -379,15 +379,7 @@ __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__r
 
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
                        const float4 *pos, float4 *acc, int *counter, cudaStream_t st) {
-  static int resident = 0;
-  if (!resident) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p2p_leaves, P2P_WARPS * 32, 0);
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    resident = (per_sm > 0 ? per_sm : 1) * nsm;
-  }
+  const int resident = fmm_resident_blocks((const void *)k_p2p_leaves, P2P_WARPS * 32, 0);
   // up to 8 waves of blocks (not a persistent grid): blocks retire continually, so that kernels of
   // a higher-priority stream (the M2L class sort running beside P2P) get SMs early
   const int need = (nleaves + P2P_WARPS - 1) / P2P_WARPS;

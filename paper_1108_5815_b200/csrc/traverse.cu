@@ -77,13 +77,17 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
   int2 *rsc = A.rscratch + (size_t)gw * A.ocap;          // P2P source ranges, parallel to [2]
 
   unsigned long long warp_pp = 0, warp_mp = 0;
+  // An earlier level of this attempt overflowed a warp's scratch or a list buffer: its deferred
+  // lists are incomplete (or were never copied), so this level must not read them. Every target
+  // gets empty lists and the host re-runs the traversal with larger buffers.
+  const bool dead = *(volatile unsigned *)A.overflow != 0u || *(volatile int *)&A.bk[12] != 0;
   for (int k = gw; k < A.nt; k += nw) {
     const int t = A.t0 + k;
     const CellRec rt = load_rec(A.pk, t);
     const int4 gt = rt.g;
     const int tcnt = rt.b.y;
     // outside this rank's target partition, or (distinct target / source sets) no target inside
-    if (!(rt.b.x < A.thi && rt.b.x + tcnt > A.tlo) || (A.tmask && A.tmask[t] == 0)) {
+    if (dead || !(rt.b.x < A.thi && rt.b.x + tcnt > A.tlo) || (A.tmask && A.tmask[t] == 0)) {
       if (lane == 0) {
         for (int c = 0; c < 3; ++c) {
           A.loff[c][t] = 0;
@@ -178,7 +182,15 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
       __syncwarp();
     }
     if (overflow || ovf_out) {  // the host re-runs the traversal with larger scratch
-      if (lane == 0) atomicOr(A.overflow, overflow ? 1u : 2u);
+      if (lane == 0) {
+        atomicOr(A.overflow, overflow ? 1u : 2u);
+        for (int c = 0; c < 3; ++c) {
+          A.loff[c][t] = 0;
+          A.lcnt[c][t] = 0;
+        }
+        A.out_off[t] = 0;  // the children of t must not read a deferred list that was not written
+        A.out_cnt[t] = 0;
+      }
       continue;
     }
     // claim the final space of the four lists (running list sizes, this level's deferred pairs:
@@ -199,8 +211,8 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
         A.loff[c][t] = base[c];
         A.lcnt[c][t] = n[c];
       }
-      A.out_off[t] = base[3];
-      A.out_cnt[t] = n[3];
+      A.out_off[t] = fits ? base[3] : 0;  // not copied: the next level is dead (see `dead`)
+      A.out_cnt[t] = fits ? n[3] : 0;
     }
     if (fits) {
 #pragma unroll

@@ -36,6 +36,21 @@ def test_near_pair_closed_form(O, case):
     assert np.sum(kinds == O.K_M2P) == 0
 
 
+def test_strict_mac_mutation_golden(O):
+    """The golden's strict-MAC count (SPEC S:257 '<' instead of the '<=' reading R5): accept-if-<
+    at theta = 0.5 equals accept-if-<= at theta just below 0.5 on this exact geometry (no pair has
+    (r_t + r_s) / R strictly between the two). It must give the extra face second-neighbour pairs
+    6 (2^L - 2) 4^L = 21,504 at L = 4, i.e. 118,840, and differ from the closed form we pin."""
+    g = json.load(open(os.path.join(GOLD, "near_pair_counts.json")))
+    mut = g["strict_mutation"]
+    base = [c for c in g["cases"] if c["L"] == mut["L"] and c["theta"] == mut["theta"]][0]
+    L = mut["L"]
+    assert mut["near"] == base["near"] + 6 * (2 ** L - 2) * 4 ** L
+    xyz, q = full_grid(L)
+    res = O.fmm(xyz, q, 1, mut["theta"] * (1 - 1e-12), 1, O.FMM)
+    assert np.sum(res.tasks["kind"] == O.K_P2P) == mut["near"] != base["near"]
+
+
 def coverage(O, res, n):
     cov = np.zeros((n, n), np.int32)
     for kind, tb, tc, sb, sc in O.task_ranges(res):

@@ -33,6 +33,20 @@ for dist, n, p, th, nc in cases:
     torch.cuda.synchronize()
     f.close()
 
+# traversal overflow-and-retry paths (stack / list scratch and list buffers far too small, small
+# theta = long lists): the retried traversal must not read past any buffer
+os.environ["FMM_TRAV_CAP"] = "32"
+os.environ["FMM_TRAV_LIST_EST"] = "2"
+xyz, q = make_particles(40000, "plummer", 6)
+f = FMM(p=4, theta=0.15, ncrit=16, tune=False)
+f.set_cost_model(*COST)
+f.set_mode("hybrid")
+phi, grad = f.evaluate(torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda())
+torch.cuda.synchronize()
+print("overflow retry", float(phi.abs().sum()), flush=True)
+f.close()
+del os.environ["FMM_TRAV_CAP"], os.environ["FMM_TRAV_LIST_EST"]
+
 # two in-process ranks (the distributed path: split-bound allreduce, particle and LET exchanges)
 xyz, q = make_particles(6000, "plummer", 9)
 grp = LocalGroup(2)
