@@ -117,6 +117,7 @@ struct fmm_ctx {
   DBuf<int> nch, excl, leafflag, leaves, bnd;
   DBuf<int2> crange;
   DBuf<int4> cpack;  // packed cell records for the traversal
+  DBuf<int4> p2p_desc;  // per target leaf: (begin, count, own P2P list offset, count | ancestor flag)
   std::vector<int> level_off, level_cnt;
   int ncells = 0, nleaves = 0, depth = 0;
   // Morton partition of the targets (multi-GPU); nparts = 1: everything
@@ -871,10 +872,12 @@ static int traverse(fmm_ctx *h) {
       continue;
     }
     if (hb2[12]) {  // a list buffer was too small: grow to what the count passes have seen so far
-      if (attempt > 8) return fail(h, FMM_E_OOM, "interaction lists do not fit");
+      // the counts only cover the levels up to the one that overflowed (later levels are dead):
+      // grow 4x per attempt, at least to what has been seen
+      if (attempt > 16) return fail(h, FMM_E_OOM, "interaction lists do not fit");
       for (int k = 0; k < 4; ++k) {
         const size_t need = (size_t)(k < 3 ? hb2[TRAV_CNT(k)] : 0);
-        cap[k] = std::min((size_t)INT32_MAX - 1, std::max(cap[k] * 2, need + need / 4 + 1024));
+        cap[k] = std::min((size_t)INT32_MAX - 1, std::max(cap[k] * 4, 2 * need + 1024));
       }
       continue;
     }
@@ -974,7 +977,10 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   const int ntl = h->tleaves_n;
   auto near_field = [&](cudaStream_t ns) -> int {
     record_on(h, EV_P2P0, ns);
-    launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p, h->d_small + 12, ns);
+    CK(h->p2p_desc.ensure(std::max(ntl, 1)));
+    launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p, h->d_small + 12,
+                      h->p2p_desc.p, ns);
+    h->stats.launches += 1;  // + the per-leaf descriptor pass
     CKL();
     record_on(h, EV_P2P, ns);
     if (h->ntask[FMM_KIND_M2P] > 0) {
@@ -1363,7 +1369,7 @@ int fmm_destroy(fmm_t h) {
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();
-  h->tleaves.release();
+  h->tleaves.release(); h->p2p_desc.release();
   h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
   h->ntgt.release(); h->ts_stage.release();

@@ -159,8 +159,9 @@ cudaError_t tc_shift_l2l_level(int p, int level, int c0, int nl, const TcShiftWo
                                float *Y, cudaStream_t st);
 
 // ---- p2p.cu ----
+// desc: scratch of nleaves int4 (per-leaf work descriptors built by the launch)
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                       const float4 *pos, float4 *acc, int *counter, cudaStream_t st);
+                       const float4 *pos, float4 *acc, int *counter, int4 *desc, cudaStream_t st);
 void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cudaStream_t st);
 
 // ---- synthetic batches for the kernel pre-calculation (autotune.cu) ----

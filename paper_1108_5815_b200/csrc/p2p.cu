@@ -16,6 +16,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 #ifndef P2P_TILE
 #define P2P_TILE 256  // 16 KiB per warp double buffer; 256 beats 128 by ~2% at C2
 #endif
@@ -27,166 +30,7 @@
 #define P2P_MINB 4  // resident blocks per SM the register budget is sized for
 #endif
 
-__device__ __forceinline__ float rsqrt_approx(float x) {  // MUFU.RSQ, no denormal fix-up
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// Packed f32x2 arithmetic on 64-bit registers (PTX add/mul/fma.rn.f32x2, sm_100+): keeping the
-// pairs in .b64 values makes the register allocator hold them in aligned register pairs, so the
-// compiler emits FADD2/FMUL2/FFMA2 without re-pairing MOVs.
-typedef unsigned long long f2x;
-__device__ __forceinline__ f2x pk(float a, float b) {
-  f2x r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 upk(f2x v) {
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-  return r;
-}
-__device__ __forceinline__ f2x add2(f2x a, f2x b) {
-  f2x d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
-  f2x d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
-  f2x d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-
-// one source against the lane's two targets (tx = -x of the two targets)
-__device__ __forceinline__ void ld_src(const float4 *sp, int j, f2x &xx, f2x &yy, f2x &zz,
-                                       f2x &qq) {
-  const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(sp + 2 * j);
-  const ulonglong2 b = *reinterpret_cast<const ulonglong2 *>(sp + 2 * j + 1);
-  xx = a.x;
-  yy = a.y;
-  zz = b.x;
-  qq = b.y;
-}
-__device__ __forceinline__ void st_src(float4 *sp, int j, float4 v) {
-  sp[2 * j] = make_float4(v.x, v.x, v.y, v.y);
-  sp[2 * j + 1] = make_float4(v.z, v.z, v.w, v.w);
-}
-
-template <bool MASK>
-__device__ __forceinline__ void p2p_pair2(const float4 *sp, int j, const f2x tx, const f2x ty,
-                                          const f2x tz, f2x &ph, f2x &gx, f2x &gy, f2x &gz) {
-  f2x sx, sy, sz, sq;
-  ld_src(sp, j, sx, sy, sz, sq);
-  const f2x dx = add2(sx, tx);
-  const f2x dy = add2(sy, ty);
-  const f2x dz = add2(sz, tz);
-  f2x r2 = mul2(dx, dx);
-  r2 = fma2(dy, dy, r2);
-  r2 = fma2(dz, dz, r2);
-  const float2 r2f = upk(r2);
-  float rx = rsqrt_approx(r2f.x), ry = rsqrt_approx(r2f.y);
-  if (MASK) {
-    rx = r2f.x > 0.f ? rx : 0.f;
-    ry = r2f.y > 0.f ? ry : 0.f;
-  }
-  const f2x ri = pk(rx, ry);
-  const f2x qr = mul2(sq, ri);
-  ph = add2(ph, qr);
-  const f2x qr3 = mul2(qr, mul2(ri, ri));
-  gx = fma2(dx, qr3, gx);
-  gy = fma2(dy, qr3, gy);
-  gz = fma2(dz, qr3, gz);
-}
-
-template <bool MASK>
-__device__ __forceinline__ void p2p_tile2(const float4 *__restrict__ sp, int ns, int h, int S,
-                                          f2x tx, f2x ty, f2x tz, f2x acc[4]) {
-  f2x ph = 0ull, gx = 0ull, gy = 0ull, gz = 0ull;  // +0.0f pairs
-  int j = h;
-  for (; j + 3 * S < ns; j += 4 * S) {
-    p2p_pair2<MASK>(sp, j, tx, ty, tz, ph, gx, gy, gz);
-    p2p_pair2<MASK>(sp, j + S, tx, ty, tz, ph, gx, gy, gz);
-    p2p_pair2<MASK>(sp, j + 2 * S, tx, ty, tz, ph, gx, gy, gz);
-    p2p_pair2<MASK>(sp, j + 3 * S, tx, ty, tz, ph, gx, gy, gz);
-  }
-  for (; j < ns; j += S) p2p_pair2<MASK>(sp, j, tx, ty, tz, ph, gx, gy, gz);
-  acc[0] = add2(acc[0], ph);
-  acc[1] = add2(acc[1], gx);
-  acc[2] = add2(acc[2], gy);
-  acc[3] = add2(acc[3], gz);
-}
-
-// raw-float4 tile variant: source value as the broadcast operand of the packed ops
-template <bool MASK>
-__device__ __forceinline__ void p2p_raw(const float4 sv, const f2x tx, const f2x ty, const f2x tz,
-                                        f2x &ph, f2x &gx, f2x &gy, f2x &gz) {
-  const f2x dx = add2(pk(sv.x, sv.x), tx);
-  const f2x dy = add2(pk(sv.y, sv.y), ty);
-  const f2x dz = add2(pk(sv.z, sv.z), tz);
-  f2x r2 = mul2(dx, dx);
-  r2 = fma2(dy, dy, r2);
-  r2 = fma2(dz, dz, r2);
-  const float2 r2f = upk(r2);
-  float rx = rsqrt_approx(r2f.x), ry = rsqrt_approx(r2f.y);
-  if (MASK) {
-    rx = r2f.x > 0.f ? rx : 0.f;
-    ry = r2f.y > 0.f ? ry : 0.f;
-  }
-  const f2x ri = pk(rx, ry);
-  const f2x qr = mul2(pk(sv.w, sv.w), ri);
-  ph = add2(ph, qr);
-  const f2x qr3 = mul2(qr, mul2(ri, ri));
-  gx = fma2(dx, qr3, gx);
-  gy = fma2(dy, qr3, gy);
-  gz = fma2(dz, qr3, gz);
-}
-
-// S (source slices) is a compile-time constant so the four LDS.128 of an unrolled step use
-// immediate offsets (no IMAD address arithmetic on the FMA pipe)
-template <bool MASK, int S>
-__device__ __forceinline__ void p2p_tile_rawS(const float4 *__restrict__ sp, int ns, int h,
-                                              f2x tx, f2x ty, f2x tz, f2x acc[4]) {
-  f2x ph = 0ull, gx = 0ull, gy = 0ull, gz = 0ull;
-  const float4 *q = sp + h;
-  // q + 3S < sp + ns; clamped so that the bound never lies below the buffer (as a 32-bit shared
-  // address sp + ns - 3S would wrap around when the buffer starts near address 0)
-  const float4 *end4 = ns > 3 * S ? sp + ns - 3 * S : sp;
-  for (; q < end4; q += 4 * S) {
-    const float4 s0 = q[0], s1 = q[S], s2 = q[2 * S], s3 = q[3 * S];
-    p2p_raw<MASK>(s0, tx, ty, tz, ph, gx, gy, gz);
-    p2p_raw<MASK>(s1, tx, ty, tz, ph, gx, gy, gz);
-    p2p_raw<MASK>(s2, tx, ty, tz, ph, gx, gy, gz);
-    p2p_raw<MASK>(s3, tx, ty, tz, ph, gx, gy, gz);
-  }
-  for (; q < sp + ns; q += S) p2p_raw<MASK>(q[0], tx, ty, tz, ph, gx, gy, gz);
-  acc[0] = add2(acc[0], ph);
-  acc[1] = add2(acc[1], gx);
-  acc[2] = add2(acc[2], gy);
-  acc[3] = add2(acc[3], gz);
-}
-template <bool MASK>
-__device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int ns, int h, int S,
-                                             f2x tx, f2x ty, f2x tz, f2x acc[4]) {
-  switch (S) {
-    case 1: p2p_tile_rawS<MASK, 1>(sp, ns, h, tx, ty, tz, acc); break;
-    case 2: p2p_tile_rawS<MASK, 2>(sp, ns, h, tx, ty, tz, acc); break;
-    case 3: p2p_tile_rawS<MASK, 3>(sp, ns, h, tx, ty, tz, acc); break;
-    case 4: p2p_tile_rawS<MASK, 4>(sp, ns, h, tx, ty, tz, acc); break;
-    case 5: p2p_tile_rawS<MASK, 5>(sp, ns, h, tx, ty, tz, acc); break;
-    case 6: p2p_tile_rawS<MASK, 6>(sp, ns, h, tx, ty, tz, acc); break;
-    case 7: p2p_tile_rawS<MASK, 7>(sp, ns, h, tx, ty, tz, acc); break;
-    case 8: p2p_tile_rawS<MASK, 8>(sp, ns, h, tx, ty, tz, acc); break;
-    case 10: p2p_tile_rawS<MASK, 10>(sp, ns, h, tx, ty, tz, acc); break;
-    case 16: p2p_tile_rawS<MASK, 16>(sp, ns, h, tx, ty, tz, acc); break;
-    default: p2p_tile_rawS<MASK, 32>(sp, ns, h, tx, ty, tz, acc); break;
-  }
-}
+#include "p2p_core.cuh"
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -377,8 +221,389 @@ __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__r
   }
 }
 
+
+// ================================================================================================
+// k_p2p_tma — the same pairs, CTA-cooperative and warp-specialised (round 2).
+//
+// One CTA works on one target chunk (<= 64 particles of a leaf) at a time, pulled from the
+// dynamic leaf queue. Warp 4 (the producer) walks the P2P lists of the leaf and its ancestors and
+// streams the source particle ranges -- contiguous in Morton order -- into a ring of P2Q_STAGES
+// shared-memory tiles with one TMA bulk copy (cp.async.bulk ... complete_tx) per range piece,
+// signalling a `full` mbarrier per tile; the leaf itself comes first, in tiles of its own flagged
+// for the r = 0 mask. Warps 0-3 (the consumers) do nothing but the packed-FP32 inner loop: each
+// takes a quarter of every tile (the 2-D lane map of k_p2p_leaves inside the warp: G target
+// pairs x S source slices), releases the tile through an `empty` mbarrier, and at the chunk's
+// last tile the slices and the four warps are reduced in a fixed order (deterministic) and the
+// chunk is written once. Compared with k_p2p_leaves the consumers never walk lists, issue copies
+// or wait on their own loads, so the FMA pipe stays fed.
+// ================================================================================================
+// Tile size and depth measured on the B200 (C2 / C3 / C4 P2P ms, bench.py): 768 x 3 stages
+// 1.33 / 6.84 / 30.1; 512 x 4: 1.31 / 7.01 / 30.6; 384 x 6: 1.39 / 7.85 / 33.4; 2 consumer
+// warps per CTA (384 x 3, 8 CTAs per SM): 1.36 / 7.87 / 32.7; per-lane cp.async instead of TMA
+// bulk copies: 1.37 / 6.84 / 31.4; round-1 k_p2p_leaves: 1.32 / 7.33 / 31.6.
+#ifndef P2Q_TILE
+#define P2Q_TILE 768
+#endif
+#ifndef P2Q_STAGES
+#define P2Q_STAGES 3
+#endif
+#ifndef P2Q_CWARPS
+#define P2Q_CWARPS 4  // consumer warps per CTA (they split every tile)
+#endif
+#define P2Q_THREADS (32 * (P2Q_CWARPS + 1))
+#ifndef P2Q_MINB
+#define P2Q_MINB 4  // 90 registers, 4 CTAs = 16 consumer warps per SM (6 CTAs at 64 registers
+                    // measured slower although tools/p2p_micro's bare loop gains 57% -> 59%)
+#endif
+#ifndef P2Q_CPASYNC
+#define P2Q_CPASYNC 0  // producer copies with per-lane cp.async (1) or one TMA bulk copy per range (0)
+#endif
+#define P2Q_CHUNK 64  // most targets per chunk: 32 lanes x 2 packed targets
+// Ring of reduction buffers. A warp finishes a chunk's reduction before it releases the chunk's
+// last tile, and the producer reopens a stage only after all four warps released it: so when a
+// warp reaches the end of chunk j, every warp has released the tile P2Q_STAGES tiles back, hence
+// finished the reductions of all chunks ending there or earlier. Each chunk has >= 1 tile, so
+// P2Q_STAGES buffers suffice.
+#define P2Q_RED P2Q_STAGES
+#define P2Q_BATCH 8   // leaves per queue atomic
+
+// Targets of the next chunk of a leaf with `rem` targets left. A chunk of k targets keeps
+// k * S(k) of the 64 lane slots busy (S(k) = floor(32 / ceil(k / 2)) source slices), so 33..48
+// targets go as 32 + rest (e.g. 40: 32 at S = 2 and 8 at S = 8 -> 0.625 of the slot-steps of one
+// 40-target chunk at S = 1); from 49 on one chunk costs no more than two.
+__device__ __forceinline__ int p2q_chunk(int rem) {
+  return rem >= 49 ? min(rem, P2Q_CHUNK) : (rem > 32 ? 32 : rem);
+}
+
+enum { QF_FIRST = 1, QF_LAST = 2, QF_MASK = 4, QF_END = 8 };
+
+__device__ __forceinline__ unsigned q_saddr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void q_mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(q_saddr(bar)), "r"(count));
+}
+__device__ __forceinline__ void q_mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(q_saddr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void q_mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(q_saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void q_mbar_wait(unsigned long long *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n Q_WAIT:\n"
+      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra Q_DONE;\n bra Q_WAIT;\n Q_DONE:\n }" ::"r"(q_saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void q_cpasync_arrive(unsigned long long *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(q_saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void q_bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                           unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          q_saddr(dst)),
+      "l"(src), "r"(bytes), "r"(q_saddr(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
+    k_p2p_tma(const int *__restrict__ leaves, int nleaves, CellsView C, ListsView Ls,
+              const float4 *__restrict__ pos, float4 *__restrict__ acc_out, float m1,
+              int *next_leaf, const int4 *__restrict__ desc) {
+  extern __shared__ __align__(128) float4 p2q_dyn[];  // [P2Q_STAGES][P2Q_TILE] source tiles
+  float4(*tile)[P2Q_TILE] = reinterpret_cast<float4(*)[P2Q_TILE]>(p2q_dyn);
+  __shared__ int4 meta[P2Q_STAGES];  // (leaf begin, count, flags, chunk start | size << 16)
+  __shared__ __align__(8) unsigned long long full[P2Q_STAGES], empty[P2Q_STAGES];
+  __shared__ __align__(16) float4 red[P2Q_RED][P2Q_CWARPS][P2Q_CHUNK];
+  __shared__ int red_cnt[P2Q_RED];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < P2Q_RED; ++b) red_cnt[b] = 0;
+    for (int s = 0; s < P2Q_STAGES; ++s) {
+      q_mbar_init(&full[s], P2Q_CPASYNC ? 33 : 1);  // (32 producer lanes' copies +) the meta
+      q_mbar_init(&empty[s], P2Q_CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == P2Q_CWARPS) {
+    // ------------------------------------------------------------------ producer warp
+    unsigned k = 0;     // tiles opened so far (tile k uses stage k % P2Q_STAGES)
+    int fill = 0;       // sources in the open tile
+    bool open = false;
+    int flags_pending = 0;
+    auto open_tile = [&]() {
+      if (k >= P2Q_STAGES) q_mbar_wait(&empty[k % P2Q_STAGES], ((k / P2Q_STAGES) + 1) & 1);
+      fill = 0;
+      open = true;
+    };
+    auto close_tile = [&](int leaf, int flags, int c0) {
+#if P2Q_CPASYNC
+      q_cpasync_arrive(&full[k % P2Q_STAGES]);  // fires when this lane's copies have landed
+#endif
+      __syncwarp();  // every lane's expect_tx precedes the arrive
+      if (lane == 0) {
+        meta[k % P2Q_STAGES] = make_int4(leaf, fill, flags, c0);
+        q_mbar_arrive(&full[k % P2Q_STAGES]);
+      }
+      __syncwarp();
+      ++k;
+      open = false;
+    };
+    // lanes hold one particle range each (cnt = 0: none); append them in lane order
+    auto emit = [&](int beg, int cnt, int leaf, int c0, bool self = false) {
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const int lo = incl - cnt;
+      int done = 0;
+      while (done < total) {
+        if (!open) open_tile();
+        const int take = min(P2Q_TILE - fill, total - done);
+        const int a = max(lo, done), e = min(lo + cnt, done + take);
+#if P2Q_CPASYNC
+        // each lane copies its own range piece, 16 B per cp.async (LDGSTS); completion is tracked
+        // by the lanes' cp.async.mbarrier.arrive at close_tile
+        {
+          float4 *dst = &tile[k % P2Q_STAGES][fill - done];
+          const float4 *src = pos + beg - lo;
+          for (int x = a; x < e; ++x) cp_async16(dst + x, src + x);
+        }
+#else
+        if (a < e) {  // one TMA bulk copy per range piece
+          unsigned long long *fb = &full[k % P2Q_STAGES];
+          q_mbar_expect_tx(fb, (unsigned)(e - a) * 16u);
+          q_bulk_g2s(&tile[k % P2Q_STAGES][fill + (a - done)], pos + beg + (a - lo),
+                     (unsigned)(e - a) * 16u, fb);
+        }
+#endif
+        fill += take;
+        done += take;
+        if (fill == P2Q_TILE) {
+          close_tile(leaf, flags_pending, c0);
+          // the next tile holds no own particle once the leaf's own range has been emitted
+          flags_pending &= self ? ~QF_FIRST : ~(QF_FIRST | QF_MASK);
+        }
+      }
+    };
+    auto emit_rng = [&](int2 r, int tb, int cw) { emit(r.x, r.y, tb, cw); };
+    // Leaves in batches of P2Q_BATCH per queue atomic; lane j holds the descriptor of leaf j of
+    // the batch. Every global load is issued one step ahead of its use so that the producer does
+    // not stall the ring on L2 latency: the next batch is claimed (and its descriptors loaded)
+    // while this one is emitted, the next leaf's first 32 source ranges are loaded while this
+    // leaf is emitted, and range batch e0 + 32 while batch e0 is emitted.
+    auto claim = [&](int &bb, int &nb) {
+      int bs = 1;
+      if (lane == 0) {  // guided: P2Q_BATCH leaves while many remain, single leaves for the tail
+        const int seen = *(volatile int *)next_leaf;
+        bs = nleaves - seen > 4 * P2Q_BATCH * (int)gridDim.x ? P2Q_BATCH : 1;
+        bb = atomicAdd(next_leaf, bs);
+      }
+      bb = __shfl_sync(0xffffffffu, bb, 0);
+      bs = __shfl_sync(0xffffffffu, bs, 0);
+      nb = bb < nleaves ? min(bs, nleaves - bb) : 0;
+    };
+    auto lane_desc = [&](int4 d, int j) {
+      return make_int4(__shfl_sync(0xffffffffu, d.x, j), __shfl_sync(0xffffffffu, d.y, j),
+                       __shfl_sync(0xffffffffu, d.z, j), __shfl_sync(0xffffffffu, d.w, j));
+    };
+    auto load_rng = [&](int off, int ncell, int e0) {
+      return e0 + lane < ncell ? Ls.p2p_rng[off + e0 + lane] : make_int2(0, 0);
+    };
+    int b0 = 0, nb0 = 0, b1 = 0, nb1 = 0;
+    claim(b0, nb0);
+    int4 dl0 = lane < nb0 ? desc[b0 + lane] : make_int4(0, 0, 0, 0);
+    claim(b1, nb1);
+    int4 dl1 = lane < nb1 ? desc[b1 + lane] : make_int4(0, 0, 0, 0);
+    int2 rfirst = make_int2(0, 0);  // first range batch of the current leaf (prefetched)
+    if (nb0 > 0) {
+      const int4 d = lane_desc(dl0, 0);
+      rfirst = load_rng(d.z, d.w & 0x7fffffff, 0);
+    }
+    while (nb0 > 0) {
+      for (int j = 0; j < nb0; ++j) {
+        const int4 d = lane_desc(dl0, j);
+        const int4 dn = j + 1 < nb0 ? lane_desc(dl0, j + 1)
+                                    : (nb1 > 0 ? lane_desc(dl1, 0) : make_int4(0, 0, 0, 0));
+        const int tb = d.x, tn = d.y, off = d.z, ncell = d.w & 0x7fffffff;
+        const bool anc = d.w < 0;
+        int2 rnext_leaf = make_int2(0, 0);
+        for (int c0 = 0, nt = 0; c0 < tn; c0 += nt) {
+          nt = p2q_chunk(tn - c0);
+          const bool last_chunk = c0 + nt >= tn;
+          const int cw = c0 | (nt << 16);  // chunk start | chunk size
+          int2 r = c0 == 0 ? rfirst : load_rng(off, ncell, 0);
+          if (last_chunk) rnext_leaf = load_rng(dn.z, dn.w & 0x7fffffff, 0);
+          // (1) the leaf itself first: the chunk's first tile starts with the leaf's own
+          // particles (the consumers read their targets there) and is evaluated with the r = 0
+          // mask, like every tile that holds own particles
+          flags_pending = QF_FIRST | QF_MASK;
+          emit(tb, lane == 0 ? tn : 0, tb, cw, true);
+          if (!open) flags_pending &= ~QF_MASK;  // the own range ended on a tile boundary
+          // (2) the leaf's P2P list, then (rare) those of its ancestors: a P2P pair with a
+          // non-leaf target applies to every particle under it
+          for (int e0 = 0; e0 < ncell; e0 += 32) {
+            const int2 rn = e0 + 32 < ncell ? load_rng(off, ncell, e0 + 32) : make_int2(0, 0);
+            if (r.x == tb) r.y = 0;  // the leaf itself: done above, masked
+            emit(r.x, r.y, tb, cw);
+            r = rn;
+          }
+          if (anc) {
+            for (int a = C.parent[leaves[b0 + j]]; a >= 0; a = C.parent[a]) {
+              const int aoff = Ls.off[2][a], an = Ls.cnt[2][a];
+              for (int e0 = 0; e0 < an; e0 += 32) emit_rng(load_rng(aoff, an, e0), tb, cw);
+            }
+          }
+          if (!open) open_tile();  // the chunk's last tile (possibly empty) carries QF_LAST
+          close_tile(tb, flags_pending | QF_LAST, cw);
+        }
+        rfirst = rnext_leaf;
+      }
+      b0 = b1;
+      nb0 = nb1;
+      dl0 = dl1;
+      if (nb0 > 0) {
+        claim(b1, nb1);
+        dl1 = lane < nb1 ? desc[b1 + lane] : make_int4(0, 0, 0, 0);
+      } else {
+        nb1 = 0;
+      }
+    }
+    open_tile();
+    close_tile(-1, QF_END, 0);
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumer warps 0..3
+  unsigned k = 0, chunk = 0;
+  f2x tx = 0ull, ty = 0ull, tz = 0ull;
+  f2x acc[4] = {0ull, 0ull, 0ull, 0ull};
+  int G = 1, S = 1, grp = 0, h = 0, nt = 0, tb = 0, c0 = 0;
+  bool active = false;
+  for (;;) {
+    const int st = k % P2Q_STAGES;
+    q_mbar_wait(&full[st], (k / P2Q_STAGES) & 1);
+    const int4 m = meta[st];
+    if (m.z & QF_END) break;
+    if (m.z & QF_FIRST) {
+      tb = m.x;
+      c0 = m.w & 0xffff;
+      nt = m.w >> 16;
+      G = (nt + 1) >> 1;
+      S = 32 / G;
+      grp = lane % G;
+      h = lane / G;
+      active = h < S;
+      const int i0 = c0 + 2 * grp, i1 = i0 + 1;
+      // the targets are particles c0.. of the leaf, i.e. of this (first, masked) tile when the
+      // whole leaf fits in one tile
+      const float4 *src = m.y > c0 + nt - 1 ? tile[st] : pos + tb;
+      const float4 t0 = 2 * grp < nt ? src[i0] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 t1 = 2 * grp + 1 < nt ? src[i1] : t0;
+      tx = pk(m1 * t0.x, m1 * t1.x);
+      ty = pk(m1 * t0.y, m1 * t1.y);
+      tz = pk(m1 * t0.z, m1 * t1.z);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = 0ull;
+    }
+    // this warp's quarter of the tile
+    const int n = m.y;
+    const int a = (warp * n) / P2Q_CWARPS, e = ((warp + 1) * n) / P2Q_CWARPS;
+    if (m.z & QF_MASK)
+      p2p_tile_raw<true>(tile[st] + a, active ? e - a : 0, h, S, tx, ty, tz, acc);
+    else
+      p2p_tile_raw<false>(tile[st] + a, active ? e - a : 0, h, S, tx, ty, tz, acc);
+    ++k;
+    if (!(m.z & QF_LAST)) {
+      __syncwarp();
+      if (lane == 0) q_mbar_arrive(&empty[st]);
+    } else {
+      // slices of this warp in slice order; the last of the four warps to finish sums the warps
+      // in warp order and writes the chunk (deterministic, and nobody waits at a barrier)
+      float2 r[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) r[c] = upk(acc[c]);
+      float2 tot[4] = {r[0], r[1], r[2], r[3]};
+      for (int sl = 1; sl < S; ++sl) {
+        const int from = grp + sl * G;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          tot[c].x += __shfl_sync(0xffffffffu, r[c].x, from);
+          tot[c].y += __shfl_sync(0xffffffffu, r[c].y, from);
+        }
+      }
+      const int b = chunk % P2Q_RED;
+      ++chunk;
+      if (h == 0) {
+        if (2 * grp < nt) red[b][warp][2 * grp] = make_float4(tot[0].x, tot[1].x, tot[2].x, tot[3].x);
+        if (2 * grp + 1 < nt)
+          red[b][warp][2 * grp + 1] = make_float4(tot[0].y, tot[1].y, tot[2].y, tot[3].y);
+      }
+      __threadfence_block();
+      __syncwarp();
+      int prev = 0;
+      if (lane == 0) prev = atomicAdd(&red_cnt[b], 1);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == P2Q_CWARPS - 1) {
+        __threadfence_block();
+        for (int i = lane; i < nt; i += 32) {
+          float4 v = red[b][0][i];
+#pragma unroll
+          for (int w = 1; w < P2Q_CWARPS; ++w) {
+            const float4 u = red[b][w][i];
+            v.x += u.x;
+            v.y += u.y;
+            v.z += u.z;
+            v.w += u.w;
+          }
+          acc_out[tb + c0 + i] = v;
+        }
+        __syncwarp();
+        if (lane == 0) red_cnt[b] = 0;
+      }
+      __syncwarp();
+      if (lane == 0) q_mbar_arrive(&empty[st]);  // after the reduction (see P2Q_RED)
+    }
+  }
+}
+
+// per target leaf: (begin, count, own P2P list offset, own list count | 1 << 31 when a proper
+// ancestor has a non-empty P2P list)
+__global__ void k_p2p_desc(const int *__restrict__ leaves, int nleaves, CellsView C, ListsView Ls,
+                           int4 *__restrict__ desc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nleaves) return;
+  const int leaf = leaves[i];
+  bool anc = false;
+  for (int a = C.parent[leaf]; a >= 0 && !anc; a = C.parent[a]) anc = Ls.cnt[2][a] > 0;
+  desc[i] = make_int4(C.beg[leaf], C.cnt[leaf], Ls.off[2][leaf],
+                      Ls.cnt[2][leaf] | (anc ? (int)0x80000000u : 0));
+}
+
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                       const float4 *pos, float4 *acc, int *counter, cudaStream_t st) {
+                       const float4 *pos, float4 *acc, int *counter, int4 *desc, cudaStream_t st) {
+  static const bool legacy = getenv("FMM_P2P_LEGACY") != nullptr;  // A/B: round-1 kernel
+  if (!legacy) {
+    const size_t dyn = sizeof(float4) * P2Q_STAGES * P2Q_TILE;
+    fmm_smem_optin((const void *)k_p2p_tma, dyn);
+    const int res = fmm_resident_blocks((const void *)k_p2p_tma, P2Q_THREADS, dyn);
+    if (nleaves <= 0) return;
+    k_p2p_desc<<<(nleaves + 255) / 256, 256, 0, st>>>(leaves, nleaves, C, Ls, desc);
+    const int b = std::max(1, std::min(res, (nleaves + P2Q_BATCH - 1) / P2Q_BATCH));
+    cudaMemsetAsync(counter, 0, sizeof(int), st);
+    k_p2p_tma<<<b, P2Q_THREADS, dyn, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f, counter, desc);
+    return;
+  }
   const int resident = fmm_resident_blocks((const void *)k_p2p_leaves, P2P_WARPS * 32, 0);
   // up to 8 waves of blocks (not a persistent grid): blocks retire continually, so that kernels of
   // a higher-priority stream (the M2L class sort running beside P2P) get SMs early

@@ -45,7 +45,9 @@ def test_binary_is_sm100a_cuda_core_code(libpath):
         funcs[chunk.split()[0]] = chunk
     m2l = [v for k, v in funcs.items() if "k_m2l_gemm" in k]
     assert m2l and "FFMA2" in m2l[0]  # packed FP32 FMA on the M2L hot loop
-    assert "MUFU.RSQ" in [v for k, v in funcs.items() if "p2p" in k][0]
+    p2p = [v for k, v in funcs.items() if "k_p2p_tma" in k]
+    assert p2p and "MUFU.RSQ" in p2p[0] and "FFMA2" in p2p[0]
+    assert "UBLKCP" in p2p[0]  # the producer warp's TMA bulk copies of the source ranges
 
 
 def test_strerror_without_gpu(libpath):
