@@ -127,6 +127,7 @@ struct fmm_ctx {
   // expansions
   DBuf<float2> M, L;
   // M2L class batching
+  DBuf<uint2> m2l_pst;
   DBuf<int> m2l_pair_t, m2l_flag, m2l_cid, m2l_cstart, m2l_counters;
   DBuf<unsigned> m2l_keys_in, m2l_keys;
   DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep, m2l_ssrc, m2l_stgt;
@@ -798,7 +799,8 @@ static int traverse(fmm_ctx *h) {
     cap[k] = std::max(est, h->trav_cap[k]);
     cap[k] = std::min(cap[k], (size_t)INT32_MAX - 1);
   }
-  for (int attempt = 0;; ++attempt) {
+  int list_attempts = 0;  // (scratch overflows are bounded by the 8 GiB check instead)
+  for (;;) {
     CK(h->stack.ensure(nwarps * h->stack_cap));
     CK(h->trav_osc.ensure(nwarps * 4 * (size_t)h->trav_ocap));
     CK(h->trav_rsc.ensure(nwarps * (size_t)h->trav_ocap));
@@ -874,7 +876,7 @@ static int traverse(fmm_ctx *h) {
     if (hb2[12]) {  // a list buffer was too small: grow to what the count passes have seen so far
       // the counts only cover the levels up to the one that overflowed (later levels are dead):
       // grow 4x per attempt, at least to what has been seen
-      if (attempt > 16) return fail(h, FMM_E_OOM, "interaction lists do not fit");
+      if (++list_attempts > 16) return fail(h, FMM_E_OOM, "interaction lists do not fit");
       for (int k = 0; k < 4; ++k) {
         const size_t need = (size_t)(k < 3 ? hb2[TRAV_CNT(k)] : 0);
         cap[k] = std::min((size_t)INT32_MAX - 1, std::max(cap[k] * 4, 2 * need + 1024));
@@ -1003,6 +1005,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   if (far_local) {
     const int np = (int)h->ntask[FMM_KIND_M2L];
     CK(h->m2l_pair_t.ensure(np));
+    CK(h->m2l_pst.ensure(np));
     CK(h->m2l_keys_in.ensure(np));
     CK(h->m2l_keys.ensure(np));
     CK(h->m2l_idx_in.ensure(np));
@@ -1025,6 +1028,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     W.cnt = h->lcnt[0].p;
     W.src = h->lsrc[0].p;
     W.pair_t = h->m2l_pair_t.p;
+    W.pst = h->m2l_pst.p;
     W.keys_in = h->m2l_keys_in.p;
     W.keys = h->m2l_keys.p;
     W.idx_in = h->m2l_idx_in.p;
@@ -1373,7 +1377,7 @@ int fmm_destroy(fmm_t h) {
   h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
   h->ntgt.release(); h->ts_stage.release();
-  h->m2l_pair_t.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
+  h->m2l_pair_t.release(); h->m2l_pst.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
   h->m2l_items_raw.release(); h->m2l_rflag.release(); h->m2l_rid.release(); h->m2l_rstart.release();

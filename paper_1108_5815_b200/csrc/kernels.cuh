@@ -97,6 +97,7 @@ struct M2LWork {
   const int *off, *cnt;     // per target cell: M2L list segment
   const unsigned *src;      // source cell of each pair
   int *pair_t;              // target cell of each pair
+  uint2 *pst;               // (source, target) of each pair, list order
   unsigned *keys_in, *keys;  // 24-bit class keys
   unsigned *idx_in, *sidx;  // pair indices sorted by class key
   unsigned *ssrc;           // source cell of each class-sorted pair

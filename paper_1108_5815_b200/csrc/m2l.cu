@@ -121,10 +121,13 @@ __global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
 __device__ __forceinline__ unsigned cell_block(int4 g, int bl);
 __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
                           const unsigned *__restrict__ src, CellsView C, int bl,
-                          unsigned *__restrict__ keys, unsigned *__restrict__ idx) {
+                          unsigned *__restrict__ keys, unsigned *__restrict__ idx,
+                          uint2 *__restrict__ pst) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
     const unsigned s = src[e];
-    const int4 gt = C.grid[pair_t[e]], gs = C.grid[s];
+    const int t = pair_t[e];
+    pst[e] = make_uint2(s, (unsigned)t);  // one 8-byte record for the class-sorted gather
+    const int4 gt = C.grid[t], gs = C.grid[s];
     const int dl = gt.w - gs.w;
     const int sh = FMM_LEVELS - max(gt.w, gs.w);
     const int dx = (gt.x - gs.x) >> sh, dy = (gt.y - gs.y) >> sh, dz = (gt.z - gs.z) >> sh;
@@ -157,15 +160,18 @@ __device__ __forceinline__ unsigned cell_block(int4 g, int bl) {
 // split where the target's spatial block changes)
 __global__ void k_m2l_class_flags(int npairs, const unsigned *__restrict__ skeys,
                                   const unsigned *__restrict__ sidx,
-                                  const unsigned *__restrict__ src, int *__restrict__ flag,
-                                  unsigned *__restrict__ ssrc, const int *__restrict__ pair_t,
-                                  unsigned *__restrict__ stgt, int bl, int *__restrict__ rflag) {
+                                  const uint2 *__restrict__ pst, int *__restrict__ flag,
+                                  unsigned *__restrict__ ssrc, unsigned *__restrict__ stgt, int bl,
+                                  int *__restrict__ rflag) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
     const unsigned k = skeys[i], cls = k >> (3 * bl);
     const int f = (i == 0 || cls != (skeys[i - 1] >> (3 * bl)) || cls == M2L_KEY_OWN) ? 1 : 0;
     flag[i] = f;
-    ssrc[i] = src[sidx[i]];  // source cell in class-sorted order (one coalesced load later)
-    if (stgt) stgt[i] = (unsigned)pair_t[sidx[i]];
+    // source and target cell in class-sorted order (one random 8-byte load per pair; later
+    // kernels read these arrays coalesced)
+    const uint2 st = pst[sidx[i]];
+    ssrc[i] = st.x;
+    if (stgt) stgt[i] = st.y;
     rflag[i] = f || k != skeys[i - 1];
   }
 }
@@ -620,7 +626,7 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   k_m2l_pair_targets<<<148 * 8, 128, 0, st>>>(ncells, W.off, W.cnt, W.pair_t);
   const int b = (npairs + 255) / 256 < 148 * 16 ? (npairs + 255) / 256 : 148 * 16;
   k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.blk_level, W.keys_in,
-                                            W.idx_in);
+                                            W.idx_in, W.pst);
   const int kbits = M2L_KEY_BITS + 3 * W.blk_level;
   size_t bytes = 0;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, W.idx_in,
@@ -630,8 +636,8 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
                                       kbits, st);
   if (e) return e;
-  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.src, W.flag, W.ssrc,
-                                                    W.pair_t, W.stgt, W.blk_level, W.rflag);
+  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.pst, W.flag, W.ssrc,
+                                                    W.stgt, W.blk_level, W.rflag);
   bytes = 0;
   e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, W.flag, W.cid, npairs, st);
   if (e) return e;
