@@ -89,6 +89,10 @@ typedef struct {
   int64_t let_cells, let_particles; /* remote multipoles / particles received (local essential tree) */
   int64_t bytes_sent;               /* bytes this rank sent in all exchanges of the evaluation */
   double ms_comm;                   /* host wall time inside collectives (includes waiting) */
+  /* sender-side local essential tree (default on distributed handles; timing enabled): device
+   * time of the exchange on its own stream, and how far it ran past the end of the traversal it
+   * overlaps (0 = hidden; the near field and M2L wait for it) */
+  double ms_let, ms_let_exposed;
 } fmm_stats_t;
 
 /* Create a handle on the current CUDA device. p = expansion order (coefficients n = 0..p,

@@ -65,7 +65,8 @@ struct DBuf {
   }
 };
 
-enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L_PREP, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_P2P0, EV_N };
+enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L_PREP, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_P2P0,
+       EV_LET0, EV_LET1, EV_TRAV_END, EV_N };
 
 }  // namespace
 
@@ -117,7 +118,21 @@ struct fmm_ctx {
   DBuf<int> nch, excl, leafflag, leaves, bnd;
   DBuf<int2> crange;
   DBuf<int4> cpack;  // packed cell records for the traversal
-  DBuf<int4> p2p_desc;  // per target leaf: (begin, count, own P2P list offset, count | ancestor flag)
+  DBuf<int4> p2p_desc;
+  // sender-side local essential tree (let_send): flags, compacted entries, send / receive buffers
+  cudaStream_t cmst = nullptr;  // its stream (the exchange overlaps the traversal)
+  cudaEvent_t ev_let = nullptr;
+  bool let_recv = false;        // FMM_LET=recv: the round-1 receiver-driven exchange after the traversal
+  bool let_check = false;       // FMM_LET_CHECK=1: verify that every remote source named was received
+  DBuf<int> let_box, let_flags, let_excl, let_cnt, let_psize, let_pexcl, let_seg0, let_haveM, let_haveP;
+  DBuf<unsigned> let_open, let_ids, let_rids;
+  DBuf<int2> let_prng;
+  DBuf<int4> let_prec, let_rrec;
+  DBuf<float2> let_rows_s, let_rows_r;
+  DBuf<float4> let_pbuf_s, let_pbuf_r;
+  DBuf<int> let_missing;
+  void *let_tmp = nullptr;
+  size_t let_tmp_cap = 0;  // per target leaf: (begin, count, own P2P list offset, count | ancestor flag)
   std::vector<int> level_off, level_cnt;
   int ncells = 0, nleaves = 0, depth = 0;
   // Morton partition of the targets (multi-GPU); nparts = 1: everything
@@ -433,9 +448,9 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
 
 // recv[r * k + j] = item j of what peer r sends to this rank (send[r * k + j] = item j for peer r)
 static int exchange_counts(fmm_ctx *h, const std::vector<int64_t> &send,
-                           std::vector<int64_t> &recv, int k) {
+                           std::vector<int64_t> &recv, int k, cudaStream_t st = nullptr) {
   const int R = h->comm->nranks, me = h->comm->rank;
-  cudaStream_t st = h->stream;
+  if (!st) st = h->stream;
   const size_t blk = (size_t)R * k;
   CK(h->d_i64.ensure(blk * (R + 1)));
   CK(cudaMemcpyAsync(h->d_i64.p, send.data(), sizeof(int64_t) * blk, cudaMemcpyHostToDevice, st));
@@ -451,7 +466,8 @@ static int exchange_counts(fmm_ctx *h, const std::vector<int64_t> &send,
 
 // alltoallv of elements of `elem` bytes; counts per peer taken from column `col` of k-wide rows
 static int a2av(fmm_ctx *h, const void *send, const std::vector<int64_t> &scnt, void *recv,
-                const std::vector<int64_t> &rcnt, size_t elem, int k = 1, int col = 0) {
+                const std::vector<int64_t> &rcnt, size_t elem, int k = 1, int col = 0,
+                cudaStream_t st = nullptr) {
   const int R = h->comm->nranks, me = h->comm->rank;
   std::vector<size_t> sc(R), sd(R), rc(R), rd(R);
   size_t so = 0, ro = 0;
@@ -464,7 +480,7 @@ static int a2av(fmm_ctx *h, const void *send, const std::vector<int64_t> &scnt, 
     ro += rc[r];
   }
   h->stats.bytes_sent += (int64_t)(so - sc[me]);
-  CC(h->comm->alltoallv(send, sc.data(), sd.data(), recv, rc.data(), rd.data(), h->stream));
+  CC(h->comm->alltoallv(send, sc.data(), sd.data(), recv, rc.data(), rd.data(), st ? st : h->stream));
   return FMM_OK;
 }
 
@@ -756,6 +772,187 @@ static int dist_let(fmm_ctx *h) {
   return FMM_OK;
 }
 
+
+// Sender-side local essential tree (NEXT-3: "The MPI
+// communication is overlapped with the kernel evaluations"). Runs on its own stream right after
+// the upward sweep, while the main stream traverses: every rank decides from the global skeleton
+// what each other rank's traversal can read from it (dist.cu k_let_open / k_let_flags, a
+// conservative superset of what the receiver-driven dist_let requests) and sends it unasked --
+// no request round trip, and nothing waits for the traversal. The host blocks only on this
+// stream's small count read-backs, after the traversal has been queued.
+static int let_send(fmm_ctx *h) {
+  FmmComm *cm = h->comm;
+  const int R = cm->nranks, me = cm->rank, nc = h->ncells, N = (int)h->n_glob;
+  const int NCS = nc_stride(h->p);
+  if (!h->cmst) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    CK(cudaStreamCreateWithPriority(&h->cmst, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&h->ev_let, cudaEventDisableTiming));
+  }
+  cudaStream_t cs = h->cmst;
+  record_on(h, EV_LET0, cs);
+  CK(cudaStreamWaitEvent(cs, h->ev_up, 0));  // own multipoles complete (P2M + M2M)
+  // straddling cells: sum the per-rank partial multipoles (M2M is linear)
+  if (h->nstrad > 0) {
+    CK(h->rows_s.ensure((size_t)h->nstrad * NCS));
+    launch_rows(h->M.p, h->rows_s.p, NCS, h->strad_ids.p, h->nstrad, false, cs);
+    CKL();
+    CC(cm->allreduce(h->rows_s.p, (size_t)h->nstrad * NCS * 2, CT_F32, CO_SUM, cs));
+    launch_rows(h->rows_s.p, h->M.p, NCS, h->strad_ids.p, h->nstrad, true, cs);
+    CKL();
+  }
+  // what each receiver can touch: flags[(kind * R + r) * nc + c], kind 0 multipole, 1 particles
+  const size_t nf = (size_t)2 * R * nc;
+  CK(h->let_box.ensure((size_t)let_box_ints(R)));
+  CK(h->let_open.ensure((size_t)2 * nc));
+  CK(h->let_flags.ensure(nf));
+  CK(h->let_excl.ensure(nf));
+  CK(h->let_cnt.ensure((size_t)2 * R + 2));
+  // an accepted pair can be P2P only in hybrid mode (cost model, see k_let_flags), and only with a
+  // target of at most t_ml / t_pp particles
+  const double tpp = h->mode == FMM_HYBRID ? h->cost.t_pp : 0.0;
+  const int kmax = tpp > 0 ? (int)std::min(2e9, h->cost.t_ml / tpp + 1.0) : 0;
+  launch_let_boxes(h->leaves.p, h->nleaves, nc, h->cells(), h->d_off.p, R, kmax, h->let_box.p, cs);
+  launch_let_flags(nc, h->cells(), h->let_box.p, h->d_off.p, R, me, h->theta, tpp, h->cost.t_mp,
+                   h->cost.t_ml, h->let_open.p, h->let_open.p + nc, h->let_flags.p, cs);
+  CKL();
+  h->stats.launches += 4;
+  {
+    size_t bytes = 0;
+    CK(exclusive_scan(nullptr, bytes, h->let_flags.p, h->let_excl.p, (int)nf, cs));
+    if (bytes > h->let_tmp_cap) {
+      if (h->let_tmp) cudaFree(h->let_tmp);
+      h->let_tmp = nullptr;
+      h->let_tmp_cap = 0;
+      CK(cudaMalloc(&h->let_tmp, bytes));
+      h->let_tmp_cap = bytes;
+    }
+    CK(exclusive_scan(h->let_tmp, bytes, h->let_flags.p, h->let_excl.p, (int)nf, cs));
+    ++h->stats.cub_calls;
+  }
+  launch_seg_counts(h->let_flags.p, h->let_excl.p, 2 * R, nc, h->let_cnt.p, cs);
+  CKL();
+  std::vector<int> cnt(2 * R);
+  CK(cudaMemcpyAsync(cnt.data(), h->let_cnt.p, sizeof(int) * 2 * R, cudaMemcpyDeviceToHost, cs));
+  CK(cudaStreamSynchronize(cs));
+  int TM = 0, TP = 0;
+  for (int r = 0; r < R; ++r) {
+    TM += cnt[r];
+    TP += cnt[R + r];
+  }
+  // compacted entries: multipole cells (receiver-major), then particle cells (receiver-major)
+  CK(h->let_ids.ensure((size_t)std::max(TM + TP, 1)));
+  launch_seg_scatter(h->let_flags.p, h->let_excl.p, (int64_t)nf, nc, h->let_ids.p, cs);
+  CKL();
+  // particle entries: my part of each cell's range, offsets, records for the receivers
+  CK(h->let_prng.ensure((size_t)std::max(TP, 1)));
+  CK(h->let_psize.ensure((size_t)std::max(TP, 1) + 1));
+  CK(h->let_pexcl.ensure((size_t)std::max(TP, 1) + 1));
+  CK(h->let_prec.ensure((size_t)std::max(TP, 1)));
+  CK(h->let_seg0.ensure((size_t)R + 1));
+  std::vector<int> seg0(R + 1, 0);
+  for (int r = 0; r < R; ++r) seg0[r + 1] = seg0[r] + cnt[R + r];
+  std::vector<int64_t> partP(R, 0);
+  if (TP > 0) {
+    launch_let_prange(h->let_ids.p + TM, TP, h->cells(), h->own_lo, h->own_hi, h->let_prng.p,
+                      h->let_psize.p, cs);
+    CKL();
+    CK(cudaMemsetAsync(h->let_psize.p + TP, 0, sizeof(int), cs));
+    size_t bytes = 0;
+    CK(exclusive_scan(nullptr, bytes, h->let_psize.p, h->let_pexcl.p, TP + 1, cs));
+    if (bytes > h->let_tmp_cap) {
+      cudaFree(h->let_tmp);
+      h->let_tmp = nullptr;
+      h->let_tmp_cap = 0;
+      CK(cudaMalloc(&h->let_tmp, bytes));
+      h->let_tmp_cap = bytes;
+    }
+    CK(exclusive_scan(h->let_tmp, bytes, h->let_psize.p, h->let_pexcl.p, TP + 1, cs));
+    ++h->stats.cub_calls;
+    CK(cudaMemcpyAsync(h->let_seg0.p, seg0.data(), sizeof(int) * (R + 1), cudaMemcpyHostToDevice, cs));
+    launch_let_precords(h->let_prng.p, h->let_pexcl.p, TP, h->let_seg0.p, R, h->let_prec.p, cs);
+    CKL();
+    std::vector<int> ex(TP + 1);
+    CK(cudaMemcpyAsync(ex.data(), h->let_pexcl.p, sizeof(int) * (TP + 1), cudaMemcpyDeviceToHost, cs));
+    CK(cudaStreamSynchronize(cs));
+    for (int r = 0; r < R; ++r) partP[r] = ex[seg0[r + 1]] - ex[seg0[r]];
+  }
+  // counts, then the four alltoallv: multipole ids, rows, particle records, particles
+  std::vector<int64_t> send3((size_t)3 * R), recv3;
+  for (int r = 0; r < R; ++r) {
+    send3[3 * r] = cnt[r];
+    send3[3 * r + 1] = cnt[R + r];
+    send3[3 * r + 2] = partP[r];
+  }
+  if (int rc = exchange_counts(h, send3, recv3, 3, cs)) return rc;
+  int64_t rM = 0, rP = 0, rPart = 0;
+  for (int r = 0; r < R; ++r) {
+    rM += recv3[3 * r];
+    rP += recv3[3 * r + 1];
+    rPart += recv3[3 * r + 2];
+  }
+  int64_t sPart = 0;
+  for (int r = 0; r < R; ++r) sPart += partP[r];
+  CK(h->let_rows_s.ensure((size_t)std::max(TM, 1) * NCS));
+  CK(h->let_pbuf_s.ensure((size_t)std::max<int64_t>(sPart, 1)));
+  launch_rows(h->M.p, h->let_rows_s.p, NCS, h->let_ids.p, TM, false, cs);
+  if (TM > 0) CKL();
+  if (TP > 0) {
+    launch_range_copy(h->pos.p, h->let_prng.p, h->let_pexcl.p, TP, h->let_pbuf_s.p, false, cs);
+    CKL();
+  }
+  CK(h->let_rids.ensure((size_t)std::max<int64_t>(rM, 1)));
+  CK(h->let_rows_r.ensure((size_t)std::max<int64_t>(rM, 1) * NCS));
+  CK(h->let_rrec.ensure((size_t)std::max<int64_t>(rP, 1)));
+  CK(h->let_pbuf_r.ensure((size_t)std::max<int64_t>(rPart, 1)));
+  if (int rc = a2av(h, h->let_ids.p, send3, h->let_rids.p, recv3, sizeof(unsigned), 3, 0, cs)) return rc;
+  if (int rc = a2av(h, h->let_rows_s.p, send3, h->let_rows_r.p, recv3, sizeof(float2) * NCS, 3, 0, cs)) return rc;
+  if (int rc = a2av(h, h->let_prec.p, send3, h->let_rrec.p, recv3, sizeof(int4), 3, 1, cs)) return rc;
+  if (int rc = a2av(h, h->let_pbuf_s.p, send3, h->let_pbuf_r.p, recv3, sizeof(float4), 3, 2, cs)) return rc;
+  // unpack into the global-index arrays
+  if (h->let_check) {
+    CK(h->let_haveM.ensure(nc));
+    CK(h->let_haveP.ensure((size_t)std::max(N, 1)));
+    CK(cudaMemsetAsync(h->let_haveM.p, 0, sizeof(int) * nc, cs));
+    CK(cudaMemsetAsync(h->let_haveP.p, 0, sizeof(int) * std::max(N, 1), cs));
+    launch_let_mark(h->let_rids.p, (int)rM, h->let_haveM.p, cs);
+  }
+  launch_rows(h->let_rows_r.p, h->M.p, NCS, h->let_rids.p, (int)rM, true, cs);
+  if (rM > 0) CKL();
+  int64_t ro = 0, po = 0;
+  for (int r = 0; r < R; ++r) {
+    launch_let_punpack(h->let_rrec.p + ro, (int)recv3[3 * r + 1], h->let_pbuf_r.p + po, h->pos.p,
+                       h->let_check ? h->let_haveP.p : nullptr, cs);
+    ro += recv3[3 * r + 1];
+    po += recv3[3 * r + 2];
+  }
+  CKL();
+  CK(cudaEventRecord(h->ev_let, cs));
+  record_on(h, EV_LET1, cs);
+  h->stats.let_cells = rM;
+  h->stats.let_particles = rPart;
+  return FMM_OK;
+}
+
+// LET check (FMM_LET_CHECK=1): every remote multipole and particle the lists name was received
+static int let_verify(fmm_ctx *h) {
+  cudaStream_t st = h->stream;
+  CK(h->let_missing.ensure(2));
+  CK(cudaMemsetAsync(h->let_missing.p, 0, 2 * sizeof(int), st));
+  launch_let_verify(h->lists(), (int)h->ntask[0], (int)h->ntask[1], (int)h->ntask[2], h->cells(),
+                    h->strad_flag.p, h->own_lo, h->own_hi, h->let_haveM.p, h->let_haveP.p,
+                    h->let_missing.p, st);
+  CKL();
+  int miss[2] = {0, 0};
+  CK(cudaMemcpyAsync(miss, h->let_missing.p, sizeof miss, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (miss[0] || miss[1])
+    return fail(h, FMM_E_INVALID, "local essential tree incomplete: %d multipoles, %d particle ranges missing",
+                miss[0], miss[1]);
+  return FMM_OK;
+}
+
 // results of the own particles (written by L2P in received order) back to the ranks that own
 // them, then into the caller's order
 static int dist_return(fmm_ctx *h, float *phi, float *grad) {
@@ -770,7 +967,7 @@ static int dist_return(fmm_ctx *h, float *phi, float *grad) {
 }
 
 // ---- a9: traversal ----------------------------------------------------------------------------
-static int traverse(fmm_ctx *h) {
+static int traverse(fmm_ctx *h, int (*between)(fmm_ctx *) = nullptr) {
   // Level-synchronous target-centric traversal (traverse.cu), one kernel per level. All
   // bookkeeping stays on the device: list buffers are sized from the previous evaluation (or an
   // estimate), a target whose lists would not fit writes nothing, and one read-back at the end
@@ -857,6 +1054,13 @@ static int traverse(fmm_ctx *h) {
       launch_traverse(A, st);
       CKL();
       in_src = ob->p;
+    }
+    record(h, EV_TRAV_END);
+    // work that must not wait for the traversal (the sender-side LET exchange) is issued here,
+    // after the first attempt has been queued and before the host waits for it
+    if (between) {
+      if (int rc = between(h)) return rc;
+      between = nullptr;
     }
     int hb2[TRAV_BK_INTS];
     unsigned ovf = 0;
@@ -968,9 +1172,18 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   }
   record_on(h, EV_UP, ua);
   CK(cudaEventRecord(h->ev_up, ua));
-  if (int rc = traverse(h)) return rc;
-  if (h->comm) {  // local essential tree: remote multipoles and particles this rank's lists name
-    if (int rc = dist_let(h)) return rc;
+  if (h->comm && !h->let_recv) {
+    // sender-side local essential tree: exchanged on its own stream while the traversal runs;
+    // everything that reads remote sources (P2P, M2P, M2L) waits for it
+    if (int rc = traverse(h, let_send)) return rc;
+    CK(cudaStreamWaitEvent(st, h->ev_let, 0));
+    if (h->let_check)
+      if (int rc = let_verify(h)) return rc;
+  } else {
+    if (int rc = traverse(h)) return rc;
+    if (h->comm) {  // receiver-driven local essential tree: what this rank's lists name
+      if (int rc = dist_let(h)) return rc;
+    }
   }
   record(h, EV_TRAV);
   // a12 P2P (writes acc), a11 M2P (adds): on the aux stream (after the upward sweep there) when
@@ -1247,6 +1460,11 @@ static void read_phase_times(fmm_ctx *h) {
   h->stats.ms_p2p = el(EV_P2P0, EV_P2P);
   h->stats.ms_m2p = el(EV_P2P, EV_M2P);
   h->stats.ms_downward = (h->overlap && h->mode != FMM_DIRECT) ? el(EV_M2L, EV_DOWN) : el(EV_M2P, EV_DOWN);
+  if (h->comm && !h->let_recv && h->mode != FMM_DIRECT) {
+    // the sender-side exchange and how far it ran past the traversal (0 = completely hidden)
+    h->stats.ms_let = el(EV_LET0, EV_LET1);
+    h->stats.ms_let_exposed = std::max(0.0, el(EV_TRAV_END, EV_LET1));
+  }
 }
 
 // ---- a6: kernel pre-calculation ------------------------------------
@@ -1352,6 +1570,8 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
     // paths of traverse() (tests/test_gpu_sanitize.py)
     if (const char *v = getenv("FMM_TRAV_CAP")) h->stack_cap = h->trav_ocap = std::max(32, atoi(v));
     if (const char *v = getenv("FMM_TRAV_LIST_EST")) h->trav_list_est = std::max(1, atoi(v));
+    if (const char *v = getenv("FMM_LET")) h->let_recv = strcmp(v, "recv") == 0;
+    if (const char *v = getenv("FMM_LET_CHECK")) h->let_check = v[0] && v[0] != '0';
     const char *no = getenv("FMM_NO_OVERLAP");
     h->overlap = !(no && no[0] && no[0] != '0');
     const char *nt = getenv("FMM_NO_TUNE");
@@ -1374,6 +1594,14 @@ int fmm_destroy(fmm_t h) {
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();
   h->tleaves.release(); h->p2p_desc.release();
+  h->let_box.release(); h->let_flags.release(); h->let_excl.release(); h->let_cnt.release();
+  h->let_psize.release(); h->let_pexcl.release(); h->let_seg0.release(); h->let_haveM.release();
+  h->let_haveP.release(); h->let_open.release(); h->let_ids.release(); h->let_rids.release();
+  h->let_prng.release(); h->let_prec.release(); h->let_rrec.release(); h->let_rows_s.release();
+  h->let_rows_r.release(); h->let_pbuf_s.release(); h->let_pbuf_r.release(); h->let_missing.release();
+  if (h->let_tmp) cudaFree(h->let_tmp);
+  if (h->cmst) cudaStreamDestroy(h->cmst);
+  if (h->ev_let) cudaEventDestroy(h->ev_let);
   h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
   h->ntgt.release(); h->ts_stage.release();

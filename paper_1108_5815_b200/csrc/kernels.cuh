@@ -198,6 +198,27 @@ void launch_range_copy(float4 *pos, const int2 *rng, const int *roff, int n, flo
                        bool to_pos, cudaStream_t st);
 void launch_scatter_results(const float *rphi, const float *rgrad, const unsigned *perm, int n,
                             float *phi, float *grad, cudaStream_t st);
+// sender-side local essential tree (dist.cu)
+int let_box_ints(int R);
+void launch_let_boxes(const int *leaves, int nleaves, int ncells, CellsView C, const int *off,
+                      int R, int kmax, int *box, cudaStream_t st);
+void launch_let_flags(int ncells, CellsView C, const int *box, const int *off, int R, int me,
+                      double theta, double t_pp, double t_mp, double t_ml, unsigned *open,
+                      unsigned *near, int *flags, cudaStream_t st);
+void launch_seg_counts(const int *flags, const int *excl, int nseg, int nc, int *cnt,
+                       cudaStream_t st);
+void launch_seg_scatter(const int *flags, const int *excl, int64_t n, int nc, unsigned *ids,
+                        cudaStream_t st);
+void launch_let_prange(const unsigned *ids, int n, CellsView C, int lo, int hi, int2 *rng,
+                       int *size, cudaStream_t st);
+void launch_let_precords(const int2 *rng, const int *excl, int n, const int *seg0, int R,
+                         int4 *rec, cudaStream_t st);
+void launch_let_punpack(const int4 *rec, int n, const float4 *data, float4 *pos, int *have,
+                        cudaStream_t st);
+void launch_let_mark(const unsigned *ids, int n, int *have, cudaStream_t st);
+void launch_let_verify(ListsView Ls, int n_m2l, int n_m2p, int n_p2p, CellsView C,
+                       const int *strad, int lo, int hi, const int *haveM, const int *haveP,
+                       int *missing, cudaStream_t st);
 cudaError_t sort_owner_pairs(void *tmp, size_t &tmp_bytes, const unsigned *kin, unsigned *kout,
                              const unsigned *vin, unsigned *vout, int n, int bits,
                              cudaStream_t st);

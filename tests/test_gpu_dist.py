@@ -27,6 +27,13 @@ from paper_1108_5815_b200.fmm import LocalGroup  # noqa: E402
 COST = (2e-12, 6e-11, 2.5e-9)
 
 
+@pytest.fixture(autouse=True)
+def let_check(monkeypatch):
+    """Every distributed evaluation verifies that its local essential tree is complete (each
+    remote multipole and particle range its lists name was received; FMM_LET_CHECK)."""
+    monkeypatch.setenv("FMM_LET_CHECK", "1")
+
+
 def shards(n, R, seed, empty_rank=None):
     """Random, uneven assignment of the particle indices to R ranks (optionally one empty)."""
     rng = np.random.default_rng(seed)
@@ -39,7 +46,7 @@ def shards(n, R, seed, empty_rank=None):
     return np.split(perm, cuts[:-1])
 
 
-def run_group(R, xyz, q, parts, p, theta, ncrit, mode, evals=1):
+def run_group(R, xyz, q, parts, p, theta, ncrit, mode, evals=1, timing=False):
     grp = LocalGroup(R)
     out = [None] * R
     errs = []
@@ -52,6 +59,7 @@ def run_group(R, xyz, q, parts, p, theta, ncrit, mode, evals=1):
             with torch.cuda.stream(s):
                 f = FMM(p=p, theta=theta, ncrit=ncrit, mode=mode, tune=False, group=(grp, r))
                 f.set_cost_model(*COST)
+                f.set_timing(timing)
                 x = torch.from_numpy(np.ascontiguousarray(xyz[parts[r]])).cuda()
                 c = torch.from_numpy(np.ascontiguousarray(q[parts[r]])).cuda()
                 for _ in range(evals):
@@ -102,8 +110,12 @@ CASES = [  # (R, dist, n, p, theta, ncrit, mode, empty rank)
 ]
 
 
+@pytest.mark.parametrize("let", ["send", "recv"])
 @pytest.mark.parametrize("R,dist,n,p,theta,ncrit,mode,empty", CASES)
-def test_dist_equals_single_gpu(R, dist, n, p, theta, ncrit, mode, empty):
+def test_dist_equals_single_gpu(monkeypatch, R, dist, n, p, theta, ncrit, mode, empty, let):
+    """Both local-essential-tree exchanges: the sender-side one (default; overlaps the traversal)
+    and the round-1 receiver-driven one (FMM_LET=recv)."""
+    monkeypatch.setenv("FMM_LET", let)
     xyz, q = make_particles(n, dist, 50 + R)
     parts = shards(n, R, 7 + R, empty)
     ref = single(xyz, q, p, theta, ncrit, mode)
@@ -151,19 +163,14 @@ def test_dist_repeated_and_single_rank():
 
 
 def test_dist_bench_workload_shape():
-    # bench.py at N > 1: rank r contributes one uniform instance shifted into unit cube r (one
-    # global problem, weak scaling); p = 10, theta = 0.4, ncrit = 64 as C2, at 2 x 200k here
-    R, n_local = 2, 200_000
-    parts_xyz, parts_q = [], []
-    for r in range(R):
-        x, q = make_particles(n_local, "uniform", 2 + 100 * r)
-        parts_xyz.append((x + np.array([r % 2, (r // 2) % 2, r // 4], np.float32)).astype(np.float32))
-        parts_q.append(q)
-    xyz = np.concatenate(parts_xyz)
-    q = np.concatenate(parts_q)
-    parts = [np.arange(r * n_local, (r + 1) * n_local) for r in range(R)]
+    # bench.py at N > 1 (C4 strong scaling): ONE uniform instance split evenly over the ranks,
+    # p = 10, theta = 0.4, ncrit = 64, here 2 x 200k; the sender-side exchange is timed on its
+    # own stream and reported with how much of it the traversal did not hide
+    R, n = 2, 400_000
+    xyz, q = make_particles(n, "uniform", 4)
+    parts = [np.arange(r * n // R, (r + 1) * n // R) for r in range(R)]
     ref = single(xyz, q, 10, 0.4, 64, "hybrid")
-    out = run_group(R, xyz, q, parts, 10, 0.4, 64, "hybrid")
+    out = run_group(R, xyz, q, parts, 10, 0.4, 64, "hybrid", evals=2, timing=True)
     phi = np.concatenate([o["phi"] for o in out])
     grad = np.concatenate([o["grad"] for o in out])
     assert O.rel_l2(phi, ref["phi"]) < 1e-6 and O.rel_l2(grad, ref["grad"]) < 1e-6
@@ -172,6 +179,7 @@ def test_dist_bench_workload_shape():
     assert O.rel_l2(phi[s], d[0]) < 1e-4 and O.rel_l2(grad[s], d[1]) < 1e-3
     st = [o["stats"] for o in out]
     assert all(x["let_cells"] > 0 and x["let_particles"] > 0 for x in st)
+    assert all(x["ms_let"] > 0 and 0 <= x["ms_let_exposed"] <= x["ms_let"] + 1e-3 for x in st)
 
 
 def test_nccl_transport_world1(tmp_path):
