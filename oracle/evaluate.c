@@ -75,6 +75,17 @@ static void group_by_target(const orc_task *tasks, int64_t ntasks, int64_t ncell
 orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double theta, int ncrit,
                      int mode, const double cost[3], const int64_t *sample, int64_t nsample,
                      double *phi, double *grad, double *phase_seconds) {
+  return orc_fmm_run_basis(xyz, q, n, p, theta, ncrit, mode, cost, sample, nsample, phi, grad,
+                           phase_seconds, ORC_SPHERICAL);
+}
+
+/* basis: ORC_SPHERICAL (harmonics.c) or ORC_CARTESIAN (cartesian.c, Taylor of total order p);
+ * tree, traversal, kind selection and P2P are the same for both. */
+orc_fmm *orc_fmm_run_basis(const float *xyz, const float *q, int64_t n, int p, double theta,
+                           int ncrit, int mode, const double cost[3], const int64_t *sample,
+                           int64_t nsample, double *phi, double *grad, double *phase_seconds,
+                           int basis) {
+  const int cart = basis == ORC_CARTESIAN;
   double ph_t[5] = {0, 0, 0, 0, 0};
   orc_fmm *f = (orc_fmm *)calloc(1, sizeof(orc_fmm));
   f->n = n;
@@ -174,11 +185,19 @@ orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double 
   const int64_t NT = (int64_t)(p + 1) * (p + 1);
   cplx *M = (cplx *)calloc((size_t)(nc * NT), sizeof(cplx));
   cplx *Lx = (cplx *)calloc((size_t)(nc * NT), sizeof(cplx));
+  const int64_t NK = orc_cart_count(p);
+  double *MC = cart ? (double *)calloc((size_t)(nc * NK), sizeof(double)) : NULL;
+  double *LC = cart ? (double *)calloc((size_t)(nc * NK), sizeof(double)) : NULL;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int64_t c = 0; c < nc; ++c)
-    if (cells[c].nchild == 0)
-      orc_p2m(p, &centre[3 * c], cells[c].count, &xs[3 * cells[c].begin], &qs[cells[c].begin],
-              &M[c * NT]);
+    if (cells[c].nchild == 0) {
+      if (cart)
+        orc_cart_p2m(p, &centre[3 * c], cells[c].count, &xs[3 * cells[c].begin],
+                     &qs[cells[c].begin], &MC[c * NK]);
+      else
+        orc_p2m(p, &centre[3 * c], cells[c].count, &xs[3 * cells[c].begin], &qs[cells[c].begin],
+                &M[c * NT]);
+    }
   for (int l = maxlev - 1; l >= 0; --l) {
 #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t k = lev_off[l]; k < lev_off[l + 1]; ++k) {
@@ -187,7 +206,8 @@ orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double 
         const int64_t C = cells[P].child[ch];
         const double b[3] = {centre[3 * C] - centre[3 * P], centre[3 * C + 1] - centre[3 * P + 1],
                              centre[3 * C + 2] - centre[3 * P + 2]};
-        orc_m2m(p, &M[C * NT], b, &M[P * NT]);
+        if (cart) orc_cart_m2m(p, &MC[C * NK], b, &MC[P * NK]);
+        else orc_m2m(p, &M[C * NT], b, &M[P * NT]);
       }
     }
   }
@@ -210,7 +230,8 @@ orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double 
       const int64_t s = f->tasks[idx[ORC_K_M2L][e]].s;
       const double d[3] = {centre[3 * t] - centre[3 * s], centre[3 * t + 1] - centre[3 * s + 1],
                            centre[3 * t + 2] - centre[3 * s + 2]};
-      orc_m2l(p, &M[s * NT], d, &Lx[t * NT]);
+      if (cart) orc_cart_m2l(p, &MC[s * NK], d, &LC[t * NK]);
+      else orc_m2l(p, &M[s * NT], d, &Lx[t * NT]);
     }
   double *acc_phi = (double *)calloc((size_t)n, sizeof(double));
   double *acc_grad = (double *)calloc(3 * (size_t)n, sizeof(double));
@@ -226,7 +247,13 @@ orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double 
           const int64_t s = f->tasks[idx[ORC_K_M2P][e]].s;
           for (int64_t i = b; i < b + cnt; ++i)
             if (slot[i] >= 0)
-              orc_m2p(p, &M[s * NT], &centre[3 * s], 1, &xs[3 * i], &acc_phi[i], &acc_grad[3 * i]);
+            {
+              if (cart)
+                orc_cart_m2p(p, &MC[s * NK], &centre[3 * s], 1, &xs[3 * i], &acc_phi[i],
+                             &acc_grad[3 * i]);
+              else
+                orc_m2p(p, &M[s * NT], &centre[3 * s], 1, &xs[3 * i], &acc_phi[i], &acc_grad[3 * i]);
+            }
         }
         for (int64_t e = off[ORC_K_P2P][a]; e < off[ORC_K_P2P][a + 1]; ++e) {
           const int64_t s = f->tasks[idx[ORC_K_P2P][e]].s;
@@ -249,7 +276,8 @@ orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double 
       if (mask && !mask[C]) continue;
       const double e[3] = {centre[3 * C] - centre[3 * P], centre[3 * C + 1] - centre[3 * P + 1],
                            centre[3 * C + 2] - centre[3 * P + 2]};
-      orc_l2l(p, &Lx[P * NT], e, &Lx[C * NT]);
+      if (cart) orc_cart_l2l(p, &LC[P * NK], e, &LC[C * NK]);
+      else orc_l2l(p, &Lx[P * NT], e, &Lx[C * NT]);
     }
   }
 #pragma omp parallel for schedule(dynamic, 4)
@@ -257,7 +285,13 @@ orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double 
     if (cells[leaf].nchild != 0) continue;
     for (int64_t i = cells[leaf].begin; i < cells[leaf].begin + cells[leaf].count; ++i)
       if (slot[i] >= 0)
-        orc_l2p(p, &Lx[leaf * NT], &centre[3 * leaf], 1, &xs[3 * i], &acc_phi[i], &acc_grad[3 * i]);
+      {
+        if (cart)
+          orc_cart_l2p(p, &LC[leaf * NK], &centre[3 * leaf], 1, &xs[3 * i], &acc_phi[i],
+                       &acc_grad[3 * i]);
+        else
+          orc_l2p(p, &Lx[leaf * NT], &centre[3 * leaf], 1, &xs[3 * i], &acc_phi[i], &acc_grad[3 * i]);
+      }
   }
   ph_t[4] = now() - t4;
 
@@ -275,6 +309,8 @@ orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double 
   free(acc_grad);
   free(M);
   free(Lx);
+  free(MC);
+  free(LC);
   free(centre);
   free(lev_off);
   free(by_lev);

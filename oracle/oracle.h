@@ -24,6 +24,7 @@ typedef double complex cplx;
 
 enum { ORC_HYBRID = 0, ORC_FMM = 1, ORC_TREECODE = 2, ORC_DIRECT = 3 };
 enum { ORC_K_M2L = 0, ORC_K_M2P = 1, ORC_K_P2P = 2 };
+enum { ORC_SPHERICAL = 0, ORC_CARTESIAN = 1 };
 
 /* ---- harmonics.c: solid harmonics and the seven operators ---- */
 void orc_harm_R(const double x[3], int P, cplx *R);
@@ -38,6 +39,21 @@ void orc_m2p(int p, const cplx *M, const double c[3], int64_t n, const double *x
              double *grad);
 void orc_p2p(int64_t nt, const double *xt, int64_t ns, const double *ys, const double *qs,
              double *phi, double *grad);
+
+/* ---- cartesian.c: Cartesian Taylor expansions of total order p (NEXT-2; DESIGN reading R17) ----
+ * Real coefficients, one per multi-index k with |k| <= p, indexed by orc_cart_index. */
+int orc_cart_count(int P);
+int orc_cart_index(int kx, int ky, int kz);
+void orc_cart_multi(int P, int *k3);
+void orc_cart_derivs(const double d[3], int P, double *a);
+void orc_cart_p2m(int p, const double c[3], int64_t n, const double *y, const double *q, double *M);
+void orc_cart_m2m(int p, const double *Mc, const double b[3], double *Mp);
+void orc_cart_m2l(int p, const double *Ms, const double d[3], double *Lt);
+void orc_cart_l2l(int p, const double *Lp, const double e[3], double *Lc);
+void orc_cart_l2p(int p, const double *L, const double c[3], int64_t n, const double *x,
+                  double *phi, double *grad);
+void orc_cart_m2p(int p, const double *M, const double c[3], int64_t n, const double *x,
+                  double *phi, double *grad);
 
 /* ---- tree.c: root cube, Morton keys, sort, adaptive octree ---- */
 typedef struct {
@@ -74,6 +90,10 @@ typedef struct orc_fmm orc_fmm;
 orc_fmm *orc_fmm_run(const float *xyz, const float *q, int64_t n, int p, double theta, int ncrit,
                      int mode, const double cost[3], const int64_t *sample, int64_t nsample,
                      double *phi, double *grad, double *phase_seconds);
+orc_fmm *orc_fmm_run_basis(const float *xyz, const float *q, int64_t n, int p, double theta,
+                           int ncrit, int mode, const double cost[3], const int64_t *sample,
+                           int64_t nsample, double *phi, double *grad, double *phase_seconds,
+                           int basis);
 int64_t orc_fmm_ncells(const orc_fmm *f);
 void orc_fmm_tree(const orc_fmm *f, int32_t *level, uint64_t *prefix, int64_t *begin,
                   int64_t *count);

@@ -16,7 +16,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
-SOURCES = ["harmonics.c", "tree.c", "traversal.c", "evaluate.c"]
+SOURCES = ["harmonics.c", "cartesian.c", "tree.c", "traversal.c", "evaluate.c"]
 
 HYBRID, FMM, TREECODE, DIRECT = 0, 1, 2, 3
 K_M2L, K_M2P, K_P2P = 0, 1, 2
@@ -61,6 +61,20 @@ def lib():
         L.orc_fmm_run.argtypes = [fp, fp, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int, dp,
                                   i64p, C.c_int64, dp, dp, dp]
         L.orc_fmm_run.restype = C.c_void_p
+        L.orc_fmm_run_basis.argtypes = L.orc_fmm_run.argtypes + [C.c_int]
+        L.orc_fmm_run_basis.restype = C.c_void_p
+        L.orc_cart_count.argtypes = [C.c_int]
+        L.orc_cart_count.restype = C.c_int
+        L.orc_cart_index.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.orc_cart_index.restype = C.c_int
+        L.orc_cart_multi.argtypes = [C.c_int, C.POINTER(C.c_int)]
+        L.orc_cart_derivs.argtypes = [dp, C.c_int, dp]
+        L.orc_cart_p2m.argtypes = [C.c_int, dp, C.c_int64, dp, dp, dp]
+        L.orc_cart_m2m.argtypes = [C.c_int, dp, dp, dp]
+        L.orc_cart_m2l.argtypes = [C.c_int, dp, dp, dp]
+        L.orc_cart_l2l.argtypes = [C.c_int, dp, dp, dp]
+        L.orc_cart_l2p.argtypes = [C.c_int, dp, dp, C.c_int64, dp, dp, dp]
+        L.orc_cart_m2p.argtypes = [C.c_int, dp, dp, C.c_int64, dp, dp, dp]
         L.orc_fmm_ncells.argtypes = [C.c_void_p]
         L.orc_fmm_ncells.restype = C.c_int64
         L.orc_fmm_ntasks.argtypes = [C.c_void_p]
@@ -162,6 +176,73 @@ def p2p(xt, ys, qs):
 
 
 # ---------------- keys ----------------
+# ---- Cartesian Taylor operators (cartesian.c; NEXT-2) --------------------------------------
+def cart_count(p: int) -> int:
+    return int(lib().orc_cart_count(p))
+
+
+def cart_index(kx, ky, kz) -> int:
+    return int(lib().orc_cart_index(kx, ky, kz))
+
+
+def cart_multi(p):
+    k3 = np.zeros((cart_count(p), 3), np.int32)
+    lib().orc_cart_multi(p, _p(k3, C.c_int))
+    return k3
+
+
+def cart_derivs(d, P):
+    a = np.zeros(cart_count(P))
+    lib().orc_cart_derivs(_p(np.ascontiguousarray(d, np.float64), C.c_double), P, _p(a, C.c_double))
+    return a
+
+
+def cart_p2m(p, c, y, q):
+    y = np.ascontiguousarray(y, np.float64).reshape(-1, 3)
+    M = np.zeros(cart_count(p))
+    lib().orc_cart_p2m(p, _p(np.ascontiguousarray(c, np.float64), C.c_double), len(y),
+                       _p(y, C.c_double), _p(np.ascontiguousarray(q, np.float64), C.c_double),
+                       _p(M, C.c_double))
+    return M
+
+
+def _cart_shift(fn, p, X, v):
+    out = np.zeros(cart_count(p))
+    fn(p, _p(np.ascontiguousarray(X, np.float64), C.c_double),
+       _p(np.ascontiguousarray(v, np.float64), C.c_double), _p(out, C.c_double))
+    return out
+
+
+def cart_m2m(p, Mc, b):
+    return _cart_shift(lib().orc_cart_m2m, p, Mc, b)
+
+
+def cart_m2l(p, Ms, d):
+    return _cart_shift(lib().orc_cart_m2l, p, Ms, d)
+
+
+def cart_l2l(p, Lp, e):
+    return _cart_shift(lib().orc_cart_l2l, p, Lp, e)
+
+
+def _cart_eval(fn, p, X, c, x):
+    x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+    phi = np.zeros(len(x))
+    grad = np.zeros((len(x), 3))
+    fn(p, _p(np.ascontiguousarray(X, np.float64), C.c_double),
+       _p(np.ascontiguousarray(c, np.float64), C.c_double), len(x), _p(x, C.c_double),
+       _p(phi, C.c_double), _p(grad, C.c_double))
+    return phi, grad
+
+
+def cart_l2p(p, L, c, x):
+    return _cart_eval(lib().orc_cart_l2p, p, L, c, x)
+
+
+def cart_m2p(p, M, c, x):
+    return _cart_eval(lib().orc_cart_m2p, p, M, c, x)
+
+
 def root_cube(xyz):
     xyz = np.ascontiguousarray(xyz, np.float32)
     o = np.zeros(3)
@@ -195,8 +276,9 @@ class OracleResult:
 
 
 def fmm(xyz, q, p, theta, ncrit, mode=HYBRID, cost=(1.0, 1.0, 1.0), sample=None,
-        want_structure=True) -> OracleResult:
-    """The whole method in FP64. cost = (t_pp, t_mp, t_ml) seconds per unit."""
+        want_structure=True, basis="spherical") -> OracleResult:
+    """The whole method (PAPER.md:145-169) in FP64. cost = (t_pp, t_mp, t_ml) seconds per unit;
+    basis = "spherical" (harmonics.c) or "cartesian" (cartesian.c, NEXT-2)."""
     xyz = np.ascontiguousarray(xyz, np.float32).reshape(-1, 3)
     q = np.ascontiguousarray(q, np.float32)
     n = len(q)
@@ -211,9 +293,10 @@ def fmm(xyz, q, p, theta, ncrit, mode=HYBRID, cost=(1.0, 1.0, 1.0), sample=None,
     grad = np.zeros((nout, 3))
     phases = np.zeros(5)
     L = lib()
-    h = L.orc_fmm_run(_p(xyz, C.c_float), _p(q, C.c_float), n, p, float(theta), ncrit, mode,
-                      _p(cost_a, C.c_double), sp, nout if sample is not None else 0,
-                      _p(phi, C.c_double), _p(grad, C.c_double), _p(phases, C.c_double))
+    h = L.orc_fmm_run_basis(_p(xyz, C.c_float), _p(q, C.c_float), n, p, float(theta), ncrit, mode,
+                            _p(cost_a, C.c_double), sp, nout if sample is not None else 0,
+                            _p(phi, C.c_double), _p(grad, C.c_double), _p(phases, C.c_double),
+                            {"spherical": 0, "cartesian": 1}[basis])
     if not h:
         raise ValueError("non-finite input")
     try:
