@@ -44,6 +44,9 @@ enum fmm_mode { FMM_HYBRID = 0, FMM_FMM = 1, FMM_TREECODE = 2, FMM_DIRECT = 3 };
 
 /* Interaction kinds in exported lists. */
 enum fmm_kind { FMM_KIND_M2L = 0, FMM_KIND_M2P = 1, FMM_KIND_P2P = 2 };
+/* expansion basis (fmm_set_basis): spherical harmonics (default), Cartesian Taylor of total order
+ * p (p <= 4), or the automatic switch between them */
+enum fmm_basis { FMM_BASIS_SPHERICAL = 0, FMM_BASIS_CARTESIAN = 1, FMM_BASIS_AUTO = 2 };
 
 enum fmm_status {
   FMM_OK = 0,
@@ -141,6 +144,23 @@ int fmm_set_timing(fmm_t h, int enable);
  * each pair's local expansion straight into its target with vector reductions in L2: faster, but
  * the summation order then varies from run to run (differences at FP32 rounding level). */
 int fmm_set_deterministic(fmm_t h, int enable);
+
+/* Expansion basis ("capability to switch to Cartesian expansions
+ * ... key to achieving high performance for low-accuracy").
+ *   FMM_BASIS_SPHERICAL  solid harmonics of order p (the default; every p).
+ *   FMM_BASIS_CARTESIAN  Cartesian Taylor expansions of total order p (reading R17:
+ *                        multipole moments sum q (y-c)^k, |k| <= p; M2L truncated at
+ *                        |k| + |n| <= p), for 1 <= p <= 4 on single-GPU handles; the cell-cell
+ *                        M2L runs on CUDA cores, one warp per target cell.
+ *   FMM_BASIS_AUTO       the automatic switch: for p <= 4 each basis gets its kernel
+ *                        pre-calculation and one hybrid evaluation of 2^20 synthetic particles is
+ *                        timed; the faster basis is kept (spherical for p > 4 or distributed
+ *                        handles). Synchronous; takes about a second.
+ * Switching basis re-runs the kernel pre-calculation when the cost model was measured.
+ * Errors: FMM_E_INVALID (unknown basis, Cartesian with p > 4 or on a distributed handle). */
+int fmm_set_basis(fmm_t h, int basis);
+/* The basis in use; after FMM_BASIS_AUTO the two measured evaluation times (ms, else 0). */
+int fmm_get_basis(fmm_t h, int *basis, double *ms_spherical, double *ms_cartesian);
 
 /* Re-run the kernel pre-calculation on this device (a single-GPU run on synthetic data).
  * On a distributed handle it is collective and every rank then holds rank 0's table. */

@@ -118,7 +118,11 @@ struct fmm_ctx {
   DBuf<int> nch, excl, leafflag, leaves, bnd;
   DBuf<int2> crange;
   DBuf<int4> cpack;  // packed cell records for the traversal
-  DBuf<int4> p2p_desc;
+  // expansion basis (NEXT-2): 0 spherical harmonics, 1 Cartesian Taylor (p <= CART_PMAX)
+  int basis = 0;
+  double basis_ms[2] = {0, 0};  // FMM_BASIS_AUTO: the measured evaluation time of each basis
+  DBuf<float> Mc, Lc;           // Cartesian expansions [ncells][cart_stride(p)]
+  DBuf<int4> p2p_desc;  // per target leaf: (begin, count, own P2P list offset, count | ancestor flag)
   // sender-side local essential tree (let_send): flags, compacted entries, send / receive buffers
   cudaStream_t cmst = nullptr;  // its stream (the exchange overlaps the traversal)
   cudaEvent_t ev_let = nullptr;
@@ -1121,7 +1125,13 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   if (NCS != NC || h->comm) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, ua));
   // M2M / L2L: octant-class GEMMs on the tensor cores (p <= 10) unless disabled
   const char *scc = getenv("FMM_SHIFT_CUDA_CORES");
-  const bool shift_tc = m2l_tc_supported(p) && h->ncells > 1 && !(scc && scc[0] && scc[0] != '0');
+  const bool cart = h->basis == FMM_BASIS_CARTESIAN;
+  const bool shift_tc = !cart && m2l_tc_supported(p) && h->ncells > 1 && !(scc && scc[0] && scc[0] != '0');
+  const int CSt = cart_stride(p);
+  if (cart) {
+    CK(h->Mc.ensure((size_t)h->ncells * CSt));
+    CK(h->Lc.ensure((size_t)h->ncells * CSt));
+  }
   TcShiftWork S{};
   if (shift_tc) {
     const size_t tw = m2l_tc_T_words(p);
@@ -1157,11 +1167,14 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.launches += 3;
     h->stats.cub_calls += 1;
   }
-  if (h->comm) launch_p2m(p, h->tleaves.p, h->tleaves_n, h->cells(), h->pos.p, h->M.p, ua);
+  if (cart) launch_cart_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->Mc.p, ua);
+  else if (h->comm) launch_p2m(p, h->tleaves.p, h->tleaves_n, h->cells(), h->pos.p, h->M.p, ua);
   else launch_p2m(p, h->leaves.p, h->nleaves, h->cells(), h->pos.p, h->M.p, ua);
   CKL();
   for (int level = h->depth - 1; level >= 0; --level) {
-    if (shift_tc) {
+    if (cart) {
+      launch_cart_m2m(p, h->level_off[level], h->level_cnt[level], h->cells(), h->Mc.p, ua);
+    } else if (shift_tc) {
       CK(tc_shift_m2m_level(p, level, h->level_off[level], h->level_cnt[level], h->cells(), S,
                             h->M.p, h->sh_Y.p, ua));
       h->stats.launches += 2;
@@ -1200,7 +1213,11 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     record_on(h, EV_P2P, ns);
     if (h->ntask[FMM_KIND_M2P] > 0) {
       CK(cudaStreamWaitEvent(ns, h->ev_up, 0));  // M2P reads the multipoles
-      launch_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, h->d_small + 13, ns);
+      if (cart)
+        launch_cart_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->Mc.p, h->acc.p,
+                        h->d_small + 13, ns);
+      else
+        launch_m2p(p, tl, ntl, h->cells(), h->lists(), h->pos.p, h->M.p, h->acc.p, h->d_small + 13, ns);
       CKL();
     }
     record_on(h, EV_M2P, ns);
@@ -1215,7 +1232,12 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   record(h, EV_M2L_PREP);  // re-recorded after the class sort when there are M2L pairs
   // a10 M2L (writes every cell's local expansion, zero where no M2L)
   const bool far_local = h->ntask[FMM_KIND_M2L] > 0;
-  if (far_local) {
+  if (far_local && cart) {  // Cartesian: one warp per target over its list (cart.cu), no classes
+    CK(cudaStreamWaitEvent(st, h->ev_up, 0));
+    record(h, EV_M2L_PREP);
+    launch_cart_m2l(p, h->ncells, h->cells(), h->lists(), h->Mc.p, h->Lc.p, st);
+    CKL();
+  } else if (far_local) {
     const int np = (int)h->ntask[FMM_KIND_M2L];
     CK(h->m2l_pair_t.ensure(np));
     CK(h->m2l_pst.ensure(np));
@@ -1331,7 +1353,9 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   // a13 L2L top-down, a14/a15 L2P + combine + un-permute
   if (far_local) {
     for (int level = 1; level <= h->depth; ++level) {
-      if (shift_tc) {
+      if (cart) {
+        launch_cart_l2l(p, h->level_off[level], h->level_cnt[level], h->cells(), h->Lc.p, st);
+      } else if (shift_tc) {
         CK(tc_shift_l2l_level(p, level, h->level_off[level], h->level_cnt[level], S, h->L.p,
                               h->sh_Y.p, st));
         h->stats.launches += 2;
@@ -1350,8 +1374,12 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     ograd = h->rgrad.p;
   }
   if (h->overlap) CK(cudaStreamWaitEvent(st, h->ev_near, 0));  // join: acc is complete
-  launch_l2p(p, tl, ntl, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, ophi,
-             ograd, far_local ? 1 : 0, st);
+  if (cart)
+    launch_cart_l2p(p, tl, ntl, h->cells(), h->pos.p, h->Lc.p, h->acc.p, h->perm.p, ophi, ograd,
+                    far_local ? 1 : 0, st);
+  else
+    launch_l2p(p, tl, ntl, h->cells(), h->pos.p, h->L.p, h->acc.p, h->perm.p, ophi,
+               ograd, far_local ? 1 : 0, st);
   CKL();
   if (h->comm) {
     if (int rc = dist_return(h, phi, grad)) return rc;
@@ -1516,6 +1544,49 @@ static int tune_impl(fmm_ctx *h) {
   return FMM_OK;
 }
 
+// FMM_BASIS_AUTO (NEXT-2: switching to Cartesian expansions is "key to achieving
+// high performance for low-accuracy"): each candidate basis gets its own kernel pre-calculation,
+// then one hybrid evaluation of the same 2^20 synthetic particles is timed (median of 3, CUDA
+// events) and the faster basis is kept with its cost model.
+static int auto_basis_impl(fmm_ctx *h) {
+  if (!cart_supported(h->p) || h->comm) {
+    h->basis = FMM_BASIS_SPHERICAL;
+    return FMM_OK;
+  }
+  const int64_t n = (int64_t)1 << 20;
+  float *d = nullptr;
+  CK(cudaMalloc(&d, sizeof(float) * 8 * n));
+  float *xyz = d, *q = d + 3 * n, *phi = d + 4 * n, *grad = d + 5 * n;
+  launch_fill_random(xyz, 3 * n, 4242u, 0.f, 1.f, h->stream);
+  launch_fill_random(q, n, 4343u, 1.0f / n, 1.0f / n, h->stream);
+  fmm_cost_t cost[2];
+  int rc = FMM_OK;
+  const int saved_mode = h->mode;
+  const bool saved_timing = h->timing;
+  for (int b = 0; b < 2 && rc == FMM_OK; ++b) {
+    h->basis = b;
+    rc = tune_impl(h);
+    cost[b] = h->cost;
+    h->mode = FMM_HYBRID;
+    h->timing = true;
+    double t[3] = {0, 0, 0};
+    for (int it = -1; it < 3 && rc == FMM_OK; ++it) {
+      rc = evaluate_impl(h, xyz, q, n, phi, grad);
+      if (it >= 0) t[it] = h->stats.ms_total;
+    }
+    std::sort(t, t + 3);
+    h->basis_ms[b] = t[1];
+    h->mode = saved_mode;
+    h->timing = saved_timing;
+  }
+  cudaFree(d);
+  if (rc) return rc;
+  h->basis = h->basis_ms[1] < h->basis_ms[0] ? FMM_BASIS_CARTESIAN : FMM_BASIS_SPHERICAL;
+  h->cost = cost[h->basis];
+  h->have_tree = false;
+  return FMM_OK;
+}
+
 // ================================ C ABI =========================================================
 extern "C" {
 
@@ -1593,7 +1664,7 @@ int fmm_destroy(fmm_t h) {
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();
-  h->tleaves.release(); h->p2p_desc.release();
+  h->tleaves.release(); h->p2p_desc.release(); h->Mc.release(); h->Lc.release();
   h->let_box.release(); h->let_flags.release(); h->let_excl.release(); h->let_cnt.release();
   h->let_psize.release(); h->let_pexcl.release(); h->let_seg0.release(); h->let_haveM.release();
   h->let_haveP.release(); h->let_open.release(); h->let_ids.release(); h->let_rids.release();
@@ -1769,6 +1840,34 @@ int fmm_set_timing(fmm_t h, int enable) {
 int fmm_set_deterministic(fmm_t h, int enable) {
   if (!h) return FMM_E_INVALID;
   h->deterministic = enable != 0;
+  return FMM_OK;
+}
+
+int fmm_set_basis(fmm_t h, int basis) {
+  if (!h) return FMM_E_INVALID;
+  DeviceGuard dg(h->device);
+  if (basis == FMM_BASIS_SPHERICAL) {
+    const bool changed = h->basis != FMM_BASIS_SPHERICAL;
+    h->basis = FMM_BASIS_SPHERICAL;
+    return changed && h->cost.measured ? tune_impl(h) : FMM_OK;
+  }
+  if (basis == FMM_BASIS_CARTESIAN) {
+    if (!cart_supported(h->p))
+      return fail(h, FMM_E_INVALID, "Cartesian expansions need 1 <= p <= %d", CART_PMAX);
+    if (h->comm) return fail(h, FMM_E_INVALID, "Cartesian expansions: single-GPU handles only");
+    const bool changed = h->basis != FMM_BASIS_CARTESIAN;
+    h->basis = FMM_BASIS_CARTESIAN;
+    return changed && h->cost.measured ? tune_impl(h) : FMM_OK;
+  }
+  if (basis == FMM_BASIS_AUTO) return auto_basis_impl(h);
+  return fail(h, FMM_E_INVALID, "unknown basis %d", basis);
+}
+
+int fmm_get_basis(fmm_t h, int *basis, double *ms_spherical, double *ms_cartesian) {
+  if (!h || !basis) return FMM_E_INVALID;
+  *basis = h->basis;
+  if (ms_spherical) *ms_spherical = h->basis_ms[0];
+  if (ms_cartesian) *ms_cartesian = h->basis_ms[1];
   return FMM_OK;
 }
 

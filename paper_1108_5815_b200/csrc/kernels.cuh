@@ -159,6 +159,24 @@ cudaError_t tc_shift_m2m_level(int p, int level, int c0, int nl, CellsView C,
 cudaError_t tc_shift_l2l_level(int p, int level, int c0, int nl, const TcShiftWork &S, float2 *L,
                                float *Y, cudaStream_t st);
 
+// ---- cart.cu (Cartesian Taylor expansions, NEXT-2) ----
+#define CART_PMAX 4
+bool cart_supported(int p);
+int cart_stride(int p);
+int cart_count(int p);
+void launch_cart_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos,
+                     float *M, cudaStream_t st);
+void launch_cart_m2m(int p, int c0, int nl, CellsView C, float *M, cudaStream_t st);
+void launch_cart_m2l(int p, int ncells, CellsView C, ListsView Ls, const float *M, float *L,
+                     cudaStream_t st);
+void launch_cart_l2l(int p, int c0, int nl, CellsView C, float *L, cudaStream_t st);
+void launch_cart_l2p(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos,
+                     const float *L, const float4 *acc, const unsigned *perm, float *phi,
+                     float *grad, int use_local, cudaStream_t st);
+void launch_cart_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsView Ls,
+                     const float4 *pos, const float *M, float4 *acc, int *counter,
+                     cudaStream_t st);
+
 // ---- p2p.cu ----
 // desc: scratch of nleaves int4 (per-leaf work descriptors built by the launch)
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,

@@ -11,9 +11,11 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 HYBRID, FMM_MODE, TREECODE, DIRECT = 0, 1, 2, 3
 MODES = {"hybrid": HYBRID, "fmm": FMM_MODE, "treecode": TREECODE, "direct": DIRECT}
+BASES = {"spherical": 0, "cartesian": 1, "auto": 2}
 SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_ts", "fmm_evaluate_host",
            "fmm_set_stream",
-           "fmm_set_mode", "fmm_set_timing", "fmm_set_deterministic", "fmm_tune", "fmm_get_cost_model",
+           "fmm_set_mode", "fmm_set_timing", "fmm_set_deterministic", "fmm_set_basis", "fmm_get_basis",
+           "fmm_tune", "fmm_get_cost_model",
            "fmm_set_cost_model", "fmm_get_stats", "fmm_export_tree", "fmm_export_lists",
            "fmm_export_perm", "fmm_set_partition", "fmm_get_partition", "fmm_partition_indices",
            "fmm_comm_unique_id", "fmm_create_dist", "fmm_group_create", "fmm_group_destroy",
@@ -74,6 +76,8 @@ def load_library():
     L.fmm_set_mode.argtypes = [vp, C.c_int]
     L.fmm_set_timing.argtypes = [vp, C.c_int]
     L.fmm_set_deterministic.argtypes = [vp, C.c_int]
+    L.fmm_set_basis.argtypes = [vp, C.c_int]
+    L.fmm_get_basis.argtypes = [vp, P(C.c_int), P(dp), P(dp)]
     L.fmm_tune.argtypes = [vp]
     L.fmm_get_cost_model.argtypes = [vp, P(CostModel)]
     L.fmm_set_cost_model.argtypes = [vp, P(CostModel)]
@@ -196,6 +200,18 @@ class FMM:
     def set_deterministic(self, on: bool):
         """Bit-reproducible M2L summation order (slower); see fmm_set_deterministic in fmm.h."""
         self._check(self.L.fmm_set_deterministic(self.h, int(bool(on))), "fmm_set_deterministic")
+
+    def set_basis(self, basis):
+        """"spherical" | "cartesian" | "auto" (fmm_set_basis; Cartesian Taylor for p <= 4)."""
+        b = BASES[basis] if isinstance(basis, str) else int(basis)
+        self._check(self.L.fmm_set_basis(self.h, b), "fmm_set_basis")
+
+    def basis(self):
+        """(basis name, auto-switch timings {basis: ms}) of the handle."""
+        b, ts, tc = C.c_int(), C.c_double(), C.c_double()
+        self._check(self.L.fmm_get_basis(self.h, C.byref(b), C.byref(ts), C.byref(tc)), "fmm_get_basis")
+        return {v: k for k, v in BASES.items() if k != "auto"}[b.value], {"spherical": ts.value,
+                                                                          "cartesian": tc.value}
 
     def set_stream(self, stream):
         self._check(self.L.fmm_set_stream(self.h, C.c_void_p(stream)), "fmm_set_stream")

@@ -33,6 +33,19 @@ for dist, n, p, th, nc in cases:
     torch.cuda.synchronize()
     f.close()
 
+# Cartesian expansions (cart.cu): every operator, all modes
+xyz, q = make_particles(5000, "plummer", 7)
+X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
+f = FMM(p=4, theta=0.5, ncrit=16, tune=False)
+f.set_basis("cartesian")
+f.set_cost_model(*COST)
+for mode in ("fmm", "treecode", "hybrid"):
+    f.set_mode(mode)
+    phi, grad = f.evaluate(X, Q)
+    torch.cuda.synchronize()
+    print("cartesian", mode, float(phi.abs().sum()), flush=True)
+f.close()
+
 # traversal overflow-and-retry paths (stack / list scratch and list buffers far too small, small
 # theta = long lists): the retried traversal must not read past any buffer
 os.environ["FMM_TRAV_CAP"] = "32"
