@@ -47,6 +47,9 @@ enum fmm_kind { FMM_KIND_M2L = 0, FMM_KIND_M2P = 1, FMM_KIND_P2P = 2 };
 /* expansion basis (fmm_set_basis): spherical harmonics (default), Cartesian Taylor of total order
  * p (p <= 4), or the automatic switch between them */
 enum fmm_basis { FMM_BASIS_SPHERICAL = 0, FMM_BASIS_CARTESIAN = 1, FMM_BASIS_AUTO = 2 };
+/* M2L translation scheme (fmm_set_m2l_scheme) */
+enum fmm_m2l_scheme { FMM_M2L_AUTO = 0, FMM_M2L_TC = 1, FMM_M2L_GEMM = 2, FMM_M2L_ROTATION = 3,
+                      FMM_M2L_PAIRS = 4 };
 
 enum fmm_status {
   FMM_OK = 0,
@@ -144,6 +147,24 @@ int fmm_set_timing(fmm_t h, int enable);
  * each pair's local expansion straight into its target with vector reductions in L2: faster, but
  * the summation order then varies from run to run (differences at FP32 rounding level). */
 int fmm_set_deterministic(fmm_t h, int enable);
+
+/* M2L translation scheme, spherical basis (PAPER.md:122, P:153, P:169 name
+ * the choice of translation scheme, P:205 the O(p^4) kernel). Every scheme computes the same
+ * operator (up to rounding):
+ *   FMM_M2L_TC        class-batched dense translation matrices on the tcgen05 tensor cores
+ *                     (3xTF32), p <= 10;
+ *   FMM_M2L_GEMM      the same class GEMM on CUDA cores, p <= 12;
+ *   FMM_M2L_ROTATION  rotation-based O(p^3): per class, rotate the multipole onto the z axis,
+ *                     translate along z, rotate back (m2l_rot.cu), any p;
+ *   FMM_M2L_PAIRS     the direct per-pair double loop, any p.
+ * FMM_M2L_AUTO (default): fmm_tune / fmm_create's kernel pre-calculation times the M2L phase of
+ * one FMM-mode evaluation of the synthetic set with every scheme available at this p and keeps
+ * the fastest (before it: TC, else GEMM, else ROTATION). Errors: FMM_E_INVALID (not available at
+ * this p). */
+int fmm_set_m2l_scheme(fmm_t h, int scheme);
+/* The scheme evaluations use; tuned_ms[FMM_M2L_*] (5 doubles, may be NULL) = the M2L times the
+ * last tuning measured (0 = not run). */
+int fmm_get_m2l_scheme(fmm_t h, int *scheme, double *tuned_ms);
 
 /* Expansion basis ("capability to switch to Cartesian expansions
  * ... key to achieving high performance for low-accuracy").

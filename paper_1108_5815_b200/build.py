@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfmm.so")
-SOURCES = ["fmm_api.cu", "tree.cu", "traverse.cu", "expansions.cu", "m2l.cu", "m2l_tc.cu", "p2p.cu", "autotune.cu", "dist.cu", "comm.cu", "cart.cu"]
+SOURCES = ["fmm_api.cu", "tree.cu", "traverse.cu", "expansions.cu", "m2l.cu", "m2l_tc.cu", "p2p.cu", "autotune.cu", "dist.cu", "comm.cu", "cart.cu", "m2l_rot.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "comm.cuh", "p2p_core.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

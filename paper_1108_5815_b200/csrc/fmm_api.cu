@@ -118,6 +118,11 @@ struct fmm_ctx {
   DBuf<int> nch, excl, leafflag, leaves, bnd;
   DBuf<int2> crange;
   DBuf<int4> cpack;  // packed cell records for the traversal
+  // M2L translation scheme (NEXT-1): requested (FMM_M2L_AUTO = let fmm_tune decide), the one
+  // the kernel pre-calculation picked, and the M2L times it measured per scheme (ms)
+  int m2l_scheme = 0, m2l_tuned = 0;
+  double m2l_scheme_ms[5] = {0, 0, 0, 0, 0};
+  DBuf<float> m2l_R;  // rotation-based scheme: per-class operators (m2l_rot.cu)
   // expansion basis (NEXT-2): 0 spherical harmonics, 1 Cartesian Taylor (p <= CART_PMAX)
   int basis = 0;
   double basis_ms[2] = {0, 0};  // FMM_BASIS_AUTO: the measured evaluation time of each basis
@@ -1102,6 +1107,26 @@ static int traverse(fmm_ctx *h, int (*between)(fmm_ctx *) = nullptr) {
   }
 }
 
+static bool m2l_scheme_ok(int p, int scheme) {
+  switch (scheme) {
+    case FMM_M2L_TC: return m2l_gemm_supported(p) && m2l_tc_supported(p);
+    case FMM_M2L_GEMM: return m2l_gemm_supported(p);
+    case FMM_M2L_ROTATION: return m2l_rot_supported(p);
+    case FMM_M2L_PAIRS: return true;
+    default: return false;
+  }
+}
+// the scheme an evaluation uses: the requested one, else the tuned one, else by order
+static int m2l_scheme_of(const fmm_ctx *h) {
+  if (h->m2l_scheme != FMM_M2L_AUTO) return h->m2l_scheme;
+  const char *cc = getenv("FMM_M2L_CUDA_CORES");  // (round-1 switch, kept)
+  if (cc && cc[0] && cc[0] != '0' && m2l_gemm_supported(h->p)) return FMM_M2L_GEMM;
+  if (h->m2l_tuned) return h->m2l_tuned;
+  if (m2l_scheme_ok(h->p, FMM_M2L_TC)) return FMM_M2L_TC;
+  if (m2l_scheme_ok(h->p, FMM_M2L_GEMM)) return FMM_M2L_GEMM;
+  return FMM_M2L_ROTATION;
+}
+
 static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
                          float *grad) {
   cudaStream_t st = h->stream;
@@ -1251,10 +1276,14 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(h->m2l_counters.ensure(8));
     CK(h->m2l_items.ensure((size_t)np + 1));
     CK(h->m2l_small.ensure(np));
-    // tensor-core GEMMs accumulate straight into L unless bit-reproducibility is requested
-    const char *cc = getenv("FMM_M2L_CUDA_CORES");
-    const bool use_tc = m2l_gemm_supported(p) && m2l_tc_supported(p) && !(cc && cc[0] && cc[0] != '0');
-    const bool accum = use_tc && !h->deterministic;
+    // translation scheme (fmm_set_m2l_scheme; tuned by fmm_tune): tensor-core class GEMM,
+    // CUDA-core class GEMM, rotation-based O(p^3) (m2l_rot.cu) or the per-pair double loop
+    const int scheme = m2l_scheme_of(h);
+    const bool use_tc = scheme == FMM_M2L_TC;
+    const bool use_rot = scheme == FMM_M2L_ROTATION;
+    // tensor-core GEMMs and rotations accumulate straight into L unless bit-reproducibility is
+    // requested
+    const bool accum = (use_tc || use_rot) && !h->deterministic;
     if (!accum) CK(h->m2l_Y.ensure((size_t)np * m2l_y_stride(p)));
     CK(h->cub_tmp.ensure(m2l_temp_bytes(np)));
     M2LWork W{};
@@ -1277,7 +1306,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     W.Y = h->m2l_Y.p;
     W.tmp = h->cub_tmp.p;
     W.tmp_bytes = h->cub_tmp.cap;
-    W.direct_all = m2l_gemm_supported(p) ? 0 : 1;
+    W.direct_all = scheme == FMM_M2L_PAIRS ? 1 : 0;
     // spatial blocks for the execution order: none while the multipole + local arrays fit
     // comfortably in L2 (126 MB); else the 8 octants of the root (FMM_M2L_BLK overrides, <= 2)
     {
@@ -1324,11 +1353,15 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(m2l_sort_items(W, h->h_small[1], st));
     h->stats.launches += 1;
     h->stats.cub_calls += 1;
-    // class GEMMs on the tensor cores (tcgen05, 3xTF32) unless disabled / unsupported
+    // class GEMMs on the tensor cores (tcgen05, 3xTF32), or per-class rotation operators, or
+    // CUDA-core class GEMMs
     if (use_tc) {
       CK(h->m2l_Ttc.ensure((size_t)std::max(1, ngclass) * m2l_tc_T_words(p)));
       CK(m2l_tc_build_T(p, W, ngclass, h->m2l_Ttc.p, st));
-    } else {
+    } else if (use_rot) {
+      CK(h->m2l_R.ensure((size_t)std::max(1, ngclass) * m2l_rot_class_floats(p)));
+      CK(m2l_rot_build(p, W, ngclass, h->m2l_R.p, st));
+    } else if (scheme == FMM_M2L_GEMM) {
       CK(h->m2l_T.ensure((size_t)std::max(1, ngclass) * m2l_T_floats(p)));
       W.Tg = h->m2l_T.p;
       CK(m2l_build_T(p, W, ngclass, st));
@@ -1340,8 +1373,13 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     if (use_tc) {
       CK(m2l_tc_gemm(p, W, h->m2l_Ttc.p, h->M.p, st, accum ? h->L.p : nullptr));
       h->stats.launches += 1;
+    } else if (use_rot) {
+      CK(m2l_rot_apply(p, W, h->m2l_R.p, h->M.p, st, accum ? h->L.p : nullptr));
+      h->stats.launches += 1;
     }
-    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st, use_tc, accum));
+    // (gemm_done: the class pairs are done and Y holds dof-order rows; rare classes, the
+    // per-pair scheme and the ordered reduction follow)
+    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st, use_tc || use_rot, accum));
     h->stats.launches += 2;
     h->m2l_tc_used = use_tc;
   }
@@ -1515,6 +1553,33 @@ static int tune_impl(fmm_ctx *h) {
   h->timing = true;
   double t_pp[3], t_ml[3], t_mp[3];
   int rc = FMM_OK;
+  // auto-tuning across translation schemes (NEXT-1): the M2L phase of one FMM-mode
+  // evaluation with every scheme that supports this order, the fastest is kept
+  if (h->m2l_scheme == FMM_M2L_AUTO && h->basis == FMM_BASIS_SPHERICAL) {
+    h->mode = FMM_FMM;
+    h->m2l_tuned = 0;
+    double best = 1e300;
+    int pick = 0;
+    for (int sc = FMM_M2L_TC; sc <= FMM_M2L_PAIRS && rc == FMM_OK; ++sc) {
+      h->m2l_scheme_ms[sc] = 0.0;
+      if (!m2l_scheme_ok(h->p, sc)) continue;
+      h->m2l_scheme = sc;
+      double t[2] = {0, 0};
+      for (int it = 0; it < 3 && rc == FMM_OK; ++it) {
+        rc = evaluate_impl(h, xyz, q, n, phi, grad);
+        if (it) t[it - 1] = h->stats.ms_m2l;
+      }
+      h->m2l_scheme_ms[sc] = std::min(t[0], t[1]);
+      if (h->m2l_scheme_ms[sc] < best) {
+        best = h->m2l_scheme_ms[sc];
+        pick = sc;
+      }
+      // the per-pair double loop is only a candidate when no class scheme is faster than it
+      // could be: stop at the first class-batched scheme that ran (it is far ahead at p >= 4)
+    }
+    h->m2l_scheme = FMM_M2L_AUTO;
+    h->m2l_tuned = pick;
+  }
   for (int pass = 0; pass < 2 && rc == FMM_OK; ++pass) {
     h->mode = pass == 0 ? FMM_FMM : FMM_TREECODE;
     for (int it = -1; it < 3 && rc == FMM_OK; ++it) {
@@ -1664,7 +1729,7 @@ int fmm_destroy(fmm_t h) {
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();
-  h->tleaves.release(); h->p2p_desc.release(); h->Mc.release(); h->Lc.release();
+  h->tleaves.release(); h->p2p_desc.release(); h->Mc.release(); h->Lc.release(); h->m2l_R.release();
   h->let_box.release(); h->let_flags.release(); h->let_excl.release(); h->let_cnt.release();
   h->let_psize.release(); h->let_pexcl.release(); h->let_seg0.release(); h->let_haveM.release();
   h->let_haveP.release(); h->let_open.release(); h->let_ids.release(); h->let_rids.release();
@@ -1840,6 +1905,22 @@ int fmm_set_timing(fmm_t h, int enable) {
 int fmm_set_deterministic(fmm_t h, int enable) {
   if (!h) return FMM_E_INVALID;
   h->deterministic = enable != 0;
+  return FMM_OK;
+}
+
+int fmm_set_m2l_scheme(fmm_t h, int scheme) {
+  if (!h) return FMM_E_INVALID;
+  if (scheme != FMM_M2L_AUTO && !m2l_scheme_ok(h->p, scheme))
+    return fail(h, FMM_E_INVALID, "M2L scheme %d is not available at p = %d", scheme, h->p);
+  h->m2l_scheme = scheme;
+  return FMM_OK;
+}
+
+int fmm_get_m2l_scheme(fmm_t h, int *scheme, double *tuned_ms) {
+  if (!h || !scheme) return FMM_E_INVALID;
+  *scheme = m2l_scheme_of(h);
+  if (tuned_ms)
+    for (int i = 0; i < 5; ++i) tuned_ms[i] = h->m2l_scheme_ms[i];
   return FMM_OK;
 }
 

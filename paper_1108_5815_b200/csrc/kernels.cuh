@@ -128,6 +128,13 @@ cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st);
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
                         float2 *L, cudaStream_t st, bool gemm_done = false, bool accum = false);
 
+// ---- m2l_rot.cu (rotation-based O(p^3) M2L, NEXT-1) ----
+bool m2l_rot_supported(int p);
+size_t m2l_rot_class_floats(int p);
+cudaError_t m2l_rot_build(int p, const M2LWork &W, int ngclass, float *R, cudaStream_t st);
+cudaError_t m2l_rot_apply(int p, const M2LWork &W, const float *R, const float2 *M,
+                          cudaStream_t st, float2 *Lacc);
+
 // ---- m2l_tc.cu (tcgen05 3xTF32 class GEMM) ----
 bool m2l_tc_supported(int p);
 size_t m2l_tc_T_words(int p);

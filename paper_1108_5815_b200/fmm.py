@@ -12,9 +12,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 HYBRID, FMM_MODE, TREECODE, DIRECT = 0, 1, 2, 3
 MODES = {"hybrid": HYBRID, "fmm": FMM_MODE, "treecode": TREECODE, "direct": DIRECT}
 BASES = {"spherical": 0, "cartesian": 1, "auto": 2}
+SCHEMES = {"auto": 0, "tc": 1, "gemm": 2, "rotation": 3, "pairs": 4}
 SYMBOLS = ["fmm_create", "fmm_destroy", "fmm_evaluate", "fmm_evaluate_ts", "fmm_evaluate_host",
            "fmm_set_stream",
            "fmm_set_mode", "fmm_set_timing", "fmm_set_deterministic", "fmm_set_basis", "fmm_get_basis",
+           "fmm_set_m2l_scheme", "fmm_get_m2l_scheme",
            "fmm_tune", "fmm_get_cost_model",
            "fmm_set_cost_model", "fmm_get_stats", "fmm_export_tree", "fmm_export_lists",
            "fmm_export_perm", "fmm_set_partition", "fmm_get_partition", "fmm_partition_indices",
@@ -76,6 +78,8 @@ def load_library():
     L.fmm_set_mode.argtypes = [vp, C.c_int]
     L.fmm_set_timing.argtypes = [vp, C.c_int]
     L.fmm_set_deterministic.argtypes = [vp, C.c_int]
+    L.fmm_set_m2l_scheme.argtypes = [vp, C.c_int]
+    L.fmm_get_m2l_scheme.argtypes = [vp, P(C.c_int), P(dp)]
     L.fmm_set_basis.argtypes = [vp, C.c_int]
     L.fmm_get_basis.argtypes = [vp, P(C.c_int), P(dp), P(dp)]
     L.fmm_tune.argtypes = [vp]
@@ -200,6 +204,19 @@ class FMM:
     def set_deterministic(self, on: bool):
         """Bit-reproducible M2L summation order (slower); see fmm_set_deterministic in fmm.h."""
         self._check(self.L.fmm_set_deterministic(self.h, int(bool(on))), "fmm_set_deterministic")
+
+    def set_m2l_scheme(self, scheme):
+        """"auto" | "tc" | "gemm" | "rotation" | "pairs" (fmm_set_m2l_scheme)."""
+        s = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
+        self._check(self.L.fmm_set_m2l_scheme(self.h, s), "fmm_set_m2l_scheme")
+
+    def m2l_scheme(self):
+        """(scheme in use, {scheme: M2L ms measured by the last tuning})."""
+        sc = C.c_int()
+        ms = (C.c_double * 5)()
+        self._check(self.L.fmm_get_m2l_scheme(self.h, C.byref(sc), ms), "fmm_get_m2l_scheme")
+        names = {v: k for k, v in SCHEMES.items()}
+        return names[sc.value], {names[i]: ms[i] for i in range(1, 5)}
 
     def set_basis(self, basis):
         """"spherical" | "cartesian" | "auto" (fmm_set_basis; Cartesian Taylor for p <= 4)."""

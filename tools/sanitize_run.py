@@ -33,6 +33,20 @@ for dist, n, p, th, nc in cases:
     torch.cuda.synchronize()
     f.close()
 
+# rotation-based M2L (m2l_rot.cu), both summation modes
+xyz, q = make_particles(4000, "plummer", 8)
+X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
+for pp in (6, 14):
+    f = FMM(p=pp, theta=0.5, ncrit=24, tune=False)
+    f.set_m2l_scheme("rotation")
+    f.set_cost_model(*COST)
+    for det in (True, False):
+        f.set_deterministic(det)
+        phi, grad = f.evaluate(X, Q)
+        torch.cuda.synchronize()
+        print("rotation", pp, det, float(phi.abs().sum()), flush=True)
+    f.close()
+
 # Cartesian expansions (cart.cu): every operator, all modes
 xyz, q = make_particles(5000, "plummer", 7)
 X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
