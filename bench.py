@@ -430,9 +430,9 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     tkey = "" if args.config == "C2" else "_" + args.config
-    p2p_line = {"bound": "alu", "kernel": "k_p2p_leaves", "achieved": p2p_gflops / 1e3,
+    p2p_line = {"bound": "alu", "kernel": "k_p2p_tma", "achieved": p2p_gflops / 1e3,
                 "peak": peak_gflops / 1e3, "unit": "TFLOP/s", "frac": p2p_gflops / peak_gflops,
-                "traffic": traffic.get("k_p2p_leaves" + tkey),
+                "traffic": traffic.get("k_p2p_tma" + tkey),
                 "peak_source": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING unit counts x "
                                "max clock); tools/peak_fp32 measured 74.0 TFLOP/s FFMA2",
                 "flop_per_pair": P2P_FLOP_PER_PAIR}
