@@ -18,6 +18,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 __constant__ short2 c_nm[nc_of(FMM_PMAX)];  // coefficient index -> (n, m) (also used by m2l.cu)
 
 static bool upload_nm_table() {
@@ -118,6 +120,126 @@ __global__ void __launch_bounds__(128, P2M_MINB) k_p2m(const int *__restrict__ l
       reinterpret_cast<float *>(M + (size_t)leaf * NCS)[o] = s;
     }
     __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// P2M, round 2: the same sums in groups of order columns m in [M0, M1) holding <= P2M_GROUP
+// complex coefficients, so the per-lane accumulators fit a small register budget (the one-pass
+// kernel above needs 2 NC accumulators: 255 registers, 8 warps per SM at p = 10). Per group the
+// lanes (one particle each) accumulate q conj(R_n^m) for its columns, then a padded shared-memory
+// transpose sums the 32 lanes in lane order (deterministic) and writes the group's coefficients.
+#ifndef P2M_GROUP
+#define P2M_GROUP 24
+#endif
+__host__ __device__ constexpr int p2m_group_end(int P, int m0) {
+  int m1 = m0, c = 0;
+  while (m1 <= P && (c + (P - m1 + 1) <= P2M_GROUP || m1 == m0)) {
+    c += P - m1 + 1;
+    ++m1;
+  }
+  return m1;
+}
+__host__ __device__ constexpr int p2m_group_coeffs(int P, int m0, int m1) {
+  int c = 0;
+  for (int m = m0; m < m1; ++m) c += P - m + 1;
+  return c;
+}
+template <int P, int M0, int M1>
+__device__ __forceinline__ void p2m_group(int leaf, const float4 g, float rinv, int b, int cnt,
+                                          const float4 *__restrict__ pos, float2 *__restrict__ M,
+                                          float *red, int lane) {
+  constexpr int G = p2m_group_coeffs(P, M0, M1), RS = 2 * G + 1, NCS = nc_stride(P);
+  float acc[2 * G];
+#pragma unroll
+  for (int o = 0; o < 2 * G; ++o) acc[o] = 0.f;
+  for (int c0 = 0; c0 < cnt; c0 += WARP) {
+    const bool valid = c0 + lane < cnt;
+    const float4 y = valid ? pos[b + c0 + lane] : make_float4(g.x, g.y, g.z, 0.f);
+    const float x = (y.x - g.x) * rinv, yy = (y.y - g.y) * rinv, z = (y.z - g.z) * rinv;
+    const float q = y.w;
+    const float r2 = x * x + yy * yy + z * z;
+    float2 Rmm = make_float2(1.f, 0.f);
+#pragma unroll
+    for (int m = 1; m <= M0; ++m) Rmm = cscale(cmul(Rmm, make_float2(x, yy)), -1.f / (2.f * m));
+    int o = 0;
+#pragma unroll
+    for (int m = M0; m < M1; ++m) {
+      if (m > M0) Rmm = cscale(cmul(Rmm, make_float2(x, yy)), -1.f / (2.f * m));
+      float2 R2 = make_float2(0.f, 0.f), R1 = Rmm;
+#pragma unroll
+      for (int n = m; n <= P; ++n) {
+        float2 Rn;
+        if (n == m) Rn = Rmm;
+        else if (n == m + 1) Rn = cscale(Rmm, z);
+        else {
+          const float inv = 1.f / ((float)(n - m) * (float)(n + m));
+          Rn = make_float2(((2 * n - 1) * z * R1.x - r2 * R2.x) * inv,
+                           ((2 * n - 1) * z * R1.y - r2 * R2.y) * inv);
+        }
+        if (n > m) {
+          R2 = R1;
+          R1 = Rn;
+        }
+        acc[o] += q * Rn.x;  // q conj(R)
+        acc[o + 1] -= q * Rn.y;
+        o += 2;
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int o = 0; o < 2 * G; ++o) red[lane * RS + o] = acc[o];
+  __syncwarp();
+  for (int o = lane; o < 2 * G; o += WARP) {
+    float sum = 0.f;
+    for (int l = 0; l < 32; ++l) sum += red[l * RS + o];
+    // group-local float o -> (m, n): columns m0.., each n = m..P, re/im
+    int c = o >> 1, m = M0;
+    while (c > P - m) {
+      c -= P - m + 1;
+      ++m;
+    }
+    const int n = m + c;
+    reinterpret_cast<float *>(M + (size_t)leaf * NCS)[2 * cidx(n, m) + (o & 1)] = sum;
+  }
+  __syncwarp();
+}
+template <int P, int M0>
+struct P2MGroups {
+  static constexpr int M1 = p2m_group_end(P, M0);
+  __device__ static void run(int leaf, const float4 g, float rinv, int b, int cnt,
+                             const float4 *pos, float2 *M, float *red, int lane) {
+    p2m_group<P, M0, M1>(leaf, g, rinv, b, cnt, pos, M, red, lane);
+    if constexpr (M1 <= P) P2MGroups<P, M1>::run(leaf, g, rinv, b, cnt, pos, M, red, lane);
+  }
+};
+__host__ __device__ constexpr int p2m_max_group(int P) {
+  int best = 0;
+  for (int m0 = 0; m0 <= P; m0 = p2m_group_end(P, m0)) {
+    const int c = p2m_group_coeffs(P, m0, p2m_group_end(P, m0));
+    best = c > best ? c : best;
+  }
+  return best;
+}
+#ifndef P2MG_MINB
+#define P2MG_MINB 4
+#endif
+template <int p>
+__global__ void __launch_bounds__(128, P2MG_MINB) k_p2m_g(const int *__restrict__ leaves, int nleaves,
+                                                         CellsView C, const float4 *__restrict__ pos,
+                                                         float2 *__restrict__ M) {
+  constexpr int RS = 2 * p2m_max_group(p) + 1;
+  extern __shared__ float sh_p2mg[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  float *red = sh_p2mg + wib * 32 * RS;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int li = gw; li < nleaves; li += nw) {
+    const int leaf = leaves[li];
+    const float4 g = C.geo[leaf];
+    const float rinv = 1.f / g.w;
+    const int b = C.beg[leaf], cnt = C.cnt[leaf];
+    P2MGroups<p, 0>::run(leaf, g, rinv, b, cnt, pos, M, red, lane);
   }
 }
 
@@ -435,10 +557,21 @@ M2LTiles make_m2l_tiles(int p) {
 void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4 *pos, float2 *M,
                 cudaStream_t st) {
   ensure_nm_table();
+  static const bool one_pass = getenv("FMM_P2M_ONEPASS") != nullptr;  // A/B: round-1 kernel
+  if (one_pass) {
+    FMM_DISPATCH_P(p, ({
+      const size_t smem = 4 * 32 * (2 * nc_of(P_) + 1) * sizeof(float);
+      fmm_smem_optin((const void *)k_p2m<P_>, smem);
+      k_p2m<P_><<<warp_grid(nleaves, 4), 128, smem, st>>>(leaves, nleaves, C, pos, M);
+    }));
+    return;
+  }
+  // column groups (k_p2m_g). Measured at C4 (ncu, serialised): one-pass 2.65 ms, column groups
+  // 1.90 ms; a 2-D (particle slot x column pair) lane map 3.77 ms (divergent column loops)
   FMM_DISPATCH_P(p, ({
-    const size_t smem = 4 * 32 * (2 * nc_of(P_) + 1) * sizeof(float);
-    fmm_smem_optin((const void *)k_p2m<P_>, smem);
-    k_p2m<P_><<<warp_grid(nleaves, 4), 128, smem, st>>>(leaves, nleaves, C, pos, M);
+    const size_t smem = 4 * 32 * (2 * p2m_max_group(P_) + 1) * sizeof(float);
+    fmm_smem_optin((const void *)k_p2m_g<P_>, smem);
+    k_p2m_g<P_><<<warp_grid(nleaves, 4), 128, smem, st>>>(leaves, nleaves, C, pos, M);
   }));
 }
 void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st) {
