@@ -118,6 +118,10 @@ struct fmm_ctx {
   DBuf<int> nch, excl, leafflag, leaves, bnd;
   DBuf<int2> crange;
   DBuf<int4> cpack;  // packed cell records for the traversal
+  DBuf<int> tc_bnd;     // cooperative tree build: child bounds [8][cells of a level]
+  DBuf<int2> tc_crange; // ... child ranges
+  int *d_tree_st = nullptr;  // ... its results (64 ints; [4] = the short sort's redo flag)
+  bool sort_redo = false;
   // M2L translation scheme (NEXT-1): requested (FMM_M2L_AUTO = let fmm_tune decide), the one
   // the kernel pre-calculation picked, and the M2L times it measured per scheme (ms)
   int m2l_scheme = 0, m2l_tuned = 0;
@@ -313,6 +317,7 @@ static double now_ms() {
 // Level-synchronous adaptive octree over n particles (a4/a5): one host readback of the child count
 // per level. keys = sorted Morton keys; nloc < 0: the keys are all n particles (single GPU);
 // nloc >= 0: they are this rank's local shard and the split bounds are allreduced (dist.cu).
+static bool host_levels_mode() { return getenv("FMM_TREE_LEVELS") != nullptr; }
 static int build_levels(fmm_ctx *h, int64_t n, const uint64_t *keys, int nloc) {
   cudaStream_t st = h->stream;
   // level-synchronous adaptive octree: one host readback of the child count per level
@@ -328,6 +333,44 @@ static int build_levels(fmm_ctx *h, int64_t n, const uint64_t *keys, int nloc) {
     if ((e = h->cgeo.ensure_keep(need, keep, st))) return e;
     return h->cprefix.ensure_keep(need, keep, st);
   };
+  // single GPU: the whole level loop in one cooperative kernel (tree.cu k_tree_coop) and ONE
+  // read-back; capacity from the previous tree (retried larger on overflow). FMM_TREE_LEVELS=1
+  // keeps the host-driven loop below (also used by the distributed build).
+  static const bool host_levels = getenv("FMM_TREE_LEVELS") != nullptr;
+  if (nloc < 0 && !host_levels && n < ((int64_t)1 << 30)) {
+    size_t ccap = std::max(cap, (size_t)(1.3 * h->ncells) + 1024);
+    const int grid = tree_coop_grid();
+    for (int attempt = 0; attempt < 6; ++attempt) {
+      CK(ensure_cells(ccap, 0));
+      CK(h->tc_bnd.ensure(8 * ccap));
+      CK(h->tc_crange.ensure(8 * ccap));
+      CK(h->nch.ensure(ccap));
+      CK(h->excl.ensure((size_t)grid + 1));
+      CK(h->leaves.ensure(ccap));
+      CK(launch_tree_coop(keys, (int)n, h->ncrit, h->d_root, h->cells(), h->cprefix.p, (int)ccap,
+                          h->tc_bnd.p, h->nch.p, h->tc_crange.p, h->excl.p, h->d_tree_st,
+                          h->leaves.p, grid, st));
+      h->stats.launches += 1;
+      int hs[64];
+      CK(cudaMemcpyAsync(hs, h->d_tree_st, sizeof hs, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      h->sort_redo = hs[4] != 0;
+      if (hs[1]) {  // the cell capacity was too small: larger, again
+        ccap *= 2;
+        continue;
+      }
+      h->ncells = hs[0];
+      h->depth = hs[2];
+      h->nleaves = hs[3];
+      h->level_off.assign(hs + 8, hs + 8 + h->depth + 1);
+      h->level_cnt.assign(hs + 32, hs + 32 + h->depth + 1);
+      // (scratch the partition / target-set code after the build expects, as the host path)
+      CK(h->leafflag.ensure(h->ncells));
+      CK(h->excl.ensure(h->ncells));
+      return FMM_OK;
+    }
+    return fail(h, FMM_E_OOM, "octree cells do not fit");
+  }
   CK(ensure_cells(cap, 0));
   launch_root_cell(n, h->d_root, h->cells(), h->cprefix.p, st);
   CKL();
@@ -395,15 +438,43 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
   CK(h->acc.ensure(n));
   launch_keys(xyz, n, h->d_root, h->keys_in.p, h->idx_in.p, st);
   CKL();
-  size_t bytes = 0;
-  CK(sort_keys(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
-  CK(h->cub_tmp.ensure(bytes));
-  CK(sort_keys(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
-  ++h->stats.cub_calls;
-  launch_gather(xyz, q, h->perm.p, n, h->pos.p, st);
-  CKL();
-
-  if (int rc = build_levels(h, n, h->keys.p, -1)) return rc;
+  // a3: 6 radix passes over key bits 16..62 + a tie fix-up (tree.cu), exactly the order of the
+  // full 63-bit stable sort; a run of equal high bits longer than 64 (a very dense cluster)
+  // flags a redo with all 8 passes, found in the tree build's single read-back
+  static const bool full_sort = getenv("FMM_SORT_FULL") != nullptr;
+  bool short_sort = !full_sort;
+  for (int pass = 0; pass < 2; ++pass) {
+    size_t bytes = 0;
+    CK(cudaMemsetAsync(h->d_tree_st + 4, 0, sizeof(int), st));
+    if (short_sort) {
+      CK(sort_keys_short(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n,
+                         h->d_tree_st + 4, st));
+      CK(h->cub_tmp.ensure(bytes));
+      CK(sort_keys_short(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n,
+                         h->d_tree_st + 4, st));
+      h->stats.launches += 1;
+    } else {
+      CK(sort_keys(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
+      CK(h->cub_tmp.ensure(bytes));
+      CK(sort_keys(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
+    }
+    ++h->stats.cub_calls;
+    launch_gather(xyz, q, h->perm.p, n, h->pos.p, st);
+    CKL();
+    h->sort_redo = false;
+    if (int rc = build_levels(h, n, h->keys.p, -1)) return rc;
+    if (!short_sort) break;
+    if (!h->sort_redo) {  // the host-driven level loop does not read the flag: check it here
+      if (host_levels_mode()) {
+        int f = 0;
+        CK(cudaMemcpyAsync(&f, h->d_tree_st + 4, sizeof f, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        h->sort_redo = f != 0;
+      }
+      if (!h->sort_redo) break;
+    }
+    short_sort = false;  // a long run of equal high bits: sort all 63 bits and build again
+  }
   const int total = h->ncells;
   // target leaves of this handle's partition
   h->part_lo = 0;
@@ -1698,6 +1769,7 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
         cudaMalloc(&h->d_small, 16 * sizeof(int)) || cudaMalloc(&h->d_overflow, sizeof(unsigned)) ||
         cudaMalloc(&h->d_stats, 4 * sizeof(unsigned long long)) ||
         cudaMalloc(&h->d_bk, TRAV_BK_INTS * sizeof(int)) ||
+        cudaMalloc(&h->d_tree_st, 64 * sizeof(int)) ||
         cudaMallocHost(&h->h_small, 16 * sizeof(int))) {
       rc = fail(h, FMM_E_OOM, "small device allocations failed");
       break;
@@ -1729,7 +1801,8 @@ int fmm_destroy(fmm_t h) {
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();
-  h->tleaves.release(); h->p2p_desc.release(); h->Mc.release(); h->Lc.release(); h->m2l_R.release();
+  h->tleaves.release(); h->p2p_desc.release(); h->tc_bnd.release(); h->tc_crange.release();
+  if (h->d_tree_st) cudaFree(h->d_tree_st); h->Mc.release(); h->Lc.release(); h->m2l_R.release();
   h->let_box.release(); h->let_flags.release(); h->let_excl.release(); h->let_cnt.release();
   h->let_psize.release(); h->let_pexcl.release(); h->let_seg0.release(); h->let_haveM.release();
   h->let_haveP.release(); h->let_open.release(); h->let_ids.release(); h->let_rids.release();

@@ -12,6 +12,14 @@ void launch_keys(const float *xyz, int64_t n, const RootInfo *root, uint64_t *ke
                  cudaStream_t st);
 void launch_gather(const float *xyz, const float *q, const unsigned *perm, int64_t n, float4 *pos,
                    cudaStream_t st);
+cudaError_t sort_keys_short(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
+                            const unsigned *vin, unsigned *vout, int64_t n, int *flag,
+                            cudaStream_t st);
+int tree_coop_grid();
+cudaError_t launch_tree_coop(const uint64_t *keys, int n, int ncrit, const RootInfo *root,
+                             CellsView C, uint64_t *prefix, int cap, int *bnd, int *nch,
+                             int2 *crange, int *blk, int *st_dev, int *leaves, int grid,
+                             cudaStream_t st);
 cudaError_t sort_keys(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
                       const unsigned *vin, unsigned *vout, int64_t n, cudaStream_t st);
 cudaError_t exclusive_scan(void *tmp, size_t &tmp_bytes, const int *in, int *out, int n,

@@ -307,6 +307,243 @@ __global__ void __launch_bounds__(256) k_part_indices(int lo, int cnt,
     out[i] = perm[lo + i];
 }
 
+// ---- a3 short sort: 6 radix passes over key bits [16, 63) + a tie fix-up -----------------------
+// Keys that agree in bits 16..62 (cells of level 16 shared by several particles) are rare; runs
+// of them are put in full-key order (stable: ties keep the index order of the stable pass) by one
+// thread each. A run longer than SORT_RUN_MAX flags the caller, which then sorts all 63 bits.
+#define SORT_LOW_BITS 16
+#define SORT_RUN_MAX 64
+__global__ void k_sort_fixup(uint64_t *__restrict__ keys, unsigned *__restrict__ vals, int64_t n,
+                             int *flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t hi = keys[i] >> SORT_LOW_BITS;
+    if ((keys[i + 1] >> SORT_LOW_BITS) != hi) continue;          // not inside a run
+    if (i > 0 && (keys[i - 1] >> SORT_LOW_BITS) == hi) continue;  // not the run's first element
+    int64_t e = i + 1;
+    while (e < n && (keys[e] >> SORT_LOW_BITS) == hi && e - i <= SORT_RUN_MAX) ++e;
+    if (e - i > SORT_RUN_MAX) {
+      atomicOr(flag, 1);
+      continue;
+    }
+    for (int64_t a = i + 1; a < e; ++a) {  // insertion sort by the full key (stable)
+      const uint64_t k = keys[a];
+      const unsigned v = vals[a];
+      int64_t b = a - 1;
+      while (b >= i && keys[b] > k) {
+        keys[b + 1] = keys[b];
+        vals[b + 1] = vals[b];
+        --b;
+      }
+      keys[b + 1] = k;
+      vals[b + 1] = v;
+    }
+  }
+}
+
+// ---- a4/a5 in one cooperative kernel (single GPU) ------------------------------------------------
+// The level loop of build_levels on the device: per level, the 8 child bounds of every cell by
+// binary search, the child counts, a grid-wide exclusive scan (block segments + one block scanning
+// the block totals) and the emission of the next level, separated by grid syncs -- no host round
+// trip per level. st[] (device): [0] total cells, [1] overflow (capacity), [2] depth,
+// [3] leaves, [8 + l] level offsets, [32 + l] level counts.
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+#define TREE_BLOCK 256
+__device__ __forceinline__ int block_excl_scan(int v, int *ws, int &total) {
+  // exclusive scan of one value per thread across the block; ws: 32 ints of shared memory
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < nw ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) ws[lane] = t;
+  }
+  __syncthreads();
+  total = ws[nw - 1];
+  const int r = x - v + (w ? ws[w - 1] : 0);
+  __syncthreads();
+  return r;
+}
+__global__ void __launch_bounds__(TREE_BLOCK) k_tree_coop(const uint64_t *__restrict__ keys, int n,
+                                                          int ncrit, const RootInfo *__restrict__ root,
+                                                          CellsView C, uint64_t *__restrict__ prefix,
+                                                          int cap, int *__restrict__ bnd,
+                                                          int *__restrict__ nch, int2 *__restrict__ crange,
+                                                          int *__restrict__ blk, int *__restrict__ st,
+                                                          int *__restrict__ leaves) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int ws[32];
+  const int G = gridDim.x, b = blockIdx.x;
+  const int gtid = b * blockDim.x + threadIdx.x, gthreads = G * blockDim.x;
+  if (gtid == 0) {
+    C.beg[0] = 0;
+    C.cnt[0] = n;
+    C.parent[0] = -1;
+    C.child0[0] = -1;
+    C.nchild[0] = 0;
+    prefix[0] = 0;
+    cell_geometry(0, 0, root, &C.grid[0], &C.geo[0]);
+    st[1] = 0;
+    st[8] = 0;
+    st[32] = 1;
+  }
+  int c0 = 0, nl = 1, total = 1, level = 0;
+  for (;; ++level) {
+    grid.sync();
+    // child bounds (one thread per (cell, octant)) -- as k_split
+    const int shift = 3 * (FMM_LEVELS - (level + 1));
+    for (int id = gtid; id < 8 * nl; id += gthreads) {
+      const int k = id >> 3, o = id & 7, c = c0 + k;
+      const int cb = C.beg[c], cn = C.cnt[c];
+      int l = cb;
+      if (split_cell(cn, ncrit, level)) {
+        const uint64_t tgt = prefix[c] * 8 + (uint64_t)o;
+        int r = cb + cn;
+        while (l < r) {
+          const int m = (l + r) >> 1;
+          if ((keys[m] >> shift) < tgt) l = m + 1;
+          else r = m;
+        }
+      }
+      bnd[id] = l;
+    }
+    grid.sync();
+    // child ranges and counts; each block owns the segment [s0, s1) of the level
+    const int seg = (nl + G - 1) / G, s0 = min(b * seg, nl), s1 = min(s0 + seg, nl);
+    int bsum = 0;
+    for (int k = s0 + threadIdx.x; k < s1; k += blockDim.x) {
+      const int c = c0 + k;
+      int cnt = 0;
+      if (split_cell(C.cnt[c], ncrit, level)) {
+        const int end = C.beg[c] + C.cnt[c];
+        for (int o = 0; o < 8; ++o) {
+          const int lo = bnd[8 * k + o], hi = o < 7 ? bnd[8 * k + o + 1] : end;
+          if (hi > lo) crange[8 * k + cnt++] = make_int2(lo, (hi - lo) | (o << 28));
+        }
+      }
+      nch[k] = cnt;
+      bsum += cnt;
+    }
+    for (int o = 16; o > 0; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = bsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+      blk[b] = t;
+    }
+    __syncthreads();
+    grid.sync();
+    // block 0: exclusive scan of the block totals; the next level's size
+    if (b == 0) {
+      int carry = 0;
+      for (int j0 = 0; j0 < G; j0 += blockDim.x) {
+        const int j = j0 + threadIdx.x;
+        const int v = j < G ? blk[j] : 0;
+        int tot;
+        const int e = block_excl_scan(v, ws, tot);
+        if (j < G) blk[j] = carry + e;
+        carry += tot;
+      }
+      if (threadIdx.x == 0) {
+        blk[G] = carry;
+        if (total + carry > cap) st[1] = 1;
+      }
+    }
+    grid.sync();
+    const int nnext = blk[G];
+    if (st[1] || nnext == 0) break;
+    // emit the children: block-local exclusive scan of the segment + the block's offset
+    int run = total + blk[b];
+    for (int k0 = s0; k0 < s1; k0 += blockDim.x) {
+      const int k = k0 + threadIdx.x;
+      const int m = k < s1 ? nch[k] : 0;
+      int tot;
+      const int e = block_excl_scan(m, ws, tot);
+      if (k < s1) {
+        const int c = c0 + k, first = run + e;
+        C.nchild[c] = m;
+        C.child0[c] = m ? first : -1;
+        const uint64_t pp = prefix[c];
+        for (int j = 0; j < m; ++j) {
+          const int2 r = crange[8 * k + j];
+          const int id = first + j, oct = (r.y >> 28) & 7;
+          C.beg[id] = r.x;
+          C.cnt[id] = r.y & 0x0fffffff;
+          C.parent[id] = c;
+          C.child0[id] = -1;
+          C.nchild[id] = 0;
+          const uint64_t cp = pp * 8 + (uint64_t)oct;
+          prefix[id] = cp;
+          cell_geometry(cp, level + 1, root, &C.grid[id], &C.geo[id]);
+        }
+      }
+      run += tot;
+    }
+    c0 = total;
+    nl = nnext;
+    total += nnext;
+    if (gtid == 0) {
+      st[8 + level + 1] = c0;
+      st[32 + level + 1] = nl;
+    }
+  }
+  // leaves in cell order (flag, grid-wide scan, scatter): the same segment scheme
+  grid.sync();
+  if (st[1]) return;
+  const int seg = (total + G - 1) / G, s0 = min(b * seg, total), s1 = min(s0 + seg, total);
+  int cnt = 0;
+  for (int c = s0 + threadIdx.x; c < s1; c += blockDim.x) cnt += C.nchild[c] == 0;
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    blk[b] = t;
+  }
+  __syncthreads();
+  grid.sync();
+  if (b == 0) {
+    int carry = 0;
+    for (int j0 = 0; j0 < G; j0 += blockDim.x) {
+      const int j = j0 + threadIdx.x;
+      const int v = j < G ? blk[j] : 0;
+      int tot;
+      const int e = block_excl_scan(v, ws, tot);
+      if (j < G) blk[j] = carry + e;
+      carry += tot;
+    }
+    if (threadIdx.x == 0) {
+      st[0] = total;
+      st[2] = level;
+      st[3] = carry;
+    }
+  }
+  grid.sync();
+  int run = blk[b];
+  for (int c0l = s0; c0l < s1; c0l += blockDim.x) {
+    const int c = c0l + threadIdx.x;
+    const int f = c < s1 ? (C.nchild[c] == 0) : 0;
+    int tot;
+    const int e = block_excl_scan(f, ws, tot);
+    if (f) leaves[run + e] = c;
+    run += tot;
+  }
+}
+
 // ---- host launchers --------------------------------------------------------------------------
 static int grid_for(int64_t n, int bs) {
   int64_t g = (n + bs - 1) / bs;
@@ -345,6 +582,30 @@ void launch_gather(const float *xyz, const float *q, const unsigned *perm, int64
 cudaError_t sort_keys(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
                       const unsigned *vin, unsigned *vout, int64_t n, cudaStream_t st) {
   return cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int)n, 0, 63, st);
+}
+// bits [16, 63) only (6 onesweep passes instead of 8), then the tie fix-up; *flag set => the
+// caller must redo the full sort
+cudaError_t sort_keys_short(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
+                            const unsigned *vin, unsigned *vout, int64_t n, int *flag,
+                            cudaStream_t st) {
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int)n,
+                                                  SORT_LOW_BITS, 63, st);
+  if (e || !tmp || n < 2) return e;
+  k_sort_fixup<<<grid_for(n, 256), 256, 0, st>>>(kout, vout, n, flag);
+  return cudaGetLastError();
+}
+// the cooperative tree build: grid size for this device (all blocks co-resident)
+int tree_coop_grid() {
+  return fmm_resident_blocks((const void *)k_tree_coop, TREE_BLOCK, 0);
+}
+cudaError_t launch_tree_coop(const uint64_t *keys, int n, int ncrit, const RootInfo *root,
+                             CellsView C, uint64_t *prefix, int cap, int *bnd, int *nch,
+                             int2 *crange, int *blk, int *st_dev, int *leaves, int grid,
+                             cudaStream_t st) {
+  void *args[] = {(void *)&keys, (void *)&n, (void *)&ncrit, (void *)&root, (void *)&C,
+                  (void *)&prefix, (void *)&cap, (void *)&bnd, (void *)&nch, (void *)&crange,
+                  (void *)&blk, (void *)&st_dev, (void *)&leaves};
+  return cudaLaunchCooperativeKernel((const void *)k_tree_coop, grid, TREE_BLOCK, args, 0, st);
 }
 cudaError_t exclusive_scan(void *tmp, size_t &tmp_bytes, const int *in, int *out, int n,
                            cudaStream_t st) {
