@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(128) k_m2p(const int *__restrict__ leaves, int
 // written to the caller's order: phi[perm[i]], grad[3 perm[i] + a].
 template <int p>
 #ifndef L2P_MINB
-#define L2P_MINB 6  // 80 registers: 6 resident blocks per SM (C2 downward 0.289 -> 0.256 ms)
+#define L2P_MINB 5  // 96 registers, no spills (round 2: C4 downward 3.28 -> 3.17 ms vs 6 blocks at 80)
 #endif
 __global__ void __launch_bounds__(128, L2P_MINB) k_l2p(const int *__restrict__ leaves, int nleaves,
                                              CellsView C, const float4 *__restrict__ pos,
