@@ -9,8 +9,8 @@ from collections import defaultdict
 ROWS = [  # (row, kernel-name prefixes)
     ("a1 bbox + root cube", ["k_bbox", "k_root"]),
     ("a2 Morton keys", ["k_keys"]),
-    ("a3 sort + gather", ["k_gather"]),
-    ("a4/a5 octree + geometry", ["k_split", "k_emit", "k_level_total", "k_leaf_", "k_root_cell",
+    ("a3 sort + gather", ["k_gather", "k_sort_fixup"]),
+    ("a4/a5 octree + geometry", ["k_tree_coop", "k_split", "k_emit", "k_level_total", "k_leaf_", "k_root_cell",
                                  ]),
     ("a7 P2M", ["k_p2m"]),
     ("a8 M2M (shift GEMM levels + reduce)", ["k_shift_m2m", "k_m2m"]),
