@@ -132,6 +132,7 @@ struct fmm_ctx {
   double basis_ms[2] = {0, 0};  // FMM_BASIS_AUTO: the measured evaluation time of each basis
   DBuf<float> Mc, Lc;           // Cartesian expansions [ncells][cart_stride(p)]
   DBuf<int4> p2p_desc;  // per target leaf: (begin, count, own P2P list offset, count | ancestor flag)
+  DBuf<int2> p2p_mrg;   // per target leaf: its P2P source ranges sorted and merged (parallel to p2p_rng)
   // sender-side local essential tree (let_send): flags, compacted entries, send / receive buffers
   cudaStream_t cmst = nullptr;  // its stream (the exchange overlaps the traversal)
   cudaEvent_t ev_let = nullptr;
@@ -1302,9 +1303,10 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
   auto near_field = [&](cudaStream_t ns) -> int {
     record_on(h, EV_P2P0, ns);
     CK(h->p2p_desc.ensure(std::max(ntl, 1)));
+    CK(h->p2p_mrg.ensure(std::max(h->p2p_rng.cap, (size_t)1)));
     launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p, h->d_small + 12,
-                      h->p2p_desc.p, ns);
-    h->stats.launches += 1;  // + the per-leaf descriptor pass
+                      h->p2p_desc.p, h->p2p_mrg.p, ns);
+    h->stats.launches += 1;  // + the per-leaf descriptor and range-merge passes
     CKL();
     record_on(h, EV_P2P, ns);
     if (h->ntask[FMM_KIND_M2P] > 0) {
@@ -1801,7 +1803,7 @@ int fmm_destroy(fmm_t h) {
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();
-  h->tleaves.release(); h->p2p_desc.release(); h->tc_bnd.release(); h->tc_crange.release();
+  h->tleaves.release(); h->p2p_desc.release(); h->p2p_mrg.release(); h->tc_bnd.release(); h->tc_crange.release();
   if (h->d_tree_st) cudaFree(h->d_tree_st); h->Mc.release(); h->Lc.release(); h->m2l_R.release();
   h->let_box.release(); h->let_flags.release(); h->let_excl.release(); h->let_cnt.release();
   h->let_psize.release(); h->let_pexcl.release(); h->let_seg0.release(); h->let_haveM.release();

@@ -193,9 +193,11 @@ void launch_cart_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsVi
                      cudaStream_t st);
 
 // ---- p2p.cu ----
-// desc: scratch of nleaves int4 (per-leaf work descriptors built by the launch)
+// desc: scratch of nleaves int4 (per-leaf work descriptors built by the launch); mrg: scratch
+// parallel to the P2P lists (their capacity) for the merged per-leaf source ranges
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                       const float4 *pos, float4 *acc, int *counter, int4 *desc, cudaStream_t st);
+                       const float4 *pos, float4 *acc, int *counter, int4 *desc, int2 *mrg,
+                       cudaStream_t st);
 void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cudaStream_t st);
 
 // ---- synthetic batches for the kernel pre-calculation (autotune.cu) ----

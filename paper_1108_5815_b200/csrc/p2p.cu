@@ -258,7 +258,14 @@ __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__r
 #ifndef P2Q_CPASYNC
 #define P2Q_CPASYNC 0  // producer copies with per-lane cp.async (1) or one TMA bulk copy per range (0)
 #endif
+#ifndef P2Q_QUAD
+#define P2Q_QUAD 1  // consumers: CTA-wide pool of 128 lanes x 4 targets (1) or per-warp 32 x 2 (0)
+#endif
+#if P2Q_QUAD
+#define P2Q_CHUNK 128  // most targets per chunk: the pool's 128 lanes x 4 targets, >= 1 slice each
+#else
 #define P2Q_CHUNK 64  // most targets per chunk: 32 lanes x 2 packed targets
+#endif
 // Ring of reduction buffers. A warp finishes a chunk's reduction before it releases the chunk's
 // last tile, and the producer reopens a stage only after all four warps released it: so when a
 // warp reaches the end of chunk j, every warp has released the tile P2Q_STAGES tiles back, hence
@@ -272,10 +279,54 @@ __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__r
 // targets go as 32 + rest (e.g. 40: 32 at S = 2 and 8 at S = 8 -> 0.625 of the slot-steps of one
 // 40-target chunk at S = 1); from 49 on one chunk costs no more than two.
 __device__ __forceinline__ int p2q_chunk(int rem) {
+#if P2Q_QUAD
+  return min(rem, P2Q_CHUNK);
+#else
   return rem >= 49 ? min(rem, P2Q_CHUNK) : (rem > 32 ? 32 : rem);
+#endif
 }
 
 enum { QF_FIRST = 1, QF_LAST = 2, QF_MASK = 4, QF_END = 8 };
+// desc.w bits: [0, 30) list count, 30: the list is the raw P2P list (else the merged runs of
+// k_p2p_merge), 31: a proper ancestor has a P2P list the producer must walk
+#define P2Q_RAW 0x40000000
+#define P2Q_CNT(w) ((w) & 0x3fffffff)
+
+#ifdef P2Q_TRACE  // tools-only build: a timeline of CTA 0's ring (device printf, globaltimer ns)
+__device__ __forceinline__ unsigned long long q_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#include <cstdio>
+#ifndef P2Q_TRACE_K0
+#define P2Q_TRACE_K0 0
+#endif
+__device__ unsigned long long g_q_tr[5][6][P2Q_TRACE];
+__device__ int g_q_trv[5][6][P2Q_TRACE];
+#define Q_TRACE(who_, ev_, k_, v_)                                                              \
+  do {                                                                                          \
+    if (blockIdx.x == 0 && (k_) >= P2Q_TRACE_K0 && (k_) < P2Q_TRACE_K0 + P2Q_TRACE) {          \
+      const int w_ = (who_) == 9 ? 4 : (who_);                                                  \
+      g_q_tr[w_][ev_][(k_) - P2Q_TRACE_K0] = q_now();                                           \
+      g_q_trv[w_][ev_][(k_) - P2Q_TRACE_K0] = (int)(v_);                                        \
+    }                                                                                           \
+  } while (0)
+__global__ void k_q_trace_dump() {
+  for (int w = 0; w < 5; ++w)
+    for (int e = 0; e < 6; ++e)
+      for (int k = 0; k < P2Q_TRACE; ++k)
+        if (g_q_tr[w][e][k])
+          printf("TR %d %d %d %d %llu\n", w == 4 ? 9 : w, e, k, g_q_trv[w][e][k], g_q_tr[w][e][k]);
+  for (int w = 0; w < 5; ++w)
+    for (int e = 0; e < 6; ++e)
+      for (int k = 0; k < P2Q_TRACE; ++k) g_q_tr[w][e][k] = 0;
+}
+#else
+#define Q_TRACE(who_, ev_, k_, v_) \
+  do {                         \
+  } while (0)
+#endif
 
 __device__ __forceinline__ unsigned q_saddr(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -314,16 +365,25 @@ __device__ __forceinline__ void q_bulk_g2s(void *dst, const void *src, unsigned 
 __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
     k_p2p_tma(const int *__restrict__ leaves, int nleaves, CellsView C, ListsView Ls,
               const float4 *__restrict__ pos, float4 *__restrict__ acc_out, float m1,
-              int *next_leaf, const int4 *__restrict__ desc) {
+              int *next_leaf, const int4 *__restrict__ desc, const int2 *__restrict__ mrg) {
   extern __shared__ __align__(128) float4 p2q_dyn[];  // [P2Q_STAGES][P2Q_TILE] source tiles
   float4(*tile)[P2Q_TILE] = reinterpret_cast<float4(*)[P2Q_TILE]>(p2q_dyn);
   __shared__ int4 meta[P2Q_STAGES];  // (leaf begin, count, flags, chunk start | size << 16)
   __shared__ __align__(8) unsigned long long full[P2Q_STAGES], empty[P2Q_STAGES];
+#if P2Q_QUAD
+  // per-lane partial sums of the chunk's last tile: [buffer][slot = slice * Q + quad][target]
+#ifndef P2Q_REDBUF
+#define P2Q_REDBUF 2  // 1: one buffer and a second consumer barrier after the reduction
+#endif
+  __shared__ __align__(16) float4 red[P2Q_REDBUF][32 * P2Q_CWARPS][4];
+  __shared__ int red_cnt[1];
+#else
   __shared__ __align__(16) float4 red[P2Q_RED][P2Q_CWARPS][P2Q_CHUNK];
   __shared__ int red_cnt[P2Q_RED];
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int b = 0; b < P2Q_RED; ++b) red_cnt[b] = 0;
+    for (int b = 0; b < (int)(sizeof(red_cnt) / sizeof(int)); ++b) red_cnt[b] = 0;
     for (int s = 0; s < P2Q_STAGES; ++s) {
       q_mbar_init(&full[s], P2Q_CPASYNC ? 33 : 1);  // (32 producer lanes' copies +) the meta
       q_mbar_init(&empty[s], P2Q_CWARPS);
@@ -339,7 +399,9 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
     bool open = false;
     int flags_pending = 0;
     auto open_tile = [&]() {
+      if (lane == 0) Q_TRACE(9, 0, k, 0);
       if (k >= P2Q_STAGES) q_mbar_wait(&empty[k % P2Q_STAGES], ((k / P2Q_STAGES) + 1) & 1);
+      if (lane == 0) Q_TRACE(9, 1, k, 0);
       fill = 0;
       open = true;
     };
@@ -349,6 +411,7 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
 #endif
       __syncwarp();  // every lane's expect_tx precedes the arrive
       if (lane == 0) {
+        Q_TRACE(9, 2, k, fill);
         meta[k % P2Q_STAGES] = make_int4(leaf, fill, flags, c0);
         q_mbar_arrive(&full[k % P2Q_STAGES]);
       }
@@ -396,7 +459,42 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
         }
       }
     };
-    auto emit_rng = [&](int2 r, int tb, int cw) { emit(r.x, r.y, tb, cw); };
+#ifndef P2Q_MERGE
+#define P2Q_MERGE 0  // per-batch sort + merge in the producer (superseded by k_p2p_merge)
+#endif
+    // A batch of (up to) 32 source ranges, one per lane, sorted by begin (bitonic, in registers)
+    // and merged where contiguous: the cells of a P2P list are largely Morton-contiguous runs
+    // (siblings), and a merged run is one bulk copy instead of several (the producer's copy issue
+    // is serialised over the lanes, and small leaves have many small ranges)
+    auto emit_rng = [&](int2 r, int tb, int cw) {
+#if P2Q_MERGE
+      int key = r.y > 0 ? r.x : 0x7fffffff, cnt = r.y > 0 ? r.y : 0;
+#pragma unroll
+      for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          const int pkey = __shfl_xor_sync(0xffffffffu, key, j);
+          const int pcnt = __shfl_xor_sync(0xffffffffu, cnt, j);
+          const bool lower = (lane & j) == 0, up = (lane & kk) == 0;
+          if (lower == up ? pkey < key : pkey > key) {
+            key = pkey;
+            cnt = pcnt;
+          }
+        }
+      }
+      const bool valid = cnt > 0;
+      const int pend = __shfl_up_sync(0xffffffffu, key + cnt, 1);
+      const bool head = valid && (lane == 0 || pend != key);
+      const unsigned heads = __ballot_sync(0xffffffffu, head);
+      const int nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+      const unsigned later = heads & ~(0xffffffffu >> (31 - lane));  // heads above this lane
+      const int last = (later ? __ffs(later) - 1 : nvalid) - 1;       // last lane of this run
+      const int rend = __shfl_sync(0xffffffffu, key + cnt, last < 0 ? 0 : last);
+      emit(key, head ? rend - key : 0, tb, cw);
+#else
+      emit(r.x, r.y, tb, cw);
+#endif
+    };
     // Leaves in batches of P2Q_BATCH per queue atomic; lane j holds the descriptor of leaf j of
     // the batch. Every global load is issued one step ahead of its use so that the producer does
     // not stall the ring on L2 latency: the next batch is claimed (and its descriptors loaded)
@@ -417,7 +515,13 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
       return make_int4(__shfl_sync(0xffffffffu, d.x, j), __shfl_sync(0xffffffffu, d.y, j),
                        __shfl_sync(0xffffffffu, d.z, j), __shfl_sync(0xffffffffu, d.w, j));
     };
-    auto load_rng = [&](int off, int ncell, int e0) {
+    // the leaf's own list: its merged source ranges (k_p2p_merge); ancestors' lists: raw ranges
+    auto load_rng = [&](int off, int dw, int e0) {  // dw: the leaf's desc.w
+      const int ncell = P2Q_CNT(dw);
+      if (e0 + lane >= ncell) return make_int2(0, 0);
+      return (dw & P2Q_RAW) ? Ls.p2p_rng[off + e0 + lane] : mrg[off + e0 + lane];
+    };
+    auto load_rng_raw = [&](int off, int ncell, int e0) {
       return e0 + lane < ncell ? Ls.p2p_rng[off + e0 + lane] : make_int2(0, 0);
     };
     int b0 = 0, nb0 = 0, b1 = 0, nb1 = 0;
@@ -428,22 +532,22 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
     int2 rfirst = make_int2(0, 0);  // first range batch of the current leaf (prefetched)
     if (nb0 > 0) {
       const int4 d = lane_desc(dl0, 0);
-      rfirst = load_rng(d.z, d.w & 0x7fffffff, 0);
+      rfirst = load_rng(d.z, d.w, 0);
     }
     while (nb0 > 0) {
       for (int j = 0; j < nb0; ++j) {
         const int4 d = lane_desc(dl0, j);
         const int4 dn = j + 1 < nb0 ? lane_desc(dl0, j + 1)
                                     : (nb1 > 0 ? lane_desc(dl1, 0) : make_int4(0, 0, 0, 0));
-        const int tb = d.x, tn = d.y, off = d.z, ncell = d.w & 0x7fffffff;
+        const int tb = d.x, tn = d.y, off = d.z, ncell = P2Q_CNT(d.w);
         const bool anc = d.w < 0;
         int2 rnext_leaf = make_int2(0, 0);
         for (int c0 = 0, nt = 0; c0 < tn; c0 += nt) {
           nt = p2q_chunk(tn - c0);
           const bool last_chunk = c0 + nt >= tn;
           const int cw = c0 | (nt << 16);  // chunk start | chunk size
-          int2 r = c0 == 0 ? rfirst : load_rng(off, ncell, 0);
-          if (last_chunk) rnext_leaf = load_rng(dn.z, dn.w & 0x7fffffff, 0);
+          int2 r = c0 == 0 ? rfirst : load_rng(off, d.w, 0);
+          if (last_chunk) rnext_leaf = load_rng(dn.z, dn.w, 0);
           // (1) the leaf itself first: the chunk's first tile starts with the leaf's own
           // particles (the consumers read their targets there) and is evaluated with the r = 0
           // mask, like every tile that holds own particles
@@ -453,15 +557,15 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
           // (2) the leaf's P2P list, then (rare) those of its ancestors: a P2P pair with a
           // non-leaf target applies to every particle under it
           for (int e0 = 0; e0 < ncell; e0 += 32) {
-            const int2 rn = e0 + 32 < ncell ? load_rng(off, ncell, e0 + 32) : make_int2(0, 0);
+            const int2 rn = e0 + 32 < ncell ? load_rng(off, d.w, e0 + 32) : make_int2(0, 0);
             if (r.x == tb) r.y = 0;  // the leaf itself: done above, masked
-            emit(r.x, r.y, tb, cw);
+            emit_rng(r, tb, cw);
             r = rn;
           }
           if (anc) {
             for (int a = C.parent[leaves[b0 + j]]; a >= 0; a = C.parent[a]) {
               const int aoff = Ls.off[2][a], an = Ls.cnt[2][a];
-              for (int e0 = 0; e0 < an; e0 += 32) emit_rng(load_rng(aoff, an, e0), tb, cw);
+              for (int e0 = 0; e0 < an; e0 += 32) emit_rng(load_rng_raw(aoff, an, e0), tb, cw);
             }
           }
           if (!open) open_tile();  // the chunk's last tile (possibly empty) carries QF_LAST
@@ -485,6 +589,93 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
   }
 
   // -------------------------------------------------------------------- consumer warps 0..3
+#if P2Q_QUAD
+  // The four consumer warps form one pool of 128 lanes. A chunk of nt targets is held as
+  // Q = ceil(nt / 4) quads (4 targets per lane in two packed pairs: every shared-memory source
+  // load feeds four pairs and two independent chains); the pool's lanes are Q quads x
+  // S = 128 / Q source slices (lane L: quad L % Q, slice L / Q takes sources L / Q, + S, ... of
+  // every tile). At the chunk's end the 4 consumer warps meet at a named barrier, each lane
+  // deposits its partial sums, and thread i sums target i's slices in slice order
+  // (deterministic).
+  {
+    const int L = threadIdx.x;  // 0 .. 32 * P2Q_CWARPS - 1
+    unsigned k = 0, chunk = 0;
+    f2x t[6];
+    f2x acc[8];
+    int Q = 1, S = 1, g = 0, h = 0, nt = 0, tb = 0, c0 = 0;
+    bool active = false;
+    for (;;) {
+      const int st = k % P2Q_STAGES;
+      if ((L & 31) == 0) Q_TRACE(L >> 5, 3, k, 0);
+      q_mbar_wait(&full[st], (k / P2Q_STAGES) & 1);
+      const int4 m = meta[st];
+      if ((L & 31) == 0) Q_TRACE(L >> 5, 4, k, m.y | ((m.w >> 16) << 16));
+      if (m.z & QF_END) break;
+      if (m.z & QF_FIRST) {
+        tb = m.x;
+        c0 = m.w & 0xffff;
+        nt = m.w >> 16;
+        Q = (nt + 3) >> 2;
+        S = (32 * P2Q_CWARPS) / Q;
+        g = L % Q;
+        h = L / Q;
+        active = h < S;
+        const float4 *src = m.y > c0 + nt - 1 ? tile[st] : pos + tb;
+        float4 tv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = 4 * g + e;
+          tv[e] = src[c0 + (i < nt ? i : 4 * g)];
+        }
+        t[0] = pk(m1 * tv[0].x, m1 * tv[1].x);
+        t[1] = pk(m1 * tv[0].y, m1 * tv[1].y);
+        t[2] = pk(m1 * tv[0].z, m1 * tv[1].z);
+        t[3] = pk(m1 * tv[2].x, m1 * tv[3].x);
+        t[4] = pk(m1 * tv[2].y, m1 * tv[3].y);
+        t[5] = pk(m1 * tv[2].z, m1 * tv[3].z);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = 0ull;
+      }
+      const int n = active ? m.y : 0;
+      if (m.z & QF_MASK)
+        p2p_tile_quad_rt<true>(tile[st], n, h, S, t, acc);
+      else
+        p2p_tile_quad_rt<false>(tile[st], n, h, S, t, acc);
+      if ((L & 31) == 0) Q_TRACE(L >> 5, 5, k, m.z);
+      ++k;
+      if (m.z & QF_LAST) {
+        float4(*rb)[4] = red[chunk % P2Q_REDBUF];
+        ++chunk;
+        if (active) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const float2 ph = upk(acc[4 * c]), gx = upk(acc[4 * c + 1]), gy = upk(acc[4 * c + 2]),
+                         gz = upk(acc[4 * c + 3]);
+            rb[h * Q + g][2 * c] = make_float4(ph.x, gx.x, gy.x, gz.x);
+            rb[h * Q + g][2 * c + 1] = make_float4(ph.y, gx.y, gy.y, gz.y);
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");
+        for (int i = L; i < nt; i += 32 * P2Q_CWARPS) {
+          const int gi = i >> 2, e = i & 3;
+          float4 v = rb[gi][e];
+          for (int hh = 1; hh < S; ++hh) {
+            const float4 u = rb[hh * Q + gi][e];
+            v.x += u.x;
+            v.y += u.y;
+            v.z += u.z;
+            v.w += u.w;
+          }
+          acc_out[tb + c0 + i] = v;
+        }
+        if (P2Q_REDBUF == 1) asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");
+      }
+      __syncwarp();
+      if ((L & 31) == 0) q_mbar_arrive(&empty[st]);
+    }
+    return;
+  }
+#else
   unsigned k = 0, chunk = 0;
   f2x tx = 0ull, ty = 0ull, tz = 0ull;
   f2x acc[4] = {0ull, 0ull, 0ull, 0ull};
@@ -575,33 +766,194 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
       if (lane == 0) q_mbar_arrive(&empty[st]);  // after the reduction (see P2Q_RED)
     }
   }
+#endif
 }
 
 // per target leaf: (begin, count, own P2P list offset, own list count | 1 << 31 when a proper
 // ancestor has a non-empty P2P list)
 __global__ void k_p2p_desc(const int *__restrict__ leaves, int nleaves, CellsView C, ListsView Ls,
-                           int4 *__restrict__ desc) {
+                           int4 *__restrict__ desc, int raw) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nleaves) return;
   const int leaf = leaves[i];
   bool anc = false;
   for (int a = C.parent[leaf]; a >= 0 && !anc; a = C.parent[a]) anc = Ls.cnt[2][a] > 0;
   desc[i] = make_int4(C.beg[leaf], C.cnt[leaf], Ls.off[2][leaf],
-                      Ls.cnt[2][leaf] | (anc ? (int)0x80000000u : 0));
+                      Ls.cnt[2][leaf] | (anc ? (int)0x80000000u : 0) | raw);
+}
+
+// Per target leaf, a warp merges the source ranges of the leaf's own P2P list AND of its
+// ancestors' lists (a P2P pair with a non-leaf target applies to every particle under it; in
+// hybrid mode a large target against a tiny source cell is P2P) where they are contiguous in
+// particle order (the cells of a P2P list are largely Morton-contiguous runs: siblings, the
+// children of a split neighbour), leaving the leaf itself out. The runs go to mrg[off ..] (the
+// slot of the leaf's own list) and desc.w = their count with the ancestor flag cleared, so the
+// producer warp of k_p2p_tma -- the bottleneck on small leaves -- issues fewer, longer bulk copies
+// and never walks the tree (measured with the oracle's lists: 88 ranges -> 23 runs per leaf of
+// < 20 particles, 109 -> 41 for 20-64). O(n) per list: the begins go into a shared-memory hash
+// table, each range finds the range starting at its end (its successor), and each run head (a
+// range nobody precedes) sums its chain. Fallback (the producer then walks the ancestors as
+// before): more than P2P_MERGE_MAX ranges, or more runs than the own list's slot holds.
+#define P2P_MERGE_MAX 256
+#ifndef P2P_MERGE_NT
+#define P2P_MERGE_NT 32  // leaves of more particles keep their raw ranges
+#endif
+#define P2P_MERGE_HT 512  // hash slots per warp (power of two, >= 2 x P2P_MERGE_MAX)
+__global__ void __launch_bounds__(128) k_p2p_merge(const int *__restrict__ leaves, int nleaves,
+                                                   CellsView C, ListsView Ls, int4 *__restrict__ desc,
+                                                   int2 *__restrict__ mrg) {
+  __shared__ int2 rr[4][P2P_MERGE_MAX];           // the ranges (own list, then ancestors')
+  __shared__ int ht[4][P2P_MERGE_HT];             // begin -> range index (-1: empty)
+  __shared__ short nx[4][P2P_MERGE_MAX];          // successor range (-1: none)
+  __shared__ short NX2[4][P2P_MERGE_MAX];         // pointer-jumping double buffer
+  __shared__ short hs[4][P2P_MERGE_MAX];          // the slot a range landed in
+  __shared__ unsigned char hp[4][P2P_MERGE_MAX];  // has a predecessor
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int2 *R = rr[w];
+  int *T = ht[w];
+  short *NX = nx[w], *HS = hs[w];
+  unsigned char *HP = hp[w];
+  for (int e = lane; e < P2P_MERGE_HT; e += 32) T[e] = -1;
+  auto slot = [](int key) { return (int)(((unsigned)key * 2654435761u) >> (32 - 9)) & (P2P_MERGE_HT - 1); };
+  for (int i = blockIdx.x * 4 + w; i < nleaves; i += gridDim.x * 4) {
+    const int leaf = leaves[i];
+    const int4 d = desc[i];  // (begin, count, own list offset, own count | ancestor flag)
+    const int tb = d.x, off = d.z, n0 = d.w & 0x7fffffff;
+    const bool anc = d.w < 0;
+    if (d.y > P2P_MERGE_NT) {  // large leaf: its consumers outpace the producer anyway
+      if (lane == 0) desc[i].w = d.w | P2Q_RAW;
+      continue;
+    }
+    __syncwarp();
+    // gather the ranges: own list, then every ancestor's (none of them is the leaf itself,
+    // which lies inside every ancestor's particle range)
+    int n = 0;
+    bool fits = true;
+    auto gather = [&](int loff, int lcnt) {
+      if (n + lcnt > P2P_MERGE_MAX) {
+        fits = false;
+        return;
+      }
+      for (int e = lane; e < lcnt; e += 32) {
+        int2 r = Ls.p2p_rng[loff + e];
+        if (r.x == tb) r.y = 0;
+        R[n + e] = r;
+      }
+      n += lcnt;
+    };
+    gather(off, n0);
+    if (anc)
+      for (int a = C.parent[leaf]; a >= 0 && fits; a = C.parent[a]) {
+        const int ac = Ls.cnt[2][a];
+        if (ac > 0) gather(Ls.off[2][a], ac);
+      }
+    if (!fits) {  // fallback: the raw own list, the producer walks the ancestors
+      if (lane == 0) desc[i].w = d.w | P2Q_RAW;
+      continue;
+    }
+    __syncwarp();
+    for (int e = lane; e < n; e += 32) {
+      const int2 r = R[e];
+      NX[e] = -1;
+      HP[e] = 0;
+      if (r.y > 0) {
+        int h = slot(r.x);
+        while (atomicCAS(&T[h], -1, e) != -1) h = (h + 1) & (P2P_MERGE_HT - 1);
+        HS[e] = (short)h;
+      }
+    }
+    __syncwarp();
+    for (int e = lane; e < n; e += 32) {
+      const int2 r = R[e];
+      if (r.y <= 0) continue;
+      const int end = r.x + r.y;
+      for (int h = slot(end);; h = (h + 1) & (P2P_MERGE_HT - 1)) {
+        const int j = T[h];
+        if (j < 0) break;
+        if (R[j].x == end) {
+          NX[e] = (short)j;
+          HP[j] = 1;
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    int m = 0;
+    for (int e0 = 0; e0 < n; e0 += 32) {
+      const int e = e0 + lane;
+      const bool head = e < n && R[e].y > 0 && !HP[e];
+      m += __popc(__ballot_sync(0xffffffffu, head));
+    }
+    const bool merged = m <= n0;  // the runs fit the own list's slot of mrg
+    if (merged) {
+      // last range of every chain by pointer jumping (NX[e] -> the chain's last range, in
+      // log2(run length) rounds, no divergent walks)
+      for (int e = lane; e < n; e += 32)
+        if (NX[e] < 0) NX[e] = (short)e;
+      __syncwarp();
+      short *A = NX, *B = NX2[w];
+      for (;;) {
+        bool changed = false;
+        for (int e = lane; e < n; e += 32) {
+          const short v = A[A[e]];
+          B[e] = v;
+          changed |= v != A[e];
+        }
+        __syncwarp();
+        short *t = A;
+        A = B;
+        B = t;
+        if (!__any_sync(0xffffffffu, changed)) break;
+      }
+      int mo = 0;
+      for (int e0 = 0; e0 < n; e0 += 32) {
+        const int e = e0 + lane;
+        bool head = false;
+        int2 run = make_int2(0, 0);
+        if (e < n) {
+          run = R[e];
+          head = run.y > 0 && !HP[e];
+          if (head) {
+            const int2 last = R[A[e]];
+            run.y = last.x + last.y - run.x;
+          }
+        }
+        const unsigned hb = __ballot_sync(0xffffffffu, head);
+        if (head) mrg[off + mo + __popc(hb & ((1u << lane) - 1u))] = run;
+        mo += __popc(hb);
+      }
+      if (lane == 0) desc[i].w = m;  // ancestors folded in: flag cleared
+    } else if (lane == 0) {
+      desc[i].w = d.w | P2Q_RAW;
+    }
+    __syncwarp();
+    for (int e = lane; e < n; e += 32)  // clear the used slots for the next leaf
+      if (R[e].y > 0) T[HS[e]] = -1;
+  }
 }
 
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
-                       const float4 *pos, float4 *acc, int *counter, int4 *desc, cudaStream_t st) {
+                       const float4 *pos, float4 *acc, int *counter, int4 *desc, int2 *mrg,
+                       cudaStream_t st) {
   static const bool legacy = getenv("FMM_P2P_LEGACY") != nullptr;  // A/B: round-1 kernel
   if (!legacy) {
     const size_t dyn = sizeof(float4) * P2Q_STAGES * P2Q_TILE;
     fmm_smem_optin((const void *)k_p2p_tma, dyn);
     const int res = fmm_resident_blocks((const void *)k_p2p_tma, P2Q_THREADS, dyn);
     if (nleaves <= 0) return;
-    k_p2p_desc<<<(nleaves + 255) / 256, 256, 0, st>>>(leaves, nleaves, C, Ls, desc);
+#ifndef P2Q_MERGE_PASS
+#define P2Q_MERGE_PASS 1
+#endif
+    k_p2p_desc<<<(nleaves + 255) / 256, 256, 0, st>>>(leaves, nleaves, C, Ls, desc,
+                                                       P2Q_MERGE_PASS ? 0 : P2Q_RAW);
+    if (P2Q_MERGE_PASS)
+      k_p2p_merge<<<std::min((nleaves + 3) / 4, 148 * 16), 128, 0, st>>>(leaves, nleaves, C, Ls, desc, mrg);
     const int b = std::max(1, std::min(res, (nleaves + P2Q_BATCH - 1) / P2Q_BATCH));
     cudaMemsetAsync(counter, 0, sizeof(int), st);
-    k_p2p_tma<<<b, P2Q_THREADS, dyn, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f, counter, desc);
+    k_p2p_tma<<<b, P2Q_THREADS, dyn, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f, counter, desc, mrg);
+#ifdef P2Q_TRACE
+    k_q_trace_dump<<<1, 1, 0, st>>>();
+#endif
     return;
   }
   const int resident = fmm_resident_blocks((const void *)k_p2p_leaves, P2P_WARPS * 32, 0);

@@ -195,3 +195,58 @@ __device__ __forceinline__ void p2p_tile_raw(const float4 *__restrict__ sp, int 
   }
 }
 
+
+// Four targets per lane (two packed target pairs) against one source: every shared-memory source
+// load feeds four pairs, and the two pairs give the scheduler two independent chains per source.
+// Accumulates straight into acc (no per-tile partial sums: P2P lists are near-field length).
+template <bool MASK, int S, int U>
+__device__ __forceinline__ void p2p_tile_quad(const float4 *__restrict__ sp, int ns, int h,
+                                              const f2x (&t)[6], f2x (&acc)[8]) {
+  const float4 *q = sp + h;
+  const float4 *endU = ns > (U - 1) * S ? sp + ns - (U - 1) * S : sp;
+  for (; q < endU; q += U * S) {
+    float4 s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) s[u] = q[u * S];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      p2p_raw<MASK>(s[u], t[0], t[1], t[2], acc[0], acc[1], acc[2], acc[3]);
+      p2p_raw<MASK>(s[u], t[3], t[4], t[5], acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+  for (; q < sp + ns; q += S) {
+    const float4 s0 = q[0];
+    p2p_raw<MASK>(s0, t[0], t[1], t[2], acc[0], acc[1], acc[2], acc[3]);
+    p2p_raw<MASK>(s0, t[3], t[4], t[5], acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// The same with a run-time slice count S (the CTA-wide lane pool of k_p2p_tma: S = 128 / Q for Q
+// target quads takes many values): two sources per unrolled step, the second one S float4 further.
+__device__ __forceinline__ float4 lds128(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+template <bool MASK>
+__device__ __forceinline__ void p2p_tile_quad_rt(const float4 *__restrict__ sp, int ns, int h, int S,
+                                                 const f2x (&t)[6], f2x (&acc)[8]) {
+  // 32-bit shared addresses (ptxas still forms them with two IMAD-immediates per step)
+  const unsigned base = (unsigned)__cvta_generic_to_shared(sp);
+  const unsigned sb = 16u * (unsigned)S, sb2 = 2u * sb;
+  unsigned a = base + 16u * (unsigned)h;
+  const unsigned end = base + 16u * (unsigned)ns;
+  const unsigned end2 = ns > S ? end - sb : base;
+  for (; a < end2; a += sb2) {
+    const float4 s0 = lds128(a), s1 = lds128(a + sb);
+    p2p_raw<MASK>(s0, t[0], t[1], t[2], acc[0], acc[1], acc[2], acc[3]);
+    p2p_raw<MASK>(s0, t[3], t[4], t[5], acc[4], acc[5], acc[6], acc[7]);
+    p2p_raw<MASK>(s1, t[0], t[1], t[2], acc[0], acc[1], acc[2], acc[3]);
+    p2p_raw<MASK>(s1, t[3], t[4], t[5], acc[4], acc[5], acc[6], acc[7]);
+  }
+  if (a < end) {
+    const float4 s0 = lds128(a);
+    p2p_raw<MASK>(s0, t[0], t[1], t[2], acc[0], acc[1], acc[2], acc[3]);
+    p2p_raw<MASK>(s0, t[3], t[4], t[5], acc[4], acc[5], acc[6], acc[7]);
+  }
+}

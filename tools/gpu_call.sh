@@ -1,0 +1,1 @@
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
