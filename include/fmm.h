@@ -99,6 +99,8 @@ typedef struct {
    * time of the exchange on its own stream, and how far it ran past the end of the traversal it
    * overlaps (0 = hidden; the near field and M2L wait for it) */
   double ms_let, ms_let_exposed;
+  /* the P2P kernel alone (ms_p2p also covers its per-leaf descriptor and range-merge passes) */
+  double ms_p2p_kernel;
 } fmm_stats_t;
 
 /* Create a handle on the current CUDA device. p = expansion order (coefficients n = 0..p,

@@ -66,7 +66,7 @@ struct DBuf {
 };
 
 enum { EV_START, EV_TREE, EV_UP, EV_TRAV, EV_M2L_PREP, EV_M2L, EV_P2P, EV_M2P, EV_DOWN, EV_P2P0,
-       EV_LET0, EV_LET1, EV_TRAV_END, EV_N };
+       EV_LET0, EV_LET1, EV_TRAV_END, EV_P2PK, EV_N };
 
 }  // namespace
 
@@ -1305,7 +1305,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     CK(h->p2p_desc.ensure(std::max(ntl, 1)));
     CK(h->p2p_mrg.ensure(std::max(h->p2p_rng.cap, (size_t)1)));
     launch_p2p_leaves(tl, ntl, h->cells(), h->lists(), h->pos.p, h->acc.p, h->d_small + 12,
-                      h->p2p_desc.p, h->p2p_mrg.p, ns);
+                      h->p2p_desc.p, h->p2p_mrg.p, ns, h->timing ? h->ev[EV_P2PK] : nullptr);
     h->stats.launches += 1;  // + the per-leaf descriptor and range-merge passes
     CKL();
     record_on(h, EV_P2P, ns);
@@ -1597,6 +1597,7 @@ static void read_phase_times(fmm_ctx *h) {
   h->stats.ms_m2l = el(EV_M2L_PREP, EV_M2L);
   // P2P / M2P: their own events (on aux when overlapping the M2L, which the phases then do)
   h->stats.ms_p2p = el(EV_P2P0, EV_P2P);
+  h->stats.ms_p2p_kernel = h->ntask[2] > 0 && h->mode != FMM_DIRECT ? el(EV_P2PK, EV_P2P) : 0.0;
   h->stats.ms_m2p = el(EV_P2P, EV_M2P);
   h->stats.ms_downward = (h->overlap && h->mode != FMM_DIRECT) ? el(EV_M2L, EV_DOWN) : el(EV_M2P, EV_DOWN);
   if (h->comm && !h->let_recv && h->mode != FMM_DIRECT) {

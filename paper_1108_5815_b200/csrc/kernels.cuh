@@ -197,7 +197,7 @@ void launch_cart_m2p(int p, const int *leaves, int nleaves, CellsView C, ListsVi
 // parallel to the P2P lists (their capacity) for the merged per-leaf source ranges
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
                        const float4 *pos, float4 *acc, int *counter, int4 *desc, int2 *mrg,
-                       cudaStream_t st);
+                       cudaStream_t st, cudaEvent_t ev_main = nullptr);
 void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cudaStream_t st);
 
 // ---- synthetic batches for the kernel pre-calculation (autotune.cu) ----

@@ -242,7 +242,11 @@ __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__r
 // warps per CTA (384 x 3, 8 CTAs per SM): 1.36 / 7.87 / 32.7; per-lane cp.async instead of TMA
 // bulk copies: 1.37 / 6.84 / 31.4; round-1 k_p2p_leaves: 1.32 / 7.33 / 31.6.
 #ifndef P2Q_TILE
+#if defined(P2Q_LASTRED) && P2Q_LASTRED
+#define P2Q_TILE 640  // 4 CTAs per SM with the P2Q_STAGES reduction buffers of the last-warp reduction
+#else
 #define P2Q_TILE 768
+#endif
 #endif
 #ifndef P2Q_STAGES
 #define P2Q_STAGES 3
@@ -372,11 +376,17 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
   __shared__ __align__(8) unsigned long long full[P2Q_STAGES], empty[P2Q_STAGES];
 #if P2Q_QUAD
   // per-lane partial sums of the chunk's last tile: [buffer][slot = slice * Q + quad][target]
-#ifndef P2Q_REDBUF
-#define P2Q_REDBUF 2  // 1: one buffer and a second consumer barrier after the reduction
+#ifndef P2Q_LASTRED
+#define P2Q_LASTRED 0  // 1: the last consumer warp to finish a chunk reduces it, no barrier (with
+                       // 640-particle tiles for the buffers: C4 P2P 28.4 ms vs 27.5, slower)
+#endif
+#if P2Q_LASTRED
+#define P2Q_REDBUF P2Q_STAGES  // see P2Q_RED
+#else
+#define P2Q_REDBUF 2  // the 4 consumer warps meet at a named barrier, then reduce together
 #endif
   __shared__ __align__(16) float4 red[P2Q_REDBUF][32 * P2Q_CWARPS][4];
-  __shared__ int red_cnt[1];
+  __shared__ int red_cnt[P2Q_REDBUF];
 #else
   __shared__ __align__(16) float4 red[P2Q_RED][P2Q_CWARPS][P2Q_CHUNK];
   __shared__ int red_cnt[P2Q_RED];
@@ -655,20 +665,40 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
             rb[h * Q + g][2 * c + 1] = make_float4(ph.y, gx.y, gy.y, gz.y);
           }
         }
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");
-        for (int i = L; i < nt; i += 32 * P2Q_CWARPS) {
-          const int gi = i >> 2, e = i & 3;
-          float4 v = rb[gi][e];
-          for (int hh = 1; hh < S; ++hh) {
-            const float4 u = rb[hh * Q + gi][e];
-            v.x += u.x;
-            v.y += u.y;
-            v.z += u.z;
-            v.w += u.w;
+        auto reduce = [&](int first, int step) {  // target i: its S slices in slice order
+          for (int i = first; i < nt; i += step) {
+            const int gi = i >> 2, e = i & 3;
+            float4 v = rb[gi][e];
+            for (int hh = 1; hh < S; ++hh) {
+              const float4 u = rb[hh * Q + gi][e];
+              v.x += u.x;
+              v.y += u.y;
+              v.z += u.z;
+              v.w += u.w;
+            }
+            acc_out[tb + c0 + i] = v;
           }
-          acc_out[tb + c0 + i] = v;
+        };
+#if P2Q_LASTRED
+        // lock-free: the last of the consumer warps to deposit its partials reduces the chunk,
+        // the others go on (a buffer is reused P2Q_STAGES chunks later, after every warp has
+        // released the tile that ended this chunk -- see P2Q_RED)
+        const int b = (chunk - 1) % P2Q_REDBUF;
+        __threadfence_block();
+        __syncwarp();
+        int prev = 0;
+        if ((L & 31) == 0) prev = atomicAdd(&red_cnt[b], 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == P2Q_CWARPS - 1) {
+          __threadfence_block();
+          reduce(L & 31, 32);
+          __syncwarp();
+          if ((L & 31) == 0) red_cnt[b] = 0;
         }
-        if (P2Q_REDBUF == 1) asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");
+#else
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");
+        reduce(L, 32 * P2Q_CWARPS);
+#endif
       }
       __syncwarp();
       if ((L & 31) == 0) q_mbar_arrive(&empty[st]);
@@ -934,7 +964,7 @@ __global__ void __launch_bounds__(128) k_p2p_merge(const int *__restrict__ leave
 
 void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls,
                        const float4 *pos, float4 *acc, int *counter, int4 *desc, int2 *mrg,
-                       cudaStream_t st) {
+                       cudaStream_t st, cudaEvent_t ev_main) {
   static const bool legacy = getenv("FMM_P2P_LEGACY") != nullptr;  // A/B: round-1 kernel
   if (!legacy) {
     const size_t dyn = sizeof(float4) * P2Q_STAGES * P2Q_TILE;
@@ -950,6 +980,7 @@ void launch_p2p_leaves(const int *leaves, int nleaves, CellsView C, ListsView Ls
       k_p2p_merge<<<std::min((nleaves + 3) / 4, 148 * 16), 128, 0, st>>>(leaves, nleaves, C, Ls, desc, mrg);
     const int b = std::max(1, std::min(res, (nleaves + P2Q_BATCH - 1) / P2Q_BATCH));
     cudaMemsetAsync(counter, 0, sizeof(int), st);
+    if (ev_main) cudaEventRecord(ev_main, st);  // the main kernel alone (bench roofline)
     k_p2p_tma<<<b, P2Q_THREADS, dyn, st>>>(leaves, nleaves, C, Ls, pos, acc, -1.0f, counter, desc, mrg);
 #ifdef P2Q_TRACE
     k_q_trace_dump<<<1, 1, 0, st>>>();

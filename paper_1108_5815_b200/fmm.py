@@ -45,7 +45,8 @@ class Stats(C.Structure):
                 ("n_global", C.c_int64), ("rank_lo", C.c_int64), ("rank_hi", C.c_int64),
                 ("n_straddle", C.c_int64), ("let_cells", C.c_int64), ("let_particles", C.c_int64),
                 ("bytes_sent", C.c_int64), ("ms_comm", C.c_double),
-                ("ms_let", C.c_double), ("ms_let_exposed", C.c_double)]
+                ("ms_let", C.c_double), ("ms_let_exposed", C.c_double),
+                ("ms_p2p_kernel", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
