@@ -1181,7 +1181,7 @@ static int traverse(fmm_ctx *h, int (*between)(fmm_ctx *) = nullptr) {
 
 static bool m2l_scheme_ok(int p, int scheme) {
   switch (scheme) {
-    case FMM_M2L_TC: return m2l_gemm_supported(p) && m2l_tc_supported(p);
+    case FMM_M2L_TC: return (m2l_gemm_supported(p) && m2l_tc_supported(p)) || m2l_tck_supported(p);
     case FMM_M2L_GEMM: return m2l_gemm_supported(p);
     case FMM_M2L_ROTATION: return m2l_rot_supported(p);
     case FMM_M2L_PAIRS: return true;
@@ -1428,7 +1428,12 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     h->stats.cub_calls += 1;
     // class GEMMs on the tensor cores (tcgen05, 3xTF32), or per-class rotation operators, or
     // CUDA-core class GEMMs
-    if (use_tc) {
+    // (10 < p <= 15: the K-tiled tensor-core GEMM, float-order operators and Y rows)
+    const bool use_tck = use_tc && !m2l_tc_supported(p);
+    if (use_tck) {
+      CK(h->m2l_Ttc.ensure((size_t)std::max(1, ngclass) * m2l_tck_T_words(p)));
+      CK(m2l_tck_build_T(p, W, ngclass, h->m2l_Ttc.p, st));
+    } else if (use_tc) {
       CK(h->m2l_Ttc.ensure((size_t)std::max(1, ngclass) * m2l_tc_T_words(p)));
       CK(m2l_tc_build_T(p, W, ngclass, h->m2l_Ttc.p, st));
     } else if (use_rot) {
@@ -1443,7 +1448,10 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     if (accum) CK(cudaMemsetAsync(h->L.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, st));
     CK(cudaStreamWaitEvent(st, h->ev_up, 0));  // join: the multipoles are complete
     record(h, EV_M2L_PREP);  // ms_m2l = the GEMM (+ the rare-class direct path / reduction)
-    if (use_tc) {
+    if (use_tck) {
+      CK(m2l_tck_gemm(p, W, h->m2l_Ttc.p, h->M.p, st, accum ? h->L.p : nullptr));
+      h->stats.launches += 1;
+    } else if (use_tc) {
       CK(m2l_tc_gemm(p, W, h->m2l_Ttc.p, h->M.p, st, accum ? h->L.p : nullptr));
       h->stats.launches += 1;
     } else if (use_rot) {
@@ -1452,7 +1460,8 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     }
     // (gemm_done: the class pairs are done and Y holds dof-order rows; rare classes, the
     // per-pair scheme and the ordered reduction follow)
-    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st, use_tc || use_rot, accum));
+    CK(m2l_execute(p, W, np, h->ncells, h->M.p, h->L.p, st, use_tc || use_rot, accum,
+                   use_tck ? 0 : -1));
     h->stats.launches += 2;
     h->m2l_tc_used = use_tc;
   }

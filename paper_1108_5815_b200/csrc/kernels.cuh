@@ -134,7 +134,8 @@ cudaError_t m2l_sort_items(const M2LWork &W, int nitems, cudaStream_t st);
 size_t m2l_T_floats(int p);
 cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st);
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
-                        float2 *L, cudaStream_t st, bool gemm_done = false, bool accum = false);
+                        float2 *L, cudaStream_t st, bool gemm_done = false, bool accum = false,
+                        int ydof = -1);  // Y rows in dof order (-1: when gemm_done)
 
 // ---- m2l_rot.cu (rotation-based O(p^3) M2L, NEXT-1) ----
 bool m2l_rot_supported(int p);
@@ -145,6 +146,12 @@ cudaError_t m2l_rot_apply(int p, const M2LWork &W, const float *R, const float2 
 
 // ---- m2l_tc.cu (tcgen05 3xTF32 class GEMM) ----
 bool m2l_tc_supported(int p);
+// K-tiled tcgen05 class GEMM for 10 < p <= 15 (float-order rows, Y in float order)
+bool m2l_tck_supported(int p);
+size_t m2l_tck_T_words(int p);
+cudaError_t m2l_tck_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg, cudaStream_t st);
+cudaError_t m2l_tck_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
+                         cudaStream_t st, float2 *Lacc);
 size_t m2l_tc_T_words(int p);
 cudaError_t m2l_tc_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg, cudaStream_t st);
 cudaError_t m2l_tc_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,

@@ -693,7 +693,8 @@ cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st) {
 }
 
 cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const float2 *M,
-                        float2 *L, cudaStream_t st, bool gemm_done, bool accum) {
+                        float2 *L, cudaStream_t st, bool gemm_done, bool accum, int ydof) {
+  if (ydof < 0) ydof = gemm_done ? 1 : 0;
   if (!W.direct_all && !gemm_done) {
     const size_t smem = m2l_gemm_smem(p);
     const int KR = 2 * nc_of(p);
@@ -720,15 +721,14 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
     const size_t smem = (size_t)4 * (nI + nM) * sizeof(float2);
     fmm_smem_optin((const void *)k_m2l_pairs, smem);
     k_m2l_pairs<<<148 * 4, 128, smem, st>>>(p, W.small, W.counters, W.pair_t, W.src, W.C, M, W.Y,
-                                            gemm_done ? 1 : 0,
-                                            accum ? reinterpret_cast<float *>(L) : nullptr);
+                                            ydof, accum ? reinterpret_cast<float *>(L) : nullptr);
   }
   if (!accum) {
-    const long long nthr = (long long)ncells * ((gemm_done ? dof_stride(p) : m2l_y_stride(p)) / 4);
+    const long long nthr = (long long)ncells * ((ydof ? dof_stride(p) : m2l_y_stride(p)) / 4);
     int b = (int)std::min<long long>((nthr + 255) / 256, 148 * 16);
     b = b > 0 ? b : 1;
     k_m2l_reduce<<<b, 256, 0, st>>>(p, ncells, W.off, W.cnt, W.Y, reinterpret_cast<float *>(L),
-                                    gemm_done ? 1 : 0);
+                                    ydof);
   }
   return cudaGetLastError();
 }

@@ -59,6 +59,17 @@ __device__ __forceinline__ unsigned f32_to_tf32(float x) {
   return r;
 }
 
+// x = hi + lo for 3xTF32: hi = x rounded to the nearest TF32 (half an ulp of the 13 dropped bits
+// added to the bit pattern, then truncated; the sign-magnitude format makes it round half away
+// from zero), lo = x - hi (exact in FP32, |lo| <= 2^-12 |x|) rounded the same way, so the split
+// loses <= 2^-24 |x| (a truncating split, hi = x & mask with the tensor core truncating lo: up to
+// 2^-22 -- measured: a 3x larger phi error floor vs direct at p = 11..15). 4 integer ops + 1 FADD
+// instead of two emulated cvt.rna.tf32.
+__device__ __forceinline__ void tf32_split(float x, unsigned &hi, unsigned &lo) {
+  hi = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+  lo = (__float_as_uint(x - __uint_as_float(hi)) + 0x1000u) & 0xFFFFE000u;
+}
+
 // tcgen05 wrappers -------------------------------------------------------------------------------
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -461,11 +472,7 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
             for (int q = 0; q < 32; ++q) {
               const int d = cb * 32 + q;
               const float x = (d < KD && valid) ? xf[dof_to_float(d < KD ? d : 0)] : 0.f;
-              // x = hi + lo, hi = x truncated to TF32 (exact); lo = x - hi is exact in FP32 and
-              // the tensor core reads its top 10 mantissa bits: 2 instructions, not the 10 of a
-              // rounding cvt.rna.tf32 (which sm_100a emulates)
-              vh[q] = __float_as_uint(x) & 0xFFFFE000u;
-              vl[q] = __float_as_uint(x - __uint_as_float(vh[q]));
+              tf32_split(x, vh[q], vl[q]);
             }
             tc_st32(tXh + lane_base + cb * 32, vh);
             tc_st32(tXl + lane_base + cb * 32, vl);
@@ -764,5 +771,400 @@ cudaError_t tc_shift_l2l_level(int p, int level, int c0, int nl, const TcShiftWo
   int b = (nl * KR + 255) / 256;
   b = b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16;
   k_shift_l2l_add<<<b, 256, 0, st>>>(p, c0, nl, Y, reinterpret_cast<float *>(L));
+  return cudaGetLastError();
+}
+
+// ================================================================================================
+// k_m2l_tck -- the tcgen05 class GEMM for 10 < p <= 15 (a K-tiled variant; PAPER.md:205 runs
+// p = 5..15). Above p = 10 neither the whole class operator (2 x N x K TF32 words: 205 KB at
+// p = 11, 627 KB at p = 15) nor a TMEM-resident A operand plus a double-buffered D fits, so:
+//   * rows and columns are in FLOAT order (the expansion row as stored: (n, m >= 0) complex, the
+//     zero Im part of m = 0 included as a zero column / row of T), so a thread gathers its pair's
+//     source row as contiguous float4s and the accumulator comes out as contiguous float4s;
+//   * K is streamed in chunks of 32 floats through a 2-stage shared-memory ring: the A chunk
+//     (128 pairs x 32, hi and lo, written by the row warps from registers) and the B chunk (the
+//     class operator's 32 K-columns, hi and lo, one TMA bulk copy by the issuer);
+//   * D (128 x N FP32, N = 2 nc padded to 16) accumulates in TMEM, double-buffered when 2N <= 512
+//     (p <= 14), so the epilogue of tile i overlaps the MMAs of tile i+1; at p = 15 (N = 272 = 256
+//     + 16, two MMAs per K step) it is single-buffered;
+//   * 3xTF32 as in k_m2l_tc (hi.hi + hi.lo + lo.hi).
+// Results: added into L with 16-byte vector reductions (accumulate mode) or written to per-pair
+// slots Y in float order (deterministic mode; k_m2l_reduce with ydof = 0).
+// ================================================================================================
+__host__ __device__ constexpr int tck_nf(int p) { return 2 * nc_of(p); }            // floats per row
+__host__ __device__ constexpr int tck_np(int p) { return (tck_nf(p) + 15) & ~15; }  // N
+__host__ __device__ constexpr int tck_kp(int p) { return (tck_nf(p) + 31) & ~31; }  // K (chunks of 32)
+#define TCK_KC 32
+
+// per class: for every K chunk c, [hi: N x 32 | lo: N x 32] TF32 words in the K-major core-matrix
+// layout (element (row, k) at word (k/4)*(N*4) + row*4 + k%4 of its half)
+__global__ void __launch_bounds__(256) k_m2l_build_T_tck(int p, const int *__restrict__ counters,
+                                                         const unsigned *__restrict__ class_rep,
+                                                         const int *__restrict__ pair_t,
+                                                         const unsigned *__restrict__ src,
+                                                         CellsView C, unsigned *__restrict__ Timg) {
+  extern __shared__ double2 itab_k[];  // FP64: the operator is built once per class
+  __shared__ int dec[2 * nc_of(FMM_PMAX)];  // float index -> n | m << 6 | part << 12, or -1
+  const int NF = tck_nf(p), NP = tck_np(p), KP = tck_kp(p);
+  const int ng = counters[3];
+  for (int f = threadIdx.x; f < NF; f += blockDim.x) {
+    const int c = f >> 1, part = f & 1;
+    int n = 0;
+    while ((n + 1) * (n + 2) / 2 <= c) ++n;
+    const int m = c - n * (n + 1) / 2;
+    dec[f] = (m == 0 && part) ? -1 : (n | (m << 6) | (part << 12));
+  }
+  for (int gid = blockIdx.x; gid < ng; gid += gridDim.x) {
+    const int rep = class_rep[gid];
+    const int4 gt = C.grid[pair_t[rep]], gs = C.grid[src[rep]];
+    const double rt_inv = 1.0 / (double)(1 << (FMM_LEVELS - gt.w));
+    const int dl = gt.w - gs.w;
+    double ux = (gt.x - gs.x) * rt_inv, uy = (gt.y - gs.y) * rt_inv, uz = (gt.z - gs.z) * rt_inv;
+    const bool vform = dl > 0;
+    if (vform) {
+      const double ir = ldexp(1.0, -dl);
+      ux *= ir;
+      uy *= ir;
+      uz *= ir;
+    }
+    __syncthreads();
+    // irregular harmonics I_a^b(u), a <= 2p, signed b (the recurrences of k_m2l_build_T_tc)
+    {
+      const double r2 = ux * ux + uy * uy + uz * uz, ir2 = 1.0 / r2;
+      for (int mm = threadIdx.x; mm <= 2 * p; mm += blockDim.x) {
+        double2 Imm = make_double2(rsqrt(r2), 0.0);
+        for (int k = 1; k <= mm; ++k) {
+          const double tx = Imm.x * ux - Imm.y * uy, ty = Imm.x * uy + Imm.y * ux;
+          const double s = -(2.0 * k - 1.0) * ir2;
+          Imm = make_double2(tx * s, ty * s);
+        }
+        double2 I2 = make_double2(0.0, 0.0), I1 = Imm;
+        const double sg = (mm & 1) ? -1.0 : 1.0;
+        for (int a = mm; a <= 2 * p; ++a) {
+          double2 Ia;
+          if (a == mm) Ia = Imm;
+          else if (a == mm + 1) {
+            const double s = (2.0 * mm + 1.0) * uz * ir2;
+            Ia = make_double2(Imm.x * s, Imm.y * s);
+          } else {
+            const double c1 = (2.0 * a - 1.0) * uz, c2 = (double)(a + mm - 1) * (double)(a - mm - 1);
+            Ia = make_double2((c1 * I1.x - c2 * I2.x) * ir2, (c1 * I1.y - c2 * I2.y) * ir2);
+          }
+          if (a > mm) {
+            I2 = I1;
+            I1 = Ia;
+          }
+          itab_k[a * a + a + mm] = Ia;
+          itab_k[a * a + a - mm] = make_double2(sg * Ia.x, -sg * Ia.y);
+        }
+      }
+    }
+    __syncthreads();
+    unsigned *img = Timg + (size_t)gid * 2 * NP * KP;
+    const int half = NP * TCK_KC;  // words per hi or lo half of a chunk
+    for (int off = threadIdx.x; off < NP * KP; off += blockDim.x) {
+      const int ch = off / half, w = off - ch * half;
+      const int kq = w / (NP * 4), rem = w - kq * NP * 4;
+      const int row = rem >> 2, kf = ch * TCK_KC + kq * 4 + (rem & 3);  // out float, in float
+      double v = 0.0;
+      if (row < NF && kf < NF && dec[row] >= 0 && dec[kf] >= 0) {
+        const int dr = dec[row], dk = dec[kf];
+        const int j = dr & 63, ko = (dr >> 6) & 63, rim = dr >> 12;
+        const int n = dk & 63, m = (dk >> 6) & 63, cim = dk >> 12;
+        const double sgn = ((j + ko) & 1) ? -1.0 : 1.0;
+        const double sc = sgn * (vform ? ldexp(1.0, -dl * (j + 1)) : ldexp(1.0, n * dl));
+        const int a = n + j;
+        const double2 Cp = itab_k[a * a + a + (m - ko)];
+        if (m == 0) {
+          v = sc * (rim ? Cp.y : Cp.x);
+        } else {
+          const double2 Cm = itab_k[a * a + a + (-m - ko)];
+          const double sm = (m & 1) ? -1.0 : 1.0;
+          if (!cim)
+            v = sc * (rim ? (Cp.y + sm * Cm.y) : (Cp.x + sm * Cm.x));
+          else
+            v = sc * (rim ? (Cp.x - sm * Cm.x) : -(Cp.y - sm * Cm.y));
+        }
+      }
+      const unsigned vh = f32_to_tf32((float)v);
+      unsigned *h = img + (size_t)ch * 2 * half;
+      h[w] = vh;
+      h[half + w] = f32_to_tf32((float)(v - (double)__uint_as_float(vh)));
+    }
+  }
+}
+
+namespace {
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, cta_group::1
+__device__ __forceinline__ void tc_mma_ss(unsigned d_tmem, unsigned long long adesc,
+                                          unsigned long long bdesc, unsigned idesc, unsigned acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__host__ __device__ constexpr unsigned tck_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(n >> 3) << 17) | (8u << 24);
+}
+}  // namespace
+
+template <int p>
+__global__ void __launch_bounds__(160, 1) k_m2l_tck(const int4 *__restrict__ items,
+                                                    const int *__restrict__ counters,
+                                                    const unsigned *__restrict__ sidx,
+                                                    const unsigned *__restrict__ ssrc,
+                                                    const unsigned *__restrict__ Timg,
+                                                    const float *__restrict__ M,
+                                                    float *__restrict__ Y, int *queue,
+                                                    float *__restrict__ Lacc) {
+  constexpr int NF = tck_nf(p), NP = tck_np(p), KP = tck_kp(p), NCH = KP / TCK_KC;
+  constexpr int MROW = 2 * nc_stride(p);                   // M / L row stride (floats)
+  constexpr int YS = (NF + 3) & ~3;                         // Y row stride (float order)
+  constexpr int N0 = NP > 256 ? 256 : NP, N1 = NP - N0;     // the MMA N parts (N1 = 16 at p = 15)
+  constexpr int DB = 2 * NP <= 512 ? 2 : 1;                 // D buffers in TMEM
+  constexpr unsigned ABYTES = 128u * TCK_KC * 4u;           // one half (hi or lo) of an A chunk
+  constexpr unsigned BBYTES = (unsigned)NP * TCK_KC * 4u;   // one half of a B chunk
+  constexpr unsigned STAGE = 2 * ABYTES + 2 * BBYTES;
+  static_assert(N1 == 0 || N1 % 16 == 0, "N parts");
+  static_assert(DB * NP <= 512, "TMEM budget");
+  extern __shared__ __align__(1024) unsigned char sh_tck[];
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(sh_tck + 2 * STAGE);
+  unsigned long long *a_full = bars, *b_full = bars + 2, *s_free = bars + 4, *d_full = bars + 6,
+                     *d_free = bars + 8;
+  unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 10);
+  volatile int *item_sh = reinterpret_cast<volatile int *>(bars + 11);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_addr(tmem_slot)),
+                 "n"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init_tc(&a_full[s], 128);
+      mbar_init_tc(&b_full[s], 1);
+      mbar_init_tc(&s_free[s], 1);
+      mbar_init_tc(&d_full[s], 1);
+      mbar_init_tc(&d_free[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem = *tmem_slot;
+  const int nitems = counters[1];
+  auto a_base = [&](int s) { return sh_tck + (size_t)s * STAGE; };
+  auto b_base = [&](int s) { return sh_tck + (size_t)s * STAGE + 2 * ABYTES; };
+  unsigned g = 0, tt = 0;  // chunks / tiles consumed so far (identical in every role)
+
+  if (warp == 4) {
+    // ---------------------------------------------------------------- issuer (one lane)
+    for (;;) {
+      if (tid == 128) item_sh[0] = atomicAdd(queue, 1);
+      item_bar();
+      const int it = item_sh[0];
+      item_bar();
+      if (it >= nitems) break;
+      const int4 item = items[it];
+      const int ntile = (item.y + 127) / 128;
+      const unsigned *Tcls = Timg + (size_t)item.w * 2 * NP * KP;
+      if (lane == 0) {
+        auto load_b = [&](unsigned gg, int ch) {  // the class operator's chunk ch -> stage gg & 1
+          const int s = gg & 1;
+          if (gg >= 2) mbar_wait_tc(&s_free[s], ((gg >> 1) - 1) & 1);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx_tc(&b_full[s], 2 * BBYTES);
+          bulk_g2s_tc(b_base(s), Tcls + (size_t)ch * 2 * NP * TCK_KC, 2 * BBYTES, &b_full[s]);
+        };
+        load_b(g, 0);
+        for (int i = 0; i < ntile; ++i, ++tt) {
+          const int db = DB == 2 ? (tt & 1) : 0;
+          const unsigned v = DB == 2 ? (tt >> 1) : tt;
+          if (v >= 1) mbar_wait_tc(&d_free[db], (v - 1) & 1);  // the epilogue drained D(db)
+          tc_fence_after();
+          const unsigned tD = tmem + (unsigned)(db * NP);
+          for (int c = 0; c < NCH; ++c, ++g) {
+            const int s = g & 1;
+            mbar_wait_tc(&b_full[s], (g >> 1) & 1);
+            mbar_wait_tc(&a_full[s], (g >> 1) & 1);
+            tc_fence_after();
+            const unsigned ah = smem_addr(a_base(s)), al = ah + ABYTES;
+            const unsigned bh = smem_addr(b_base(s)), bl = bh + BBYTES;
+#pragma unroll
+            for (int ks = 0; ks < TCK_KC / 8; ++ks) {
+              const unsigned acc = (c > 0 || ks > 0) ? 1u : 0u;
+              const unsigned long long dah = make_bdesc(ah + ks * 2 * 128 * 16, 128);
+              const unsigned long long dal = make_bdesc(al + ks * 2 * 128 * 16, 128);
+              const unsigned long long dbh = make_bdesc(bh + ks * 2 * NP * 16, NP);
+              const unsigned long long dbl = make_bdesc(bl + ks * 2 * NP * 16, NP);
+              tc_mma_ss(tD, dah, dbh, tck_idesc(N0), acc);
+              tc_mma_ss(tD, dah, dbl, tck_idesc(N0), 1u);
+              tc_mma_ss(tD, dal, dbh, tck_idesc(N0), 1u);
+              if (N1 > 0) {  // rows N0.. of B: 16-byte core-matrix rows further
+                const unsigned long long dbh1 = make_bdesc(bh + ks * 2 * NP * 16 + N0 * 16, NP);
+                const unsigned long long dbl1 = make_bdesc(bl + ks * 2 * NP * 16 + N0 * 16, NP);
+                tc_mma_ss(tD + N0, dah, dbh1, tck_idesc(N1 > 0 ? N1 : 16), acc);
+                tc_mma_ss(tD + N0, dah, dbl1, tck_idesc(N1 > 0 ? N1 : 16), 1u);
+                tc_mma_ss(tD + N0, dal, dbh1, tck_idesc(N1 > 0 ? N1 : 16), 1u);
+              }
+            }
+            tc_commit(&s_free[s]);  // stage s is free once these MMAs completed
+            // the next chunk's operator (this item's next chunk, or the next tile's first)
+            if (c + 1 < NCH) load_b(g + 1, c + 1);
+            else if (i + 1 < ntile) load_b(g + 1, 0);
+          }
+          tc_commit(&d_full[db]);
+        }
+      } else {
+        g += (unsigned)(ntile * NCH);
+        tt += (unsigned)ntile;
+      }
+      __syncwarp();
+      g = __shfl_sync(0xffffffffu, g, 0);
+      tt = __shfl_sync(0xffffffffu, tt, 0);
+    }
+  } else {
+    // ---------------------------------------------------------------- row warps (thread = pair row)
+    const unsigned lane_base = (unsigned)(warp * 32) << 16;
+    auto epilogue = [&](unsigned ttile, int cnt, int r0, unsigned slot) {
+      const int db = DB == 2 ? (ttile & 1) : 0;
+      const unsigned v = DB == 2 ? (ttile >> 1) : ttile;
+      mbar_wait_tc(&d_full[db], v & 1);
+      tc_fence_after();
+      const bool valid = r0 + tid < cnt;
+      float *dst = Lacc ? Lacc + (size_t)slot * MROW : Y + (size_t)slot * YS;
+#pragma unroll
+      for (int cb = 0; cb < (NF + 31) / 32; ++cb) {
+        unsigned vv[32];
+        tc_ld32(tmem + (unsigned)(db * NP) + lane_base + cb * 32, vv);
+        tc_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int f = cb * 32 + 4 * q;
+            if (f < (Lacc ? MROW : YS)) {
+              const float o0 = __uint_as_float(vv[4 * q]), o1 = __uint_as_float(vv[4 * q + 1]);
+              const float o2 = __uint_as_float(vv[4 * q + 2]), o3 = __uint_as_float(vv[4 * q + 3]);
+              if (Lacc)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + f),
+                             "f"(o0), "f"(o1), "f"(o2), "f"(o3)
+                             : "memory");
+              else
+                __stcs(reinterpret_cast<float4 *>(dst + f), make_float4(o0, o1, o2, o3));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&d_free[db])) : "memory");
+    };
+    for (;;) {
+      item_bar();
+      const int it = item_sh[0];
+      item_bar();
+      if (it >= nitems) break;
+      const int4 item = items[it];
+      const int pos0 = item.x, cnt = item.y;
+      const int ntile = (cnt + 127) / 128;
+      unsigned prev_slot = 0;
+      for (int i = 0; i < ntile; ++i, ++tt) {
+        const int r = i * 128 + tid;
+        const bool valid = r < cnt;
+        const float *row = M + (size_t)(valid ? ssrc[pos0 + r] : 0u) * MROW;
+        const unsigned slot = valid ? sidx[pos0 + r] : 0u;
+        float4 x[8];
+        auto load_chunk = [&](int c) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int f = c * TCK_KC + 4 * q;
+            float4 v4 = (valid && f < MROW) ? __ldg(reinterpret_cast<const float4 *>(row + f))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (f + 3 >= NF) {  // the row's padding floats (never written) must not reach the MMA
+              if (f + 0 >= NF) v4.x = 0.f;
+              if (f + 1 >= NF) v4.y = 0.f;
+              if (f + 2 >= NF) v4.z = 0.f;
+              v4.w = 0.f;
+            }
+            x[q] = v4;
+          }
+        };
+        load_chunk(0);
+        for (int c = 0; c < NCH; ++c, ++g) {
+          const int s = g & 1;
+          if (g >= 2) {
+            mbar_wait_tc(&s_free[s], ((g >> 1) - 1) & 1);  // the MMAs that read stage s are done
+            tc_fence_after();
+          }
+          // A chunk: row tid, K-columns 4q..4q+3 of the chunk at (q * 128 + tid) * 16 bytes
+          float4 *ah = reinterpret_cast<float4 *>(a_base(s)), *al = reinterpret_cast<float4 *>(a_base(s) + ABYTES);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 v4 = x[q];
+            const float vs[4] = {v4.x, v4.y, v4.z, v4.w};
+            float hv[4], lv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              unsigned hb, lb;
+              tf32_split(vs[e], hb, lb);
+              hv[e] = __uint_as_float(hb);
+              lv[e] = __uint_as_float(lb);
+            }
+            ah[q * 128 + tid] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+            al[q * 128 + tid] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+          }
+          if (c + 1 < NCH) load_chunk(c + 1);  // in flight while the MMAs run
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_fence_before();
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&a_full[s])) : "memory");
+        }
+        // the previous tile's epilogue overlaps this tile's MMAs (double-buffered D)
+        if (DB == 2 && i > 0) epilogue(tt - 1, cnt, (i - 1) * 128, prev_slot);
+        if (DB == 1) epilogue(tt, cnt, i * 128, slot);
+        prev_slot = slot;
+      }
+      if (DB == 2 && ntile > 0) epilogue(tt - 1, cnt, (ntile - 1) * 128, prev_slot);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512)
+                 : "memory");
+}
+
+bool m2l_tck_supported(int p) { return p >= 11 && p <= 15; }
+size_t m2l_tck_T_words(int p) { return (size_t)2 * tck_np(p) * tck_kp(p); }
+
+cudaError_t m2l_tck_build_T(int p, const M2LWork &W, int ngclass, unsigned *Timg, cudaStream_t st) {
+  if (ngclass <= 0) return cudaSuccess;
+  const size_t smem = (size_t)(2 * p + 1) * (2 * p + 1) * sizeof(double2);
+  k_m2l_build_T_tck<<<ngclass < 148 * 4 ? ngclass : 148 * 4, 256, smem, st>>>(
+      p, W.counters, W.class_rep, W.pair_t, W.src, W.C, Timg);
+  return cudaGetLastError();
+}
+
+cudaError_t m2l_tck_gemm(int p, const M2LWork &W, const unsigned *Timg, const float2 *M,
+                         cudaStream_t st, float2 *Lacc) {
+  int *queue = W.counters + 4;
+  cudaMemsetAsync(queue, 0, sizeof(int), st);
+  const unsigned *slots = Lacc ? W.stgt : W.sidx;
+#define M2L_TCK_CASE(PP)                                                                        \
+  case PP: {                                                                                  \
+    const size_t smem = (size_t)2 * (2u * 128u * TCK_KC * 4u + 2u * tck_np(PP) * TCK_KC * 4u) + 128; \
+    fmm_smem_optin((const void *)k_m2l_tck<PP>, smem);                                        \
+    k_m2l_tck<PP><<<148, 160, smem, st>>>(W.items, W.counters, slots, W.ssrc, Timg,           \
+                                          reinterpret_cast<const float *>(M), W.Y, queue,      \
+                                          reinterpret_cast<float *>(Lacc));                    \
+  } break;
+  switch (p) {
+    M2L_TCK_CASE(11) M2L_TCK_CASE(12) M2L_TCK_CASE(13) M2L_TCK_CASE(14) M2L_TCK_CASE(15)
+    default: break;
+  }
+#undef M2L_TCK_CASE
   return cudaGetLastError();
 }

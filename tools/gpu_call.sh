@@ -1,10 +1,3 @@
-L=$PWD/paper_1108_5815_b200
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "bitexact or lists or hybrid" > gpurun_out/parity.log 2>&1; tail -2 gpurun_out/parity.log
-CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "cp4:" "cp1:FMM_LIB=$L/libfmm_cp1.so" "pf0:FMM_LIB=$L/libfmm_pf0.so"
-python - <<'PY'
-import json,glob
-for f in sorted(glob.glob('gpurun_out/ab_*.json')):
-    try: d=json.loads([x for x in open(f) if x.startswith('{')][-1])
-    except Exception: print(f,'FAIL'); continue
-    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), 'trav', round(ph['ms_traverse'],3), 'up', round(ph['ms_upward'],3), 'tree', round(ph['ms_tree'],3))
-PY
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
+timeout 900 python tools/p_ladder.py 1000000 6 8 10 11 12 13 14 15 > gpurun_out/p_ladder.jsonl 2> gpurun_out/p_ladder.err
+cat gpurun_out/p_ladder.jsonl | cut -c1-400
