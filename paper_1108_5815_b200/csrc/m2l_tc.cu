@@ -24,7 +24,16 @@
 
 namespace {
 
-__host__ __device__ constexpr int tc_dim(int p) { return (dof_of(p) + 31) & ~31; }  // K = N, 32-column TMEM chunks
+// K = N is padded to at least 96 when the dofs exceed 32 (p = 5..7: 36..64 dofs): with K = N =
+// 64 this kernel runs 3-4x slower than with the zero-padded 96 (C2 M2L at p = 5 / 6 / 7: 2.23 /
+// 3.00 / 4.07 ms at 64, 0.67 / 0.76 / 0.92 ms at 96; measured, cause not identified), which made
+// p = 5..7 slower than p = 8 (the "p = 6 outlier")
+#ifndef TC_DIM_MIN
+#define TC_DIM_MIN 96
+#endif
+__host__ __device__ constexpr int tc_dim(int p) {  // K = N, 32-column TMEM chunks
+  return ((dof_of(p) + 31) & ~31) < TC_DIM_MIN && dof_of(p) > 32 ? TC_DIM_MIN : ((dof_of(p) + 31) & ~31);
+}
 
 __device__ __forceinline__ unsigned smem_addr(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);

@@ -1,3 +1,7 @@
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
-timeout 900 python tools/p_ladder.py 1000000 6 8 10 11 12 13 14 15 > gpurun_out/p_ladder.jsonl 2> gpurun_out/p_ladder.err
-cat gpurun_out/p_ladder.jsonl | cut -c1-400
+timeout 900 python tools/p_ladder.py 1000000 4 5 6 7 8 9 10 11 12 13 14 15 > gpurun_out/p_ladder.jsonl 2> gpurun_out/p_ladder.err
+python -c "
+import json
+for l in open('gpurun_out/p_ladder.jsonl'):
+    d=json.loads(l); print(d['p'], d['scheme'], round(d['ms'],3), round(d['ms_m2l'],3), '%.2e %.2e'%(d['err_phi'], d['err_grad']))
+"
