@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) k_p2p_direct(int64_t n, const float4 *__r
 // warps per CTA (384 x 3, 8 CTAs per SM): 1.36 / 7.87 / 32.7; per-lane cp.async instead of TMA
 // bulk copies: 1.37 / 6.84 / 31.4; round-1 k_p2p_leaves: 1.32 / 7.33 / 31.6.
 #ifndef P2Q_TILE
-#if defined(P2Q_LASTRED) && P2Q_LASTRED
+#if defined(P2Q_LASTRED) && P2Q_LASTRED == 1
 #define P2Q_TILE 640  // 4 CTAs per SM with the P2Q_STAGES reduction buffers of the last-warp reduction
 #else
 #define P2Q_TILE 768
@@ -380,20 +380,23 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
 #define P2Q_LASTRED 0  // 1: the last consumer warp to finish a chunk reduces it, no barrier (with
                        // 640-particle tiles for the buffers: C4 P2P 28.4 ms vs 27.5, slower)
 #endif
-#if P2Q_LASTRED
+#if P2Q_LASTRED == 2
+#define P2Q_REDBUF 2  // two buffers, reuse guarded by a per-buffer generation count
+#elif P2Q_LASTRED
 #define P2Q_REDBUF P2Q_STAGES  // see P2Q_RED
 #else
 #define P2Q_REDBUF 2  // the 4 consumer warps meet at a named barrier, then reduce together
 #endif
   __shared__ __align__(16) float4 red[P2Q_REDBUF][32 * P2Q_CWARPS][4];
   __shared__ int red_cnt[P2Q_REDBUF];
+  __shared__ int red_gen[P2Q_REDBUF];  // reductions completed on each buffer (P2Q_LASTRED == 2)
 #else
   __shared__ __align__(16) float4 red[P2Q_RED][P2Q_CWARPS][P2Q_CHUNK];
   __shared__ int red_cnt[P2Q_RED];
 #endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int b = 0; b < (int)(sizeof(red_cnt) / sizeof(int)); ++b) red_cnt[b] = 0;
+    for (int b = 0; b < (int)(sizeof(red_cnt) / sizeof(int)); ++b) red_cnt[b] = red_gen[b] = 0;
     for (int s = 0; s < P2Q_STAGES; ++s) {
       q_mbar_init(&full[s], P2Q_CPASYNC ? 33 : 1);  // (32 producer lanes' copies +) the meta
       q_mbar_init(&empty[s], P2Q_CWARPS);
@@ -655,6 +658,13 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
       ++k;
       if (m.z & QF_LAST) {
         float4(*rb)[4] = red[chunk % P2Q_REDBUF];
+#if P2Q_LASTRED == 2
+        // buffer chunk % 2 was last used by chunk - 2: wait (rarely) until that reduction is done
+        if (chunk >= 2)
+          while (*(volatile int *)&red_gen[chunk % 2] < (int)(chunk >> 1)) {
+          }
+        __syncwarp();
+#endif
         ++chunk;
         if (active) {
 #pragma unroll
@@ -693,7 +703,13 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
           __threadfence_block();
           reduce(L & 31, 32);
           __syncwarp();
-          if ((L & 31) == 0) red_cnt[b] = 0;
+          if ((L & 31) == 0) {
+            red_cnt[b] = 0;
+            if (P2Q_LASTRED == 2) {
+              __threadfence_block();
+              atomicAdd(&red_gen[b], 1);
+            }
+          }
         }
 #else
         asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");

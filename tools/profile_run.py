@@ -10,7 +10,8 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
 mode = sys.argv[2] if len(sys.argv) > 2 else "hybrid"
 xyz, q = make_particles(cfg["n"], cfg["dist"], cfg["seed"])
 X, Q = torch.from_numpy(xyz).cuda(), torch.from_numpy(q).cuda()
-f = FMM(p=cfg["p"], theta=cfg["theta"], ncrit=cfg["ncrit"], mode=mode, tune="FMM_COST" not in os.environ)
+p = int(os.environ.get("FMM_P", cfg["p"]))  # (an order other than the config's, e.g. the p ladder)
+f = FMM(p=p, theta=cfg["theta"], ncrit=cfg["ncrit"], mode=mode, tune="FMM_COST" not in os.environ)
 if "FMM_COST" in os.environ:  # a fixed cost model (else the one measured at create, as bench.py)
     f.set_cost_model(*map(float, os.environ["FMM_COST"].split(",")))
 f.set_deterministic(os.environ.get("FMM_DET", "0") == "1")
