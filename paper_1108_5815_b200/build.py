@@ -29,7 +29,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8, out: str | 
     lib = out or LIB
     if out is None and not force and not stale():
         return LIB
-    objdir = os.path.join(HERE, "build" if out is None else "build_alt")
+    objdir = os.path.join(HERE, "build" if out is None else
+                          ("build_check" if "-DFMM_CHECK" in (extra or []) else "build_alt"))
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []

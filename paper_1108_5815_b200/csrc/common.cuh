@@ -94,3 +94,46 @@ bool fmm_once_per_device(const void *key, bool (*fn)());
 // Resident blocks per SM x SMs for `func` at `threads` threads and `smem` dynamic bytes on the
 // current device (cached per device).
 int fmm_resident_blocks(const void *func, int threads, size_t smem);
+
+// ---- FMM_CHECK builds: device-side bounds checks of the data-dependent indices ----------------
+// (compute-sanitizer is not available on the GPU pool; tests/test_gpu_check.py builds the library
+// with -DFMM_CHECK and runs the small all-kernel workload of tools/sanitize_run.py.) The bounds are
+// the capacities (elements) of the handle's buffers, published per evaluation to every
+// translation unit's copy (fmm_check_publish). A failed check prints the site and traps.
+struct FmmChk {
+  long long pos;    // particles in the sorted position / accumulator arrays (incl. LET copies)
+  long long cells;  // cell records
+  long long rows;   // expansion rows of M and L
+  long long yrows;  // per-pair result slots (deterministic M2L)
+  long long lists;  // entries of each interaction list
+};
+#ifdef FMM_CHECK
+#include <cstdio>
+static __device__ FmmChk g_fmm_chk;
+#define FMM_CHK_DEFINE_SETTER(name)                                                             \
+  void name(const FmmChk &c, cudaStream_t st) {                                                 \
+    cudaMemcpyToSymbolAsync(g_fmm_chk, &c, sizeof c, 0, cudaMemcpyHostToDevice, st);           \
+  }
+#define FMM_DCHECK(cond, what)                                                                  \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("FMM_CHECK failed: %s [%s] at %s:%d (block %d thread %d)\n", what, #cond, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                      \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#define FMM_IN(i, bound) ((long long)(i) >= 0 && (long long)(i) < (long long)(bound))
+#else
+#define FMM_CHK_DEFINE_SETTER(name) \
+  void name(const FmmChk &, cudaStream_t) {}
+#define FMM_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#define FMM_IN(i, bound) true
+#endif
+// one setter per translation unit that checks (their g_fmm_chk copies are separate)
+void fmm_chk_set_p2p(const FmmChk &, cudaStream_t);
+void fmm_chk_set_m2l_tc(const FmmChk &, cudaStream_t);
+void fmm_chk_set_m2l(const FmmChk &, cudaStream_t);
+void fmm_chk_set_traverse(const FmmChk &, cudaStream_t);
+void fmm_chk_set_expansions(const FmmChk &, cudaStream_t);

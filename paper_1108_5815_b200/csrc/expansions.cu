@@ -239,6 +239,8 @@ __global__ void __launch_bounds__(128, P2MG_MINB) k_p2m_g(const int *__restrict_
     const float4 g = C.geo[leaf];
     const float rinv = 1.f / g.w;
     const int b = C.beg[leaf], cnt = C.cnt[leaf];
+    FMM_DCHECK(FMM_IN(leaf, g_fmm_chk.rows) && b >= 0 && (long long)b + cnt <= g_fmm_chk.pos,
+               "P2M leaf / particle range");
     P2MGroups<p, 0>::run(leaf, g, rinv, b, cnt, pos, M, red, lane);
   }
 }
@@ -441,6 +443,8 @@ __global__ void __launch_bounds__(128, L2P_MINB) k_l2p(const int *__restrict__ l
   for (int li = gw; li < nleaves; li += nw) {
     const int leaf = leaves[li];
     const int b = C.beg[leaf], cnt = C.cnt[leaf];
+    FMM_DCHECK(FMM_IN(leaf, g_fmm_chk.rows) && b >= 0 && (long long)b + cnt <= g_fmm_chk.pos,
+               "L2P leaf / particle range");
     const float4 g = C.geo[leaf];
     const float rinv = 1.f / g.w;
     __syncwarp();
@@ -597,3 +601,5 @@ void launch_l2p(int p, const int *leaves, int nleaves, CellsView C, const float4
   FMM_DISPATCH_P(p, (k_l2p<P_><<<warp_grid(nleaves, 4), 128, 4 * nc_of(P_) * sizeof(float2), st>>>(
                         leaves, nleaves, C, pos, L, acc, perm, phi, grad, use_local)));
 }
+
+FMM_CHK_DEFINE_SETTER(fmm_chk_set_expansions)

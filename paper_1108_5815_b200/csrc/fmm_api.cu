@@ -1199,6 +1199,28 @@ static int m2l_scheme_of(const fmm_ctx *h) {
   return FMM_M2L_ROTATION;
 }
 
+// FMM_CHECK builds: publish the buffer capacities the device-side bounds checks test against
+// (every translation unit holds its own copy); the capacities only grow within an evaluation
+static void publish_chk(fmm_ctx *h, cudaStream_t st) {
+#ifdef FMM_CHECK
+  FmmChk c;
+  c.pos = (long long)std::min(h->pos.cap, h->acc.cap);
+  c.cells = (long long)h->cbeg.cap;
+  c.rows = (long long)(std::min(h->M.cap, h->L.cap) / nc_stride(h->p));
+  c.yrows = (long long)(h->m2l_Y.cap / m2l_y_stride(h->p));
+  c.lists = (long long)h->p2p_rng.cap;
+  if (getenv("FMM_CHECK_SELFTEST")) c.pos = 1;  // tests: a bound every evaluation violates
+  fmm_chk_set_p2p(c, st);
+  fmm_chk_set_m2l_tc(c, st);
+  fmm_chk_set_m2l(c, st);
+  fmm_chk_set_traverse(c, st);
+  fmm_chk_set_expansions(c, st);
+#else
+  (void)h;
+  (void)st;
+#endif
+}
+
 static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n, float *phi,
                          float *grad) {
   cudaStream_t st = h->stream;
@@ -1209,14 +1231,15 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     if (int rc = build_tree(h, xyz, q, n)) return rc;
   }
   record(h, EV_TREE);
+  const int NCS = nc_stride(p);
+  CK(h->M.ensure((size_t)h->ncells * NCS));
+  CK(h->L.ensure((size_t)h->ncells * NCS));
+  publish_chk(h, st);
   // a7/a8 upward sweep, on the aux stream: it overlaps the traversal and the M2L class sort (which
   // do not read M); the stream joins before the first kernel that reads M
   CK(cudaEventRecord(h->ev_fork, st));
   CK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
   cudaStream_t ua = h->aux;
-  const int NCS = nc_stride(p);
-  CK(h->M.ensure((size_t)h->ncells * NCS));
-  CK(h->L.ensure((size_t)h->ncells * NCS));
   // (distributed: every cell starts at zero -- only the own leaves get a P2M, so the M2M leaves
   // straddling cells with this rank's partial sum and remote cells at zero)
   if (NCS != NC || h->comm) CK(cudaMemsetAsync(h->M.p, 0, sizeof(float2) * (size_t)h->ncells * NCS, ua));
@@ -1321,6 +1344,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     record_on(h, EV_M2P, ns);
     return FMM_OK;
   };
+  publish_chk(h, st);  // (list capacities after the traversal's retries)
   if (h->overlap) {
     CK(cudaEventRecord(h->ev_trav, st));
     CK(cudaStreamWaitEvent(h->nf, h->ev_trav, 0));
@@ -1358,6 +1382,7 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     // requested
     const bool accum = (use_tc || use_rot) && !h->deterministic;
     if (!accum) CK(h->m2l_Y.ensure((size_t)np * m2l_y_stride(p)));
+    publish_chk(h, st);
     CK(h->cub_tmp.ensure(m2l_temp_bytes(np)));
     M2LWork W{};
     W.C = h->cells();

@@ -574,6 +574,8 @@ __global__ void __launch_bounds__(256) k_m2l_reduce(int p, int ncells, const int
        i += (long long)gridDim.x * blockDim.x) {
     const int t = (int)(i / NQ), q = (int)(i - (long long)t * NQ);
     const int o = off[t], c = cnt[t];
+    FMM_DCHECK(o >= 0 && (long long)o + c <= g_fmm_chk.yrows && FMM_IN(t, g_fmm_chk.rows),
+               "M2L per-pair slots of a target");
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 *y = Y4 + (size_t)o * NQ + q;
 #pragma unroll 4
@@ -732,3 +734,5 @@ cudaError_t m2l_execute(int p, const M2LWork &W, int npairs, int ncells, const f
   }
   return cudaGetLastError();
 }
+
+FMM_CHK_DEFINE_SETTER(fmm_chk_set_m2l)

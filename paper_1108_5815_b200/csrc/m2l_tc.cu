@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
     // row's bytes when it has one, so a phase completes only after all passed the previous one)
     auto stage = [&](int cnt, int c0, int s) {
       if (c0 + tid < cnt) {
+        FMM_DCHECK(FMM_IN(s, g_fmm_chk.rows), "tcgen05 M2L / shift source row");
         mbar_expect_tx_tc(x_full, (unsigned)(MROW * 4));
         bulk_g2s_tc(myrow, M + (size_t)s * MROW, MROW * 4, x_full);
       } else {
@@ -388,6 +389,7 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tc(const int4 *__restrict__ item
       }
       tc_wait_ld();
       if (c0 + tid < cnt) {
+        FMM_DCHECK(FMM_IN(trow, g_fmm_chk.rows), "tcgen05 M2L target row");
         float *dst = Lacc + (size_t)trow * MROW;
 #pragma unroll
         for (int q = 0; q < MROW / 4; ++q) {
@@ -1086,6 +1088,9 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tck(const int4 *__restrict__ ite
         const bool valid = r < cnt;
         const float *row = M + (size_t)(valid ? ssrc[pos0 + r] : 0u) * MROW;
         const unsigned slot = valid ? sidx[pos0 + r] : 0u;
+        FMM_DCHECK(!valid || (FMM_IN(ssrc[pos0 + r], g_fmm_chk.rows) &&
+                              FMM_IN(slot, Lacc ? g_fmm_chk.rows : g_fmm_chk.yrows)),
+                   "K-tiled M2L source row / result slot");
         float4 x[8];
         auto load_chunk = [&](int c) {
 #pragma unroll
@@ -1177,3 +1182,5 @@ cudaError_t m2l_tck_gemm(int p, const M2LWork &W, const unsigned *Timg, const fl
 #undef M2L_TCK_CASE
   return cudaGetLastError();
 }
+
+FMM_CHK_DEFINE_SETTER(fmm_chk_set_m2l_tc)

@@ -457,6 +457,8 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
         }
 #else
         if (a < e) {  // one TMA bulk copy per range piece
+          FMM_DCHECK(beg + (a - lo) >= 0 && (long long)beg + (e - lo) <= g_fmm_chk.pos,
+                     "P2P source range");
           unsigned long long *fb = &full[k % P2Q_STAGES];
           q_mbar_expect_tx(fb, (unsigned)(e - a) * 16u);
           q_bulk_g2s(&tile[k % P2Q_STAGES][fill + (a - done)], pos + beg + (a - lo),
@@ -628,6 +630,8 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
         tb = m.x;
         c0 = m.w & 0xffff;
         nt = m.w >> 16;
+        FMM_DCHECK(tb >= 0 && (long long)tb + c0 + nt <= g_fmm_chk.pos && nt <= P2Q_CHUNK,
+                   "P2P target chunk");
         Q = (nt + 3) >> 2;
         S = (32 * P2Q_CWARPS) / Q;
         g = L % Q;
@@ -968,7 +972,8 @@ __global__ void __launch_bounds__(128) k_p2p_merge(const int *__restrict__ leave
         if (head) mrg[off + mo + __popc(hb & ((1u << lane) - 1u))] = run;
         mo += __popc(hb);
       }
-      if (lane == 0) desc[i].w = m;  // ancestors folded in: flag cleared
+      FMM_DCHECK((long long)off + m <= g_fmm_chk.lists, "P2P merged runs");
+    if (lane == 0) desc[i].w = m;  // ancestors folded in: flag cleared
     } else if (lane == 0) {
       desc[i].w = d.w | P2Q_RAW;
     }
@@ -1018,3 +1023,5 @@ void launch_p2p_direct(int64_t n, const float4 *pos, float *phi, float *grad, cu
   if (b < 1) b = 1;
   k_p2p_direct<<<(int)b, 256, 0, st>>>(n, pos, phi, grad, -1.0f);
 }
+
+FMM_CHK_DEFINE_SETTER(fmm_chk_set_p2p)

@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
         if (forced_cat >= 0) {
           cat = forced_cat;
         } else {
+          FMM_DCHECK(FMM_IN(s, g_fmm_chk.cells), "traversal source cell");
           const CellRec rs = prec ? *prec : load_rec(A.pk, s);
           scnt = rs.b.y;
           sbeg = rs.b.x;
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
     }
     // claim the final space of the four lists (running list sizes, this level's deferred pairs:
     // counters in separate 128-byte lines, see TRAV_CNT) and copy them there
+    FMM_DCHECK(FMM_IN(t, g_fmm_chk.cells), "traversal target cell");
     int base[4];
     if (lane == 0) {
 #pragma unroll
@@ -309,3 +311,5 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
 void launch_traverse(const TravArgs &A, cudaStream_t st) {
   k_traverse<<<A.grid_blocks, 128, 0, st>>>(A);
 }
+
+FMM_CHK_DEFINE_SETTER(fmm_chk_set_traverse)
