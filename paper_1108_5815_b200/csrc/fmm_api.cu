@@ -120,7 +120,9 @@ struct fmm_ctx {
   DBuf<int4> cpack;  // packed cell records for the traversal
   DBuf<int> tc_bnd;     // cooperative tree build: child bounds [8][cells of a level]
   DBuf<int2> tc_crange; // ... child ranges
-  int *d_tree_st = nullptr;  // ... its results (64 ints; [4] = the short sort's redo flag)
+  int *d_tree_st = nullptr;  // ... its results (64 ints; [4] = the short sort's redo flag,
+                             // [5] = its long-run count)
+  DBuf<int2> sort_runs;      // the short sort's runs of equal high key bits (> 64 particles)
   bool sort_redo = false;
   // M2L translation scheme (NEXT-1): requested (FMM_M2L_AUTO = let fmm_tune decide), the one
   // the kernel pre-calculation picked, and the M2L times it measured per scheme (ms)
@@ -439,21 +441,24 @@ static int build_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n) {
   CK(h->acc.ensure(n));
   launch_keys(xyz, n, h->d_root, h->keys_in.p, h->idx_in.p, st);
   CKL();
-  // a3: 6 radix passes over key bits 16..62 + a tie fix-up (tree.cu), exactly the order of the
-  // full 63-bit stable sort; a run of equal high bits longer than 64 (a very dense cluster)
-  // flags a redo with all 8 passes, found in the tree build's single read-back
+  // a3: radix passes over the key bits of levels 0..D+2 (D = the previous tree's depth; bits
+  // 16..62 on the first evaluation) + a tie fix-up (tree.cu), exactly the order of the full
+  // 63-bit stable sort; a run of equal high bits longer than 4096 (a very dense cluster) flags a
+  // redo with all 8 passes, found in the tree build's single read-back
+  const int low_bits = h->depth > 0 ? std::max(16, std::min(40, 63 - 3 * (h->depth + 2))) : 16;
   static const bool full_sort = getenv("FMM_SORT_FULL") != nullptr;
   bool short_sort = !full_sort;
   for (int pass = 0; pass < 2; ++pass) {
     size_t bytes = 0;
     CK(cudaMemsetAsync(h->d_tree_st + 4, 0, sizeof(int), st));
     if (short_sort) {
+      CK(h->sort_runs.ensure((size_t)sort_runs_cap(n)));
       CK(sort_keys_short(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n,
-                         h->d_tree_st + 4, st));
+                         h->d_tree_st + 4, h->sort_runs.p, low_bits, st));
       CK(h->cub_tmp.ensure(bytes));
       CK(sort_keys_short(h->cub_tmp.p, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n,
-                         h->d_tree_st + 4, st));
-      h->stats.launches += 1;
+                         h->d_tree_st + 4, h->sort_runs.p, low_bits, st));
+      h->stats.launches += 2;
     } else {
       CK(sort_keys(nullptr, bytes, h->keys_in.p, h->keys.p, h->idx_in.p, h->perm.p, n, st));
       CK(h->cub_tmp.ensure(bytes));
@@ -1835,6 +1840,7 @@ int fmm_destroy(fmm_t h) {
   DeviceGuard dg(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->keys_in.release(); h->keys.release(); h->idx_in.release(); h->perm.release();
+  h->sort_runs.release();
   h->pos.release(); h->acc.release(); h->cub_tmp.release(); h->host_stage.release();
   h->cbeg.release(); h->ccnt.release(); h->cparent.release(); h->cchild0.release();
   h->cnchild.release(); h->cgrid.release(); h->cgeo.release(); h->cprefix.release(); h->cpack.release();

@@ -12,9 +12,10 @@ void launch_keys(const float *xyz, int64_t n, const RootInfo *root, uint64_t *ke
                  cudaStream_t st);
 void launch_gather(const float *xyz, const float *q, const unsigned *perm, int64_t n, float4 *pos,
                    cudaStream_t st);
+int sort_runs_cap(int64_t n);  // entries of the long-run scratch sort_keys_short needs
 cudaError_t sort_keys_short(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
-                            const unsigned *vin, unsigned *vout, int64_t n, int *flag,
-                            cudaStream_t st);
+                            const unsigned *vin, unsigned *vout, int64_t n, int *flag, int2 *runs,
+                            int low_bits, cudaStream_t st);
 int tree_coop_grid();
 cudaError_t launch_tree_coop(const uint64_t *keys, int n, int ncrit, const RootInfo *root,
                              CellsView C, uint64_t *prefix, int cap, int *bnd, int *nch,

@@ -307,23 +307,33 @@ __global__ void __launch_bounds__(256) k_part_indices(int lo, int cnt,
     out[i] = perm[lo + i];
 }
 
-// ---- a3 short sort: 6 radix passes over key bits [16, 63) + a tie fix-up -----------------------
-// Keys that agree in bits 16..62 (cells of level 16 shared by several particles) are rare; runs
-// of them are put in full-key order (stable: ties keep the index order of the stable pass) by one
-// thread each. A run longer than SORT_RUN_MAX flags the caller, which then sorts all 63 bits.
-#define SORT_LOW_BITS 16
+// ---- a3 short sort: radix passes over the key bits [SORT_LOW_BITS, 63) + a tie fix-up ---------
+// Keys that agree in bits SORT_LOW_BITS..62 form runs that the stable radix pass left in index
+// order; each run is put in full-key order (ties in the full key keep the index order, so the
+// result is exactly the stable 63-bit sort): runs of <= SORT_RUN_MAX by one thread (insertion
+// sort), runs of <= SORT_BLOCK_MAX by one CTA (bitonic sort of (key, original index) pairs in
+// shared memory), longer runs flag the caller, which then sorts all 63 bits. The caller picks
+// SORT_LOW_BITS (a run-time argument) from the previous tree's depth D: the bits of levels
+// 0..D+2, so the runs are particles sharing a cell two levels below the deepest leaf (C2, D = 5:
+// 21 bits, 3 passes; C4, D = 7: 27 bits, 4 passes; C3, D = 12: 42 bits, 6 passes).
 #define SORT_RUN_MAX 64
+#define SORT_BLOCK_MAX 4096
 __global__ void k_sort_fixup(uint64_t *__restrict__ keys, unsigned *__restrict__ vals, int64_t n,
-                             int *flag) {
+                             int *flag, int2 *__restrict__ runs, int *nruns, int runs_cap,
+                             int SORT_LOW_BITS) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t hi = keys[i] >> SORT_LOW_BITS;
     if ((keys[i + 1] >> SORT_LOW_BITS) != hi) continue;          // not inside a run
     if (i > 0 && (keys[i - 1] >> SORT_LOW_BITS) == hi) continue;  // not the run's first element
     int64_t e = i + 1;
-    while (e < n && (keys[e] >> SORT_LOW_BITS) == hi && e - i <= SORT_RUN_MAX) ++e;
-    if (e - i > SORT_RUN_MAX) {
-      atomicOr(flag, 1);
+    while (e < n && (keys[e] >> SORT_LOW_BITS) == hi && e - i <= SORT_BLOCK_MAX) ++e;
+    if (e - i > SORT_RUN_MAX) {  // a CTA sorts it (k_sort_fixup_block), or the caller redoes all
+      const int r = e - i <= SORT_BLOCK_MAX ? atomicAdd(nruns, 1) : runs_cap;
+      if (r < runs_cap)
+        runs[r] = make_int2((int)i, (int)(e - i));
+      else
+        atomicOr(flag, 1);
       continue;
     }
     for (int64_t a = i + 1; a < e; ++a) {  // insertion sort by the full key (stable)
@@ -337,6 +347,49 @@ __global__ void k_sort_fixup(uint64_t *__restrict__ keys, unsigned *__restrict__
       }
       keys[b + 1] = k;
       vals[b + 1] = v;
+    }
+  }
+}
+// one CTA per long run: bitonic sort of (full key, original index) -- a total order, so the
+// result equals the stable sort's
+__global__ void __launch_bounds__(512) k_sort_fixup_block(uint64_t *__restrict__ keys,
+                                                          unsigned *__restrict__ vals,
+                                                          const int2 *__restrict__ runs,
+                                                          const int *__restrict__ nruns) {
+  __shared__ uint64_t sk[SORT_BLOCK_MAX];
+  __shared__ unsigned sv[SORT_BLOCK_MAX];
+  const int nr = *nruns;
+  for (int r = blockIdx.x; r < nr; r += gridDim.x) {
+    const int2 run = runs[r];
+    int P = 64;
+    while (P < run.y) P <<= 1;
+    __syncthreads();
+    for (int t = threadIdx.x; t < P; t += blockDim.x) {
+      sk[t] = t < run.y ? keys[run.x + t] : ~0ull;
+      sv[t] = t < run.y ? vals[run.x + t] : ~0u;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = threadIdx.x; t < P; t += blockDim.x) {
+          const int u = t ^ j;
+          if (u > t) {
+            const uint64_t a = sk[t], b = sk[u];
+            const unsigned va = sv[t], vb = sv[u];
+            const bool gt = a > b || (a == b && va > vb);
+            if (((t & k) == 0) == gt) {
+              sk[t] = b;
+              sk[u] = a;
+              sv[t] = vb;
+              sv[u] = va;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int t = threadIdx.x; t < run.y; t += blockDim.x) {
+      keys[run.x + t] = sk[t];
+      vals[run.x + t] = sv[t];
     }
   }
 }
@@ -583,15 +636,19 @@ cudaError_t sort_keys(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_
                       const unsigned *vin, unsigned *vout, int64_t n, cudaStream_t st) {
   return cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int)n, 0, 63, st);
 }
-// bits [16, 63) only (6 onesweep passes instead of 8), then the tie fix-up; *flag set => the
-// caller must redo the full sort
+// bits [low_bits, 63) only (3-6 onesweep passes instead of 8), then the tie fix-up; *flag set
+// => the caller must redo the full sort. runs: scratch of runs_cap entries, flag[1] their count.
+int sort_runs_cap(int64_t n) { return (int)(n / (SORT_RUN_MAX + 1)) + 1; }
 cudaError_t sort_keys_short(void *tmp, size_t &tmp_bytes, const uint64_t *kin, uint64_t *kout,
                             const unsigned *vin, unsigned *vout, int64_t n, int *flag,
-                            cudaStream_t st) {
+                            int2 *runs, int low_bits, cudaStream_t st) {
   cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin, kout, vin, vout, (int)n,
-                                                  SORT_LOW_BITS, 63, st);
+                                                  low_bits, 63, st);
   if (e || !tmp || n < 2) return e;
-  k_sort_fixup<<<grid_for(n, 256), 256, 0, st>>>(kout, vout, n, flag);
+  cudaMemsetAsync(flag + 1, 0, sizeof(int), st);
+  k_sort_fixup<<<grid_for(n, 256), 256, 0, st>>>(kout, vout, n, flag, runs, flag + 1,
+                                                 sort_runs_cap(n), low_bits);
+  k_sort_fixup_block<<<148 * 2, 512, 0, st>>>(kout, vout, runs, flag + 1);
   return cudaGetLastError();
 }
 // the cooperative tree build: grid size for this device (all blocks co-resident)
