@@ -452,42 +452,79 @@ __global__ void __launch_bounds__(TREE_BLOCK) k_tree_coop(const uint64_t *__rest
     st[8] = 0;
     st[32] = 1;
   }
+  // Two grid syncs per level: (1) every block takes a contiguous segment of the level's cells,
+  // finds each cell's 8 child bounds by binary search (8 lanes per cell, the next octant's bound
+  // by a shuffle), counts and compacts the non-empty children and publishes its segment's child
+  // total; (2) after the sync every block sums the totals of the blocks before it (its offset) and
+  // of all blocks (the next level's size) itself -- no serial scan by one block, no extra sync --
+  // and emits its children in cell order (deterministic).
+  auto prefix_of = [&](int upto, int &all) {  // sum of blk[0, upto) and of blk[0, G), block-wide
+    int a = 0, t = 0;
+    for (int j = threadIdx.x; j < G; j += blockDim.x) {
+      const int v = blk[j];
+      t += v;
+      if (j < upto) a += v;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      ws[threadIdx.x >> 5] = a;
+      ws[16 + (threadIdx.x >> 5)] = t;
+    }
+    __syncthreads();
+    a = 0;
+    t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += ws[w];
+      t += ws[16 + w];
+    }
+    __syncthreads();
+    all = t;
+    return a;
+  };
   int c0 = 0, nl = 1, total = 1, level = 0;
   for (;; ++level) {
     grid.sync();
-    // child bounds (one thread per (cell, octant)) -- as k_split
     const int shift = 3 * (FMM_LEVELS - (level + 1));
-    for (int id = gtid; id < 8 * nl; id += gthreads) {
-      const int k = id >> 3, o = id & 7, c = c0 + k;
-      const int cb = C.beg[c], cn = C.cnt[c];
-      int l = cb;
-      if (split_cell(cn, ncrit, level)) {
-        const uint64_t tgt = prefix[c] * 8 + (uint64_t)o;
-        int r = cb + cn;
-        while (l < r) {
-          const int m = (l + r) >> 1;
-          if ((keys[m] >> shift) < tgt) l = m + 1;
-          else r = m;
-        }
-      }
-      bnd[id] = l;
-    }
-    grid.sync();
-    // child ranges and counts; each block owns the segment [s0, s1) of the level
     const int seg = (nl + G - 1) / G, s0 = min(b * seg, nl), s1 = min(s0 + seg, nl);
     int bsum = 0;
-    for (int k = s0 + threadIdx.x; k < s1; k += blockDim.x) {
-      const int c = c0 + k;
-      int cnt = 0;
-      if (split_cell(C.cnt[c], ncrit, level)) {
-        const int end = C.beg[c] + C.cnt[c];
-        for (int o = 0; o < 8; ++o) {
-          const int lo = bnd[8 * k + o], hi = o < 7 ? bnd[8 * k + o + 1] : end;
-          if (hi > lo) crange[8 * k + cnt++] = make_int2(lo, (hi - lo) | (o << 28));
+    for (int base = s0 * 8; base < s1 * 8; base += blockDim.x) {
+      const int id = base + threadIdx.x;
+      const bool live = id < s1 * 8;
+      const int k = id >> 3, o = id & 7, c = c0 + k;
+      int lo = 0, end = 0;
+      bool split = false;
+      if (live) {
+        const int cb = C.beg[c], cn = C.cnt[c];
+        end = cb + cn;
+        lo = cb;
+        split = split_cell(cn, ncrit, level);
+        if (split) {
+          const uint64_t tgt = prefix[c] * 8 + (uint64_t)o;
+          int r = end;
+          while (lo < r) {
+            const int m = (lo + r) >> 1;
+            if ((keys[m] >> shift) < tgt) lo = m + 1;
+            else r = m;
+          }
         }
       }
-      nch[k] = cnt;
-      bsum += cnt;
+      const int nxt = __shfl_down_sync(0xffffffffu, lo, 1);  // the next octant's bound
+      const int hi = o < 7 ? nxt : end;
+      const bool ne = live && split && hi > lo;
+      const unsigned bal = __ballot_sync(0xffffffffu, ne);
+      const unsigned grp = (bal >> (threadIdx.x & 24)) & 0xffu;  // this cell's 8 lanes
+      if (ne) {
+        const int pos = __popc(grp & ((1u << o) - 1u));
+        crange[8 * k + pos] = make_int2(lo, (hi - lo) | (o << 28));
+      }
+      if (live && o == 0) {
+        nch[k] = __popc(grp);
+        bsum += __popc(grp);
+      }
     }
     for (int o = 16; o > 0; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = bsum;
@@ -499,27 +536,14 @@ __global__ void __launch_bounds__(TREE_BLOCK) k_tree_coop(const uint64_t *__rest
     }
     __syncthreads();
     grid.sync();
-    // block 0: exclusive scan of the block totals; the next level's size
-    if (b == 0) {
-      int carry = 0;
-      for (int j0 = 0; j0 < G; j0 += blockDim.x) {
-        const int j = j0 + threadIdx.x;
-        const int v = j < G ? blk[j] : 0;
-        int tot;
-        const int e = block_excl_scan(v, ws, tot);
-        if (j < G) blk[j] = carry + e;
-        carry += tot;
-      }
-      if (threadIdx.x == 0) {
-        blk[G] = carry;
-        if (total + carry > cap) st[1] = 1;
-      }
+    int nnext = 0;
+    int run = total + prefix_of(b, nnext);
+    if (total + nnext > cap) {
+      if (gtid == 0) st[1] = 1;
+      break;  // every block takes the same decision
     }
-    grid.sync();
-    const int nnext = blk[G];
-    if (st[1] || nnext == 0) break;
+    if (nnext == 0) break;
     // emit the children: block-local exclusive scan of the segment + the block's offset
-    int run = total + blk[b];
     for (int k0 = s0; k0 < s1; k0 += blockDim.x) {
       const int k = k0 + threadIdx.x;
       const int m = k < s1 ? nch[k] : 0;
@@ -569,24 +593,13 @@ __global__ void __launch_bounds__(TREE_BLOCK) k_tree_coop(const uint64_t *__rest
   }
   __syncthreads();
   grid.sync();
-  if (b == 0) {
-    int carry = 0;
-    for (int j0 = 0; j0 < G; j0 += blockDim.x) {
-      const int j = j0 + threadIdx.x;
-      const int v = j < G ? blk[j] : 0;
-      int tot;
-      const int e = block_excl_scan(v, ws, tot);
-      if (j < G) blk[j] = carry + e;
-      carry += tot;
-    }
-    if (threadIdx.x == 0) {
-      st[0] = total;
-      st[2] = level;
-      st[3] = carry;
-    }
+  int nleaves = 0;
+  int run = prefix_of(b, nleaves);
+  if (gtid == 0) {
+    st[0] = total;
+    st[2] = level;
+    st[3] = nleaves;
   }
-  grid.sync();
-  int run = blk[b];
   for (int c0l = s0; c0l < s1; c0l += blockDim.x) {
     const int c = c0l + threadIdx.x;
     const int f = c < s1 ? (C.nchild[c] == 0) : 0;

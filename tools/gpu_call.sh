@@ -1,6 +1,6 @@
 L=$PWD/paper_1108_5815_b200
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_property.py tests/test_gpu_dist.py -x -q > gpurun_out/parity.log 2>&1; tail -2 gpurun_out/parity.log
-CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "s31:" "s16:FMM_LIB=$L/libfmm_s16.so"
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_property.py -x -q > gpurun_out/parity.log 2>&1; tail -2 gpurun_out/parity.log
+CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "coop2:" "coop1:FMM_LIB=$L/libfmm_coop1.so"
 python - <<'PY'
 import json,glob
 for f in sorted(glob.glob('gpurun_out/ab_*.json')):
