@@ -7,6 +7,8 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include <algorithm>
+#include <cstdlib>
 #include "kernels.cuh"
 
 // ---- a1: bounding box + non-finite check ---------------------------------------------------
@@ -666,7 +668,9 @@ cudaError_t sort_keys_short(void *tmp, size_t &tmp_bytes, const uint64_t *kin, u
 }
 // the cooperative tree build: grid size for this device (all blocks co-resident)
 int tree_coop_grid() {
-  return fmm_resident_blocks((const void *)k_tree_coop, TREE_BLOCK, 0);
+  const int res = fmm_resident_blocks((const void *)k_tree_coop, TREE_BLOCK, 0);
+  static const int per_sm = getenv("FMM_TREE_GRID") ? atoi(getenv("FMM_TREE_GRID")) : 0;
+  return per_sm > 0 ? std::min(res, 148 * per_sm) : res;  // (A/B knob: blocks per SM)
 }
 cudaError_t launch_tree_coop(const uint64_t *keys, int n, int ncrit, const RootInfo *root,
                              CellsView C, uint64_t *prefix, int cap, int *bnd, int *nch,

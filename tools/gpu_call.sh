@@ -1,6 +1,4 @@
-L=$PWD/paper_1108_5815_b200
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_property.py -x -q > gpurun_out/parity.log 2>&1; tail -2 gpurun_out/parity.log
-CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "coop2:" "coop1:FMM_LIB=$L/libfmm_coop1.so"
+CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "g8:" "g1:FMM_TREE_GRID=1" "g2:FMM_TREE_GRID=2" "g4:FMM_TREE_GRID=4"
 python - <<'PY'
 import json,glob
 for f in sorted(glob.glob('gpurun_out/ab_*.json')):
