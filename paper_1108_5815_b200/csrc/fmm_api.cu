@@ -1206,6 +1206,20 @@ static int m2l_scheme_of(const fmm_ctx *h) {
 
 // FMM_CHECK builds: publish the buffer capacities the device-side bounds checks test against
 // (every translation unit holds its own copy); the capacities only grow within an evaluation
+#ifdef FMM_CHECK
+#include <map>
+#include <mutex>
+// the device-side bounds are device-global: with several live handles (in-process groups run
+// their ranks on host threads) the published value is the maximum over the live handles
+static std::mutex g_chk_mu;
+static std::map<const void *, FmmChk> g_chk_live;
+static void forget_chk(const void *h) {
+  std::lock_guard<std::mutex> lk(g_chk_mu);
+  g_chk_live.erase(h);
+}
+#else
+static void forget_chk(const void *) {}
+#endif
 static void publish_chk(fmm_ctx *h, cudaStream_t st) {
 #ifdef FMM_CHECK
   FmmChk c;
@@ -1215,6 +1229,17 @@ static void publish_chk(fmm_ctx *h, cudaStream_t st) {
   c.yrows = (long long)(h->m2l_Y.cap / m2l_y_stride(h->p));
   c.lists = (long long)h->p2p_rng.cap;
   if (getenv("FMM_CHECK_SELFTEST")) c.pos = 1;  // tests: a bound every evaluation violates
+  {
+    std::lock_guard<std::mutex> lk(g_chk_mu);
+    g_chk_live[h] = c;
+    for (const auto &kv : g_chk_live) {
+      c.pos = std::max(c.pos, kv.second.pos);
+      c.cells = std::max(c.cells, kv.second.cells);
+      c.rows = std::max(c.rows, kv.second.rows);
+      c.yrows = std::max(c.yrows, kv.second.yrows);
+      c.lists = std::max(c.lists, kv.second.lists);
+    }
+  }
   fmm_chk_set_p2p(c, st);
   fmm_chk_set_m2l_tc(c, st);
   fmm_chk_set_m2l(c, st);
@@ -1837,6 +1862,7 @@ int fmm_create(fmm_t *out, int p, double theta, int ncrit) {
 
 int fmm_destroy(fmm_t h) {
   if (!h) return FMM_OK;
+  forget_chk(h);
   DeviceGuard dg(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->keys_in.release(); h->keys.release(); h->idx_in.release(); h->perm.release();
