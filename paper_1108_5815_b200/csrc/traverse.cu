@@ -21,12 +21,21 @@
 
 enum { CAT_M2L = 0, CAT_M2P = 1, CAT_P2P = 2, CAT_OUT = 3, CAT_PUSH = 4, CAT_NONE = 5 };
 
-__device__ __forceinline__ bool mac_accept(int4 gt, int4 gs, double theta) {
+// The MAC's decision is the FP64 expression rsum <= theta * sqrt(R2) (R4/R5, the
+// oracle's). Away from the boundary it equals the exact comparison rsum^2 <= theta^2 R2, which
+// needs no square root: rsum and R2 are integers below 2^45 (exact in FP64, rsum^2 too), and
+// theta2 * R2 is within 3e-16 relative of theta^2 R2 while the FP64 expression's rounding moves the
+// boundary by at most 3e-16 relative; a pair within 1e-14 of it takes the exact FP64 path.
+__device__ __forceinline__ bool mac_accept(int4 gt, int4 gs, double theta, double theta2) {
   const long long dx = gt.x - gs.x, dy = gt.y - gs.y, dz = gt.z - gs.z;
   const long long R2 = dx * dx + dy * dy + dz * dz;
   const long long rsum = (1LL << (FMM_LEVELS - gt.w)) + (1LL << (FMM_LEVELS - gs.w));
+  const double a = __ll2double_rn(rsum), a2 = __dmul_rn(a, a);
+  const double t = __dmul_rn(theta2, __ll2double_rn(R2));
+  if (a2 < __dmul_rn(t, 1.0 - 1e-14)) return true;
+  if (a2 > __dmul_rn(t, 1.0 + 1e-14)) return false;
   const double rhs = __dmul_rn(theta, __dsqrt_rn(__ll2double_rn(R2)));
-  return __ll2double_rn(rsum) <= rhs;
+  return a <= rhs;
 }
 
 __device__ __forceinline__ int select_kind(const TravArgs &A, int nt, int ns) {
@@ -84,6 +93,7 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
   const int wib = threadIdx.x >> 5;
 #endif
   const CellsView C = A.C;
+  const double theta2 = __dmul_rn(A.theta, A.theta);
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -116,7 +126,9 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
     }
     const bool tleaf = rt.b.w == 0;
     int n[4] = {0, 0, 0, 0};
-    unsigned long long pp_pairs = 0, mp_evals = 0;  // this target's lane partials
+    // this target's lane partials: source particles of its P2P pairs, number of M2P pairs
+    // (32-bit adds per candidate; multiplied by the target's count once, at the end)
+    unsigned pp_src = 0, mp_n = 0;
     int top = 0;
     bool overflow = false, ovf_out = false;
 
@@ -133,7 +145,7 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
           const CellRec rs = prec ? *prec : load_rec(A.pk, s);
           scnt = rs.b.y;
           sbeg = rs.b.x;
-          if (mac_accept(gt, rs.g, A.theta))
+          if (mac_accept(gt, rs.g, A.theta, theta2))
             cat = select_kind(A, tcnt, scnt);
           else if (tleaf && rs.b.w == 0)
             cat = CAT_P2P;
@@ -141,8 +153,8 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
             cat = CAT_PUSH;
         }
       }
-      if (cat == CAT_P2P) pp_pairs += (unsigned long long)tcnt * (unsigned long long)scnt;
-      if (cat == CAT_M2P) mp_evals += (unsigned long long)tcnt;
+      pp_src += cat == CAT_P2P ? (unsigned)scnt : 0u;
+      mp_n += cat == CAT_M2P ? 1u : 0u;
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         const unsigned b = __ballot_sync(0xffffffffu, cat == c);
@@ -295,8 +307,8 @@ __global__ void __launch_bounds__(128, TRAV_MINB) k_traverse(TravArgs A) {
       }
     }
     __syncwarp();
-    warp_pp += pp_pairs;  // one atomic per warp at the end, not two per target
-    warp_mp += mp_evals;
+    warp_pp += (unsigned long long)tcnt * pp_src;  // one atomic per warp at the end
+    warp_mp += (unsigned long long)tcnt * mp_n;
   }
   for (int o = 16; o > 0; o >>= 1) {
     warp_pp += __shfl_xor_sync(0xffffffffu, warp_pp, o);
