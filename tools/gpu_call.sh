@@ -1,10 +1,8 @@
-L=$PWD/paper_1108_5815_b200
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_property.py tests/test_gpu_dist.py -x -q > gpurun_out/parity.log 2>&1; tail -2 gpurun_out/parity.log
-CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "new:" "old:FMM_LIB=$L/libfmm_travold.so"
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -2 gpurun_out/gputest.log
+CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "new:"
 python - <<'PY'
 import json,glob
 for f in sorted(glob.glob('gpurun_out/ab_*.json')):
-    try: d=json.loads([x for x in open(f) if x.startswith('{')][-1])
-    except Exception: print(f,'FAIL'); continue
-    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), 'trav', round(ph['ms_traverse'],3), 'up', round(ph['ms_upward'],3), d['counts']['p2p_pairs'])
+    d=json.loads([x for x in open(f) if x.startswith('{')][-1])
+    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), {k[3:]:round(v,3) for k,v in ph.items()})
 PY
