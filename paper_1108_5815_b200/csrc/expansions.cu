@@ -148,14 +148,14 @@ __host__ __device__ constexpr int p2m_group_coeffs(int P, int m0, int m1) {
 template <int P, int M0, int M1>
 __device__ __forceinline__ void p2m_group(int leaf, const float4 g, float rinv, int b, int cnt,
                                           const float4 *__restrict__ pos, float2 *__restrict__ M,
-                                          float *red, int lane) {
+                                          float *red, int lane, int sl, int W) {
   constexpr int G = p2m_group_coeffs(P, M0, M1), RS = 2 * G + 1, NCS = nc_stride(P);
   float acc[2 * G];
 #pragma unroll
   for (int o = 0; o < 2 * G; ++o) acc[o] = 0.f;
-  for (int c0 = 0; c0 < cnt; c0 += WARP) {
-    const bool valid = c0 + lane < cnt;
-    const float4 y = valid ? pos[b + c0 + lane] : make_float4(g.x, g.y, g.z, 0.f);
+  for (int c0 = 0; c0 < cnt; c0 += W) {
+    const bool valid = c0 + sl < cnt;
+    const float4 y = valid ? pos[b + c0 + sl] : make_float4(g.x, g.y, g.z, 0.f);
     const float x = (y.x - g.x) * rinv, yy = (y.y - g.y) * rinv, z = (y.z - g.z) * rinv;
     const float q = y.w;
     const float r2 = x * x + yy * yy + z * z;
@@ -191,9 +191,10 @@ __device__ __forceinline__ void p2m_group(int leaf, const float4 g, float rinv, 
 #pragma unroll
   for (int o = 0; o < 2 * G; ++o) red[lane * RS + o] = acc[o];
   __syncwarp();
-  for (int o = lane; o < 2 * G; o += WARP) {
+  const int base = lane - sl;  // first row of this leaf's lanes
+  for (int o = sl; o < 2 * G; o += W) {
     float sum = 0.f;
-    for (int l = 0; l < 32; ++l) sum += red[l * RS + o];
+    for (int l = 0; l < W; ++l) sum += red[(base + l) * RS + o];
     // group-local float o -> (m, n): columns m0.., each n = m..P, re/im
     int c = o >> 1, m = M0;
     while (c > P - m) {
@@ -209,9 +210,9 @@ template <int P, int M0>
 struct P2MGroups {
   static constexpr int M1 = p2m_group_end(P, M0);
   __device__ static void run(int leaf, const float4 g, float rinv, int b, int cnt,
-                             const float4 *pos, float2 *M, float *red, int lane) {
-    p2m_group<P, M0, M1>(leaf, g, rinv, b, cnt, pos, M, red, lane);
-    if constexpr (M1 <= P) P2MGroups<P, M1>::run(leaf, g, rinv, b, cnt, pos, M, red, lane);
+                             const float4 *pos, float2 *M, float *red, int lane, int sl, int W) {
+    p2m_group<P, M0, M1>(leaf, g, rinv, b, cnt, pos, M, red, lane, sl, W);
+    if constexpr (M1 <= P) P2MGroups<P, M1>::run(leaf, g, rinv, b, cnt, pos, M, red, lane, sl, W);
   }
 };
 __host__ __device__ constexpr int p2m_max_group(int P) {
@@ -234,14 +235,24 @@ __global__ void __launch_bounds__(128, P2MG_MINB) k_p2m_g(const int *__restrict_
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   float *red = sh_p2mg + wib * 32 * RS;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int li = gw; li < nleaves; li += nw) {
-    const int leaf = leaves[li];
+  // one leaf on W lanes: a whole warp, or a half-warp each of two leaves of <= 16 particles
+  auto leaf_body = [&](int leaf, int sl, int W) {
     const float4 g = C.geo[leaf];
     const float rinv = 1.f / g.w;
     const int b = C.beg[leaf], cnt = C.cnt[leaf];
     FMM_DCHECK(FMM_IN(leaf, g_fmm_chk.rows) && b >= 0 && (long long)b + cnt <= g_fmm_chk.pos,
                "P2M leaf / particle range");
-    P2MGroups<p, 0>::run(leaf, g, rinv, b, cnt, pos, M, red, lane);
+    P2MGroups<p, 0>::run(leaf, g, rinv, b, cnt, pos, M, red, lane, sl, W);
+  };
+  const int npairs = (nleaves + 1) / 2;
+  for (int pk = gw; pk < npairs; pk += nw) {
+    const int la = leaves[2 * pk], lb = 2 * pk + 1 < nleaves ? leaves[2 * pk + 1] : -1;
+    if (lb >= 0 && C.cnt[la] <= 16 && C.cnt[lb] <= 16) {
+      leaf_body((lane >> 4) ? lb : la, lane & 15, 16);
+    } else {
+      leaf_body(la, lane, 32);
+      if (lb >= 0) leaf_body(lb, lane, 32);
+    }
   }
 }
 
@@ -575,7 +586,7 @@ void launch_p2m(int p, const int *leaves, int nleaves, CellsView C, const float4
   FMM_DISPATCH_P(p, ({
     const size_t smem = 4 * 32 * (2 * p2m_max_group(P_) + 1) * sizeof(float);
     fmm_smem_optin((const void *)k_p2m_g<P_>, smem);
-    k_p2m_g<P_><<<warp_grid(nleaves, 4), 128, smem, st>>>(leaves, nleaves, C, pos, M);
+    k_p2m_g<P_><<<warp_grid((nleaves + 1) / 2, 4), 128, smem, st>>>(leaves, nleaves, C, pos, M);
   }));
 }
 void launch_m2m(int p, int c0, int nl, CellsView C, float2 *M, cudaStream_t st) {

@@ -1,8 +1,8 @@
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -2 gpurun_out/gputest.log
-CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "new:"
+L=$PWD/paper_1108_5815_b200
+CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "new:" "old:FMM_LIB=$L/libfmm_old.so" "new2:" "old2:FMM_LIB=$L/libfmm_old.so"
 python - <<'PY'
 import json,glob
 for f in sorted(glob.glob('gpurun_out/ab_*.json')):
     d=json.loads([x for x in open(f) if x.startswith('{')][-1])
-    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), {k[3:]:round(v,3) for k,v in ph.items()})
+    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), 'up', round(ph['ms_upward'],3), 'down', round(ph['ms_downward'],3), 'trav', round(ph['ms_traverse'],3))
 PY
