@@ -1090,31 +1090,41 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tck(const int4 *__restrict__ ite
       const int pos0 = item.x, cnt = item.y;
       const int ntile = (cnt + 127) / 128;
       unsigned prev_slot = 0;
+      // the row chunks are gathered two chunks ahead (a 2-deep register ring that crosses tile
+      // boundaries): a chunk's MMAs take ~0.6 us at p = 12, an L2 gather ~1 us
+      auto row_of = [&](int tile, bool &v) {
+        const int r = tile * 128 + tid;
+        v = r < cnt;
+        return M + (size_t)(v ? ssrc[pos0 + r] : 0u) * MROW;
+      };
+      auto load_to = [&](float4(&x)[8], const float *row, bool valid, int c) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int f = c * TCK_KC + 4 * q;
+          float4 v4 = (valid && f < MROW) ? __ldg(reinterpret_cast<const float4 *>(row + f))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (f + 3 >= NF) {  // the row's padding floats (never written) must not reach the MMA
+            if (f + 0 >= NF) v4.x = 0.f;
+            if (f + 1 >= NF) v4.y = 0.f;
+            if (f + 2 >= NF) v4.z = 0.f;
+            v4.w = 0.f;
+          }
+          x[q] = v4;
+        }
+      };
+      float4 xa[8], xb[8];
+      bool lvalid = false;
+      const float *lrow = row_of(0, lvalid);
+      load_to(xa, lrow, lvalid, 0);
+      load_to(xb, lrow, lvalid, 1);  // (NCH >= 5)
+      int lt = 0, lc = 2;            // the next chunk to gather: tile lt, chunk lc
       for (int i = 0; i < ntile; ++i, ++tt) {
         const int r = i * 128 + tid;
         const bool valid = r < cnt;
-        const float *row = M + (size_t)(valid ? ssrc[pos0 + r] : 0u) * MROW;
         const unsigned slot = valid ? sidx[pos0 + r] : 0u;
         FMM_DCHECK(!valid || (FMM_IN(ssrc[pos0 + r], g_fmm_chk.rows) &&
                               FMM_IN(slot, Lacc ? g_fmm_chk.rows : g_fmm_chk.yrows)),
                    "K-tiled M2L source row / result slot");
-        float4 x[8];
-        auto load_chunk = [&](int c) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int f = c * TCK_KC + 4 * q;
-            float4 v4 = (valid && f < MROW) ? __ldg(reinterpret_cast<const float4 *>(row + f))
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (f + 3 >= NF) {  // the row's padding floats (never written) must not reach the MMA
-              if (f + 0 >= NF) v4.x = 0.f;
-              if (f + 1 >= NF) v4.y = 0.f;
-              if (f + 2 >= NF) v4.z = 0.f;
-              v4.w = 0.f;
-            }
-            x[q] = v4;
-          }
-        };
-        load_chunk(0);
         for (int c = 0; c < NCH; ++c, ++g) {
           const int s = g & 1;
           if (g >= 2) {
@@ -1125,7 +1135,7 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tck(const int4 *__restrict__ ite
           float4 *ah = reinterpret_cast<float4 *>(a_base(s)), *al = reinterpret_cast<float4 *>(a_base(s) + ABYTES);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const float4 v4 = x[q];
+            const float4 v4 = xa[q];
             const float vs[4] = {v4.x, v4.y, v4.z, v4.w};
             float hv[4], lv[4];
 #pragma unroll
@@ -1138,10 +1148,17 @@ __global__ void __launch_bounds__(160, 1) k_m2l_tck(const int4 *__restrict__ ite
             ah[q * 128 + tid] = make_float4(hv[0], hv[1], hv[2], hv[3]);
             al[q * 128 + tid] = make_float4(lv[0], lv[1], lv[2], lv[3]);
           }
-          if (c + 1 < NCH) load_chunk(c + 1);  // in flight while the MMAs run
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           tc_fence_before();
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&a_full[s])) : "memory");
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xa[q] = xb[q];
+          if (lc == NCH) {
+            lc = 0;
+            if (++lt < ntile) lrow = row_of(lt, lvalid);
+          }
+          if (lt < ntile) load_to(xb, lrow, lvalid, lc);
+          ++lc;
         }
         // the previous tile's epilogue overlaps this tile's MMAs (double-buffered D)
         if (DB == 2 && i > 0) epilogue(tt - 1, cnt, (i - 1) * 128, prev_slot);

@@ -1,8 +1,7 @@
-L=$PWD/paper_1108_5815_b200
-CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "new:" "old:FMM_LIB=$L/libfmm_old.so" "new2:" "old2:FMM_LIB=$L/libfmm_old.so"
-python - <<'PY'
-import json,glob
-for f in sorted(glob.glob('gpurun_out/ab_*.json')):
-    d=json.loads([x for x in open(f) if x.startswith('{')][-1])
-    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), 'up', round(ph['ms_upward'],3), 'down', round(ph['ms_downward'],3), 'trav', round(ph['ms_traverse'],3))
-PY
+timeout 900 python -m pytest tests/test_gpu_rotation.py -x -q > gpurun_out/tck.log 2>&1; tail -2 gpurun_out/tck.log
+timeout 900 python tools/p_ladder.py 1000000 10 11 12 13 14 15 > gpurun_out/p_ladder2.jsonl 2> gpurun_out/p_ladder.err
+python -c "
+import json
+for l in open('gpurun_out/p_ladder2.jsonl'):
+    d=json.loads(l); print(d['p'], d['scheme'], round(d['ms'],3), round(d['ms_m2l'],3), '%.2e %.2e'%(d['err_phi'], d['err_grad']))
+"
