@@ -394,7 +394,14 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
   __shared__ __align__(16) float4 red[P2Q_RED][P2Q_CWARPS][P2Q_CHUNK];
   __shared__ int red_cnt[P2Q_RED];
 #endif
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
+#ifndef P2Q_PROD_ROT
+#define P2Q_PROD_ROT 0  // 1: the producer is warp blockIdx % 4 (measured: C4 P2P 27.9 -> 31.7 ms;
+                        // with warp 4 the 4 CTAs of an SM already put one producer on each SMSP)
+#endif
+  // role: the producer warp, and the consumers' pool rank 0..P2Q_CWARPS-1 (`warp` below)
+  const int wraw = threadIdx.x >> 5, prod = P2Q_PROD_ROT ? (int)(blockIdx.x & 3) : P2Q_CWARPS;
+  const int warp = wraw == prod ? P2Q_CWARPS : (wraw < prod ? wraw : wraw - 1);
   if (threadIdx.x == 0) {
     for (int b = 0; b < (int)(sizeof(red_cnt) / sizeof(int)); ++b) red_cnt[b] = red_gen[b] = 0;
     for (int s = 0; s < P2Q_STAGES; ++s) {
@@ -613,7 +620,7 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
   // deposits its partial sums, and thread i sums target i's slices in slice order
   // (deterministic).
   {
-    const int L = threadIdx.x;  // 0 .. 32 * P2Q_CWARPS - 1
+    const int L = 32 * warp + lane;  // 0 .. 32 * P2Q_CWARPS - 1
     unsigned k = 0, chunk = 0;
     f2x t[6];
     f2x acc[8];

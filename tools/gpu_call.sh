@@ -1,6 +1,10 @@
-# final round-2 evidence: bench line, launch lists, HBM tables, p-ladder, C2-C5 configs + C5 sweep
-bash tools/profile_r2final.sh > /dev/null 2>&1
-timeout 900 python tools/p_ladder.py 1000000 4 5 6 7 8 9 10 11 12 13 14 15 > gpurun_out/r2f_p_ladder.jsonl 2> gpurun_out/r2f_p_ladder.err
-timeout 1500 python tools/config_sweep.py configs --steps 10 > gpurun_out/r2f_configs.jsonl 2> gpurun_out/r2f_configs.err
-timeout 1500 python tools/config_sweep.py sweep --steps 5 > gpurun_out/r2f_sweep.jsonl 2> gpurun_out/r2f_sweep.err
-ls -la gpurun_out/r2f_*
+L=$PWD/paper_1108_5815_b200
+FMM_LIB=$L/libfmm_rot.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "full_size or hybrid" > gpurun_out/parity.log 2>&1; tail -2 gpurun_out/parity.log
+CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "base:" "rot:FMM_LIB=$L/libfmm_rot.so" "base2:" "rot2:FMM_LIB=$L/libfmm_rot.so"
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob('gpurun_out/ab_*.json')):
+    d=json.loads([x for x in open(f) if x.startswith('{')][-1])
+    ph=d['phases_ms']; r=d['roofline']; fr = r['frac'] if r['kernel']=='k_p2p_tma' else r['secondary']['frac']
+    print(f.split('/')[-1], round(d['ms_per_step'],3), 'kernel', round(ph['ms_p2p_kernel'],3), 'frac', round(fr,4))
+PY
