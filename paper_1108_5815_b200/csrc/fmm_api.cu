@@ -127,6 +127,7 @@ struct fmm_ctx {
   // M2L translation scheme (NEXT-1): requested (FMM_M2L_AUTO = let fmm_tune decide), the one
   // the kernel pre-calculation picked, and the M2L times it measured per scheme (ms)
   int m2l_scheme = 0, m2l_tuned = 0;
+  bool m2l_compact_key = false;  // 21-bit M2L class keys (set when the last evaluation's fitted)
   double m2l_scheme_ms[5] = {0, 0, 0, 0, 0};
   DBuf<float> m2l_R;  // rotation-based scheme: per-class operators (m2l_rot.cu)
   // expansion basis (NEXT-2): 0 spherical harmonics, 1 Cartesian Taylor (p <= CART_PMAX)
@@ -1472,12 +1473,14 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
       CK(h->m2l_stgt.ensure(np));
       W.stgt = h->m2l_stgt.p;
     }
+    W.compact_key = h->m2l_compact_key ? 1 : 0;
     CK(m2l_prepare(W, np, h->ncells, st));
     h->stats.launches += 6;
     h->stats.cub_calls += 2;
-    CK(cudaMemcpyAsync(h->h_small, h->m2l_counters.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->h_small, h->m2l_counters.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int ngclass = h->h_small[3];
+    h->m2l_compact_key = h->h_small[6] == 0;  // the next evaluation's class-key width
     CK(m2l_sort_items(W, h->h_small[1], st));
     h->stats.launches += 1;
     h->stats.cub_calls += 1;

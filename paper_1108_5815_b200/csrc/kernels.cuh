@@ -122,6 +122,7 @@ struct M2LWork {
   int direct_all;           // 1: every pair on the direct path (p > 12)
   // block-major execution order (m2l_sort_items): runs of a class split at target blocks
   int blk_level;            // Morton level of the spatial blocks (0: one block)
+  int compact_key;          // 21-bit class keys (counters[6] reports pairs they cannot hold)
   int *rflag, *rid, *rstart, *gid_of;
   int4 *items_raw;          // items as emitted (unordered); `items` = block-major order
   unsigned *ikeys_in, *ikeys, *iidx_in, *iidx;

@@ -118,11 +118,19 @@ __global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
 // M2L_KEY_OWN and form classes of their own (evaluated by the direct per-pair path).
 #define M2L_KEY_BITS 24
 #define M2L_KEY_OWN 0xFFFFFFu
+// compact class key (21 bits, so that with the 3 bits of spatial block the radix sort still takes 3
+// passes): 6-bit offsets, |offset| <= 30; used when the previous evaluation had no pair outside
+// that range (uniform trees), else the 24-bit key (k_m2l_keys reports any pair the compact key
+// cannot hold; in compact mode such a pair takes the reserved key: its own class, direct path)
+#define M2L_KEYC_BITS 21
+#define M2L_KEYC_OWN 0x1FFFFFu
+#define M2L_KEYC_LIM 30
 __device__ __forceinline__ unsigned cell_block(int4 g, int bl);
 __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
                           const unsigned *__restrict__ src, CellsView C, int bl,
                           unsigned *__restrict__ keys, unsigned *__restrict__ idx,
-                          uint2 *__restrict__ pst) {
+                          uint2 *__restrict__ pst, int compact, int *wide) {
+  bool any_wide = false;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
     const unsigned s = src[e];
     const int t = pair_t[e];
@@ -131,15 +139,28 @@ __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
     const int dl = gt.w - gs.w;
     const int sh = FMM_LEVELS - max(gt.w, gs.w);
     const int dx = (gt.x - gs.x) >> sh, dy = (gt.y - gs.y) >> sh, dz = (gt.z - gs.z) >> sh;
-    unsigned key = M2L_KEY_OWN;
-    if (abs(dx) < 63 && abs(dy) < 63 && abs(dz) < 63 && dl >= -4 && dl <= 3)  // never all ones
-      key = ((unsigned)(dl + 4) << 21) | ((unsigned)(dx + 64) << 14) | ((unsigned)(dy + 64) << 7) |
-            (unsigned)(dz + 64);
+    const bool fits_c = abs(dx) <= M2L_KEYC_LIM && abs(dy) <= M2L_KEYC_LIM &&
+                        abs(dz) <= M2L_KEYC_LIM && dl >= -4 && dl <= 3;
+    any_wide |= !fits_c;
+    unsigned key;
+    if (compact) {
+      key = M2L_KEYC_OWN;
+      if (fits_c)  // fields in [2, 62]: never all ones
+        key = ((unsigned)(dl + 4) << 18) | ((unsigned)(dx + 32) << 12) | ((unsigned)(dy + 32) << 6) |
+              (unsigned)(dz + 32);
+    } else {
+      key = M2L_KEY_OWN;
+      if (abs(dx) < 63 && abs(dy) < 63 && abs(dz) < 63 && dl >= -4 && dl <= 3)  // never all ones
+        key = ((unsigned)(dl + 4) << 21) | ((unsigned)(dx + 64) << 14) | ((unsigned)(dy + 64) << 7) |
+              (unsigned)(dz + 64);
+    }
     // below the class: the spatial block of the target, so that each class is ordered by block
     // and a run (class, block) is contiguous whatever the target levels
     keys[e] = (key << (3 * bl)) | cell_block(gt, bl);
     idx[e] = (unsigned)e;
   }
+  if (__any_sync(__activemask(), any_wide) && (threadIdx.x & 31) == (__ffs(__activemask()) - 1))
+    atomicOr(wide, 1);
 }
 
 // Spatial block (Morton index at level bl) of a cell, from its doubled-grid centre. Work items are
@@ -162,10 +183,10 @@ __global__ void k_m2l_class_flags(int npairs, const unsigned *__restrict__ skeys
                                   const unsigned *__restrict__ sidx,
                                   const uint2 *__restrict__ pst, int *__restrict__ flag,
                                   unsigned *__restrict__ ssrc, unsigned *__restrict__ stgt, int bl,
-                                  int *__restrict__ rflag) {
+                                  int *__restrict__ rflag, unsigned own) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
     const unsigned k = skeys[i], cls = k >> (3 * bl);
-    const int f = (i == 0 || cls != (skeys[i - 1] >> (3 * bl)) || cls == M2L_KEY_OWN) ? 1 : 0;
+    const int f = (i == 0 || cls != (skeys[i - 1] >> (3 * bl)) || cls == own) ? 1 : 0;
     flag[i] = f;
     // source and target cell in class-sorted order (one random 8-byte load per pair; later
     // kernels read these arrays coalesced)
@@ -627,9 +648,10 @@ int m2l_y_stride(int p) { return (2 * nc_of(p) + 3) & ~3; }
 cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st) {
   k_m2l_pair_targets<<<148 * 8, 128, 0, st>>>(ncells, W.off, W.cnt, W.pair_t);
   const int b = (npairs + 255) / 256 < 148 * 16 ? (npairs + 255) / 256 : 148 * 16;
+  cudaMemsetAsync(W.counters + 6, 0, sizeof(int), st);
   k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.blk_level, W.keys_in,
-                                            W.idx_in, W.pst);
-  const int kbits = M2L_KEY_BITS + 3 * W.blk_level;
+                                            W.idx_in, W.pst, W.compact_key, W.counters + 6);
+  const int kbits = (W.compact_key ? M2L_KEYC_BITS : M2L_KEY_BITS) + 3 * W.blk_level;
   size_t bytes = 0;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, W.idx_in,
                                                   W.sidx, npairs, 0, kbits, st);
@@ -639,7 +661,8 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
                                       kbits, st);
   if (e) return e;
   k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.pst, W.flag, W.ssrc,
-                                                    W.stgt, W.blk_level, W.rflag);
+                                                    W.stgt, W.blk_level, W.rflag,
+                                                    W.compact_key ? M2L_KEYC_OWN : M2L_KEY_OWN);
   bytes = 0;
   e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, W.flag, W.cid, npairs, st);
   if (e) return e;

@@ -1,5 +1,9 @@
-#!/bin/bash
-# Scratch entry point for one gpurun call (edited per experiment; tools/profile_r2final.sh is the
-# reproducible evidence run): the GPU test suite and one bench line.
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -2 gpurun_out/gputest.log
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -c 300 gpurun_out/bench.json
+L=$PWD/paper_1108_5815_b200
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_rotation.py tests/test_gpu_dist.py -x -q > gpurun_out/parity.log 2>&1; tail -2 gpurun_out/parity.log
+CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "new:" "old:FMM_LIB=$L/libfmm_old.so" "new2:" "old2:FMM_LIB=$L/libfmm_old.so"
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob('gpurun_out/ab_*.json')):
+    d=json.loads([x for x in open(f) if x.startswith('{')][-1])
+    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), 'm2l', round(ph['ms_m2l'],3), 'trav', round(ph['ms_traverse'],3))
+PY
