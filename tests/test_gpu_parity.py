@@ -410,3 +410,34 @@ def test_traversal_overflow_retry(O, monkeypatch):
     ref = O.fmm(xyz, q, 4, 0.2, 32, O.HYBRID, cost=COST)
     assert np.array_equal(lists, O.canonical_tasks(ref.tasks))
     assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
+
+
+def test_sort_fixup_paths(O):
+    """The tree sort radix-sorts only the key bits of levels 0..D+2 (D = the previous tree's depth)
+    and fixes the runs of equal high bits: one thread (<= 64), one CTA (<= 4096), or a full 63-bit
+    redo (longer). A handle first sees a uniform set (shallow tree), then a set with a 3,000- and a
+    6,000-particle cluster inside one cell of the cut level: both fix-up paths, keys and perm
+    bit-exact against the oracle's stable 63-bit sort, the tree too."""
+    f = FMM(p=4, theta=0.5, ncrit=64, tune=False)
+    try:
+        f.set_cost_model(*COST)
+        xyz, q = make_particles(20000, "uniform", 31)
+        run(f, xyz, q)
+        rng = np.random.default_rng(32)
+        back = rng.random((11000, 3)).astype(np.float32)
+        c1 = (0.3 + 1e-4 * rng.random((3000, 3))).astype(np.float32)
+        c2 = (0.7 + 1e-4 * rng.random((6000, 3))).astype(np.float32)
+        xyz = np.ascontiguousarray(np.concatenate([back, c1, c2]))
+        q = rng.uniform(-1, 1, len(xyz)).astype(np.float32)
+        phi, grad = run(f, xyz, q)
+        n = len(q)
+        ref = O.fmm(xyz, q, 4, 0.5, 64, O.HYBRID, cost=COST)
+        perm, keys, origin, L = f.export_perm(n)
+        assert np.array_equal(keys, ref.sorted_keys)
+        assert np.array_equal(perm, ref.perm)
+        t = f.export_tree()
+        for k in ("level", "prefix", "begin", "count"):
+            assert np.array_equal(t[k], ref.tree[k]), k
+        assert O.rel_l2(phi, ref.phi) < 1e-5 and O.rel_l2(grad, ref.grad) < 1e-5
+    finally:
+        f.close()
