@@ -1,1 +1,8 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "sort_fixup or degenerate" > gpurun_out/fix.log 2>&1; tail -15 gpurun_out/fix.log
+L=$PWD/paper_1108_5815_b200
+CFGS="C2 C3 C4" STEPS=10 bash tools/ab_bench.sh "m32:" "m16:FMM_LIB=$L/libfmm_m16.so" "m12:FMM_LIB=$L/libfmm_m12.so"
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob('gpurun_out/ab_*.json')):
+    d=json.loads([x for x in open(f) if x.startswith('{')][-1])
+    ph=d['phases_ms']; print(f.split('/')[-1], round(d['ms_per_step'],3), 'p2p', round(ph['ms_p2p'],3), 'kernel', round(ph['ms_p2p_kernel'],3))
+PY
