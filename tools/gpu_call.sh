@@ -1,8 +1,9 @@
-#!/bin/bash
-# Scratch entry point for one gpurun call (edited per experiment; tools/profile_r2final.sh is the
-# reproducible evidence run): the GPU test suite, then the evidence run.
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -2 gpurun_out/gputest.log
-bash tools/profile_r2final.sh > /dev/null 2>&1
-timeout 900 python tools/p_ladder.py 1000000 4 5 6 7 8 9 10 11 12 13 14 15 > gpurun_out/r2f_p_ladder.jsonl 2> gpurun_out/r2f_p_ladder.err
-timeout 1500 python tools/config_sweep.py configs --steps 10 > gpurun_out/r2f_configs.jsonl 2> gpurun_out/r2f_configs.err
-tail -c 400 gpurun_out/r2f_bench.json
+L=$PWD/paper_1108_5815_b200
+for v in base new pm4; do
+  lib=$L/libfmm.so; [ $v != new ] && lib=$L/libfmm_$v.so
+  for c in C2 C3 C4; do
+    FMM_LIB=$lib ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "profiled/" -k regex:"k_l2p" --csv python tools/profile_run.py $c hybrid > gpurun_out/l2p_${v}_$c.csv 2>&1
+    echo $v $c $(grep -h "k_l2p" gpurun_out/l2p_${v}_$c.csv | awk -F'","' '{print $NF}')
+  done
+done
+FMM_LIB=$L/libfmm.so timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "full_size or hybrid" > gpurun_out/parity.log 2>&1; tail -1 gpurun_out/parity.log
