@@ -384,6 +384,8 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
 #define P2Q_REDBUF 2  // two buffers, reuse guarded by a per-buffer generation count
 #elif P2Q_LASTRED
 #define P2Q_REDBUF P2Q_STAGES  // see P2Q_RED
+#elif defined(P2Q_ONEBUF) && P2Q_ONEBUF
+#define P2Q_REDBUF 1  // one buffer, a second consumer barrier after the reduction (8 KB for tiles)
 #else
 #define P2Q_REDBUF 2  // the 4 consumer warps meet at a named barrier, then reduce together
 #endif
@@ -725,6 +727,7 @@ __global__ void __launch_bounds__(P2Q_THREADS, P2Q_MINB)
 #else
         asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");
         reduce(L, 32 * P2Q_CWARPS);
+        if (P2Q_REDBUF == 1) asm volatile("bar.sync 2, %0;" ::"n"(32 * P2Q_CWARPS) : "memory");
 #endif
       }
       __syncwarp();
