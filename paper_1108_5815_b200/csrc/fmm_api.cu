@@ -159,7 +159,7 @@ struct fmm_ctx {
   // expansions
   DBuf<float2> M, L;
   // M2L class batching
-  DBuf<uint2> m2l_pst;
+  DBuf<uint2> m2l_pst, m2l_spst;
   DBuf<int> m2l_pair_t, m2l_flag, m2l_cid, m2l_cstart, m2l_counters;
   DBuf<unsigned> m2l_keys_in, m2l_keys;
   DBuf<unsigned> m2l_idx_in, m2l_sidx, m2l_small, m2l_class_rep, m2l_ssrc, m2l_stgt;
@@ -1472,9 +1472,19 @@ static int evaluate_tree(fmm_ctx *h, const float *xyz, const float *q, int64_t n
     if (accum) {
       CK(h->m2l_stgt.ensure(np));
       W.stgt = h->m2l_stgt.p;
+      static const bool idx_sort = getenv("FMM_M2L_IDXSORT") != nullptr;  // (A/B: round-2 path)
+      if (!idx_sort) {
+        CK(h->m2l_spst.ensure(np));
+        W.spst = h->m2l_spst.p;
+      }
     }
     W.compact_key = h->m2l_compact_key ? 1 : 0;
     CK(m2l_prepare(W, np, h->ncells, st));
+    if (W.spst) {
+      // the class representatives and the direct-path list hold class-sorted positions
+      W.pair_t = reinterpret_cast<int *>(W.stgt);
+      W.src = W.ssrc;
+    }
     h->stats.launches += 6;
     h->stats.cub_calls += 2;
     CK(cudaMemcpyAsync(h->h_small, h->m2l_counters.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1892,7 +1902,7 @@ int fmm_destroy(fmm_t h) {
   h->nch.release(); h->bnd.release(); h->excl.release(); h->leafflag.release(); h->leaves.release(); h->crange.release();
   h->M.release(); h->L.release();
   h->ntgt.release(); h->ts_stage.release();
-  h->m2l_pair_t.release(); h->m2l_pst.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
+  h->m2l_pair_t.release(); h->m2l_pst.release(); h->m2l_spst.release(); h->m2l_flag.release(); h->m2l_cid.release(); h->m2l_cstart.release();
   h->m2l_counters.release(); h->m2l_keys_in.release(); h->m2l_keys.release();
   h->m2l_idx_in.release(); h->m2l_sidx.release(); h->m2l_small.release(); h->m2l_items.release();
   h->m2l_items_raw.release(); h->m2l_rflag.release(); h->m2l_rid.release(); h->m2l_rstart.release();

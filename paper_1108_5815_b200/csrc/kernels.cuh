@@ -107,6 +107,8 @@ struct M2LWork {
   const unsigned *src;      // source cell of each pair
   int *pair_t;              // target cell of each pair
   uint2 *pst;               // (source, target) of each pair, list order
+  uint2 *spst;              // accumulate mode: the same records in class-sorted order (else null;
+                            // class_rep and the direct-path list then hold sorted positions)
   unsigned *keys_in, *keys;  // 24-bit class keys
   unsigned *idx_in, *sidx;  // pair indices sorted by class key
   unsigned *ssrc;           // source cell of each class-sorted pair

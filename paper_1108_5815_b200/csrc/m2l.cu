@@ -197,6 +197,23 @@ __global__ void k_m2l_class_flags(int npairs, const unsigned *__restrict__ skeys
   }
 }
 
+// accumulate mode: the class sort carried the (source, target) records, so the flags pass reads
+// them coalesced (the pair-index gather of k_m2l_class_flags was a random 8-byte load per pair)
+__global__ void k_m2l_class_flags_sorted(int npairs, const unsigned *__restrict__ skeys,
+                                         const uint2 *__restrict__ spst, int *__restrict__ flag,
+                                         unsigned *__restrict__ ssrc, unsigned *__restrict__ stgt,
+                                         int bl, int *__restrict__ rflag, unsigned own) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
+    const unsigned k = skeys[i], cls = k >> (3 * bl);
+    const int f = (i == 0 || cls != (skeys[i - 1] >> (3 * bl)) || cls == own) ? 1 : 0;
+    flag[i] = f;
+    const uint2 st = spst[i];
+    ssrc[i] = st.x;
+    stgt[i] = st.y;
+    rflag[i] = f || k != skeys[i - 1];
+  }
+}
+
 __global__ void k_m2l_run_start(int npairs, const int *__restrict__ rflag,
                                 const int *__restrict__ rid, int *__restrict__ rstart) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += gridDim.x * blockDim.x) {
@@ -232,12 +249,12 @@ __global__ void k_m2l_class_gid(int npairs, int direct_all, const int *__restric
     const int n = cstart[c + 1] - i;
     if (!direct_all && n >= M2L_SMALL) {
       const int gid = atomicAdd(&counters[3], 1);
-      class_rep[gid] = sidx[i];
+      class_rep[gid] = sidx ? sidx[i] : (unsigned)i;  // accumulate mode: the sorted position
       gid_of[c] = gid;
     } else {
       gid_of[c] = -1;
       const int base = atomicAdd(&counters[2], n);
-      for (int b = 0; b < n; ++b) small[base + b] = sidx[i + b];
+      for (int b = 0; b < n; ++b) small[base + b] = sidx ? sidx[i + b] : (unsigned)(i + b);
     }
   }
 }
@@ -260,7 +277,7 @@ __global__ void k_m2l_run_items(int npairs, const int *__restrict__ flag, const 
     const int base = atomicAdd(&counters[1], ni);
     const unsigned key = ((skeys[i] & ((1u << (3 * bl)) - 1u)) << 20) | (unsigned)gid;
     for (int a = 0; a < ni; ++a) {
-      items[base + a] = make_int4(i + a * M2L_ITEM, min(M2L_ITEM, n - a * M2L_ITEM), (int)sidx[i], gid);
+      items[base + a] = make_int4(i + a * M2L_ITEM, min(M2L_ITEM, n - a * M2L_ITEM), i, gid);
       ikeys[base + a] = key;
       iidx[base + a] = (unsigned)(base + a);
     }
@@ -653,16 +670,34 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
                                             W.idx_in, W.pst, W.compact_key, W.counters + 6);
   const int kbits = (W.compact_key ? M2L_KEYC_BITS : M2L_KEY_BITS) + 3 * W.blk_level;
   size_t bytes = 0;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, W.idx_in,
-                                                  W.sidx, npairs, 0, kbits, st);
-  if (e) return e;
-  if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
-  e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
-                                      kbits, st);
-  if (e) return e;
-  k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.pst, W.flag, W.ssrc,
-                                                    W.stgt, W.blk_level, W.rflag,
-                                                    W.compact_key ? M2L_KEYC_OWN : M2L_KEY_OWN);
+  cudaError_t e;
+  const bool by_record = W.spst != nullptr;  // accumulate mode: sort the (source, target) records
+  if (by_record) {
+    unsigned long long *vin = reinterpret_cast<unsigned long long *>(W.pst);
+    unsigned long long *vout = reinterpret_cast<unsigned long long *>(W.spst);
+    e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, vin, vout, npairs, 0,
+                                        kbits, st);
+    if (e) return e;
+    if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
+    e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, vin, vout, npairs, 0, kbits,
+                                        st);
+    if (e) return e;
+    k_m2l_class_flags_sorted<<<b > 0 ? b : 1, 256, 0, st>>>(
+        npairs, W.keys, W.spst, W.flag, W.ssrc, W.stgt, W.blk_level, W.rflag,
+        W.compact_key ? M2L_KEYC_OWN : M2L_KEY_OWN);
+  } else {
+    e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs,
+                                        0, kbits, st);
+    if (e) return e;
+    if (bytes > W.tmp_bytes) return cudaErrorMemoryAllocation;
+    e = cub::DeviceRadixSort::SortPairs(W.tmp, bytes, W.keys_in, W.keys, W.idx_in, W.sidx, npairs, 0,
+                                        kbits, st);
+    if (e) return e;
+    k_m2l_class_flags<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.keys, W.sidx, W.pst, W.flag, W.ssrc,
+                                                      W.stgt, W.blk_level, W.rflag,
+                                                      W.compact_key ? M2L_KEYC_OWN : M2L_KEY_OWN);
+  }
+  const unsigned *sidx = by_record ? nullptr : W.sidx;  // (pair indices exist only without records)
   bytes = 0;
   e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, W.flag, W.cid, npairs, st);
   if (e) return e;
@@ -675,9 +710,9 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   k_m2l_class_start<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.flag, W.cid, W.cstart, W.counters);
   k_m2l_run_start<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.rflag, W.rid, W.rstart);
   k_m2l_class_gid<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.direct_all, W.flag, W.cid, W.cstart,
-                                                 W.sidx, W.gid_of, W.small, W.class_rep, W.counters);
+                                                 sidx, W.gid_of, W.small, W.class_rep, W.counters);
   k_m2l_run_items<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.flag, W.rflag, W.rid, W.rstart, W.cid, W.gid_of,
-                                                 W.sidx, W.keys, W.blk_level, W.items_raw,
+                                                 sidx, W.keys, W.blk_level, W.items_raw,
                                                  W.ikeys_in, W.iidx_in, W.counters);
   return cudaGetLastError();
 }
@@ -706,7 +741,11 @@ size_t m2l_temp_bytes(int npairs) {
   size_t c = 0;  // the work-item sort (at most npairs items, 32-bit keys)
   cub::DeviceRadixSort::SortPairs(nullptr, c, (unsigned *)nullptr, (unsigned *)nullptr,
                                   (unsigned *)nullptr, (unsigned *)nullptr, npairs, 0, 32);
-  return std::max(a, std::max(b, c));
+  size_t d = 0;  // the accumulate mode's class sort carries the 8-byte (source, target) records
+  cub::DeviceRadixSort::SortPairs(nullptr, d, (unsigned *)nullptr, (unsigned *)nullptr,
+                                  (unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                  npairs, 0, 32);
+  return std::max(std::max(a, d), std::max(b, c));
 }
 
 cudaError_t m2l_build_T(int p, const M2LWork &W, int ngclass, cudaStream_t st) {
