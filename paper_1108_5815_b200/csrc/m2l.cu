@@ -157,7 +157,7 @@ __global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
     // below the class: the spatial block of the target, so that each class is ordered by block
     // and a run (class, block) is contiguous whatever the target levels
     keys[e] = (key << (3 * bl)) | cell_block(gt, bl);
-    idx[e] = (unsigned)e;
+    if (idx) idx[e] = (unsigned)e;  // (null: the sort carries the records instead)
   }
   if (__any_sync(__activemask(), any_wide) && (threadIdx.x & 31) == (__ffs(__activemask()) - 1))
     atomicOr(wide, 1);
@@ -667,7 +667,8 @@ cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t s
   const int b = (npairs + 255) / 256 < 148 * 16 ? (npairs + 255) / 256 : 148 * 16;
   cudaMemsetAsync(W.counters + 6, 0, sizeof(int), st);
   k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.blk_level, W.keys_in,
-                                            W.idx_in, W.pst, W.compact_key, W.counters + 6);
+                                            W.spst ? nullptr : W.idx_in, W.pst, W.compact_key,
+                                            W.counters + 6);
   const int kbits = (W.compact_key ? M2L_KEYC_BITS : M2L_KEY_BITS) + 3 * W.blk_level;
   size_t bytes = 0;
   cudaError_t e;
