@@ -100,16 +100,6 @@ __device__ __forceinline__ PairGeo pair_geo(int4 gt, int4 gs) {
 }
 
 // ---- pair bookkeeping -------------------------------------------------------------------------
-__global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
-                                   const int *__restrict__ cnt, int *__restrict__ pair_t) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = gw; t < ncells; t += nw) {
-    const int o = off[t], c = cnt[t];
-    for (int e = lane; e < c; e += 32) pair_t[o + e] = t;
-  }
-}
-
 // Class key = (level difference, integer offset in units of the smaller cell); the source cell
 // id fills the low bits so that, after the radix sort, each class lists its pairs in source
 // order (consecutive source cells -> contiguous multipole rows -> one bulk copy per chunk).
@@ -126,41 +116,57 @@ __global__ void k_m2l_pair_targets(int ncells, const int *__restrict__ off,
 #define M2L_KEYC_OWN 0x1FFFFFu
 #define M2L_KEYC_LIM 30
 __device__ __forceinline__ unsigned cell_block(int4 g, int bl);
-__global__ void k_m2l_keys(int npairs, const int *__restrict__ pair_t,
+__device__ __forceinline__ unsigned m2l_class_key(int4 gt, int4 gs, int bl, int compact,
+                                                  bool &any_wide) {
+  const int dl = gt.w - gs.w;
+  const int sh = FMM_LEVELS - max(gt.w, gs.w);
+  const int dx = (gt.x - gs.x) >> sh, dy = (gt.y - gs.y) >> sh, dz = (gt.z - gs.z) >> sh;
+  const bool fits_c = abs(dx) <= M2L_KEYC_LIM && abs(dy) <= M2L_KEYC_LIM &&
+                      abs(dz) <= M2L_KEYC_LIM && dl >= -4 && dl <= 3;
+  any_wide |= !fits_c;
+  unsigned key;
+  if (compact) {
+    key = M2L_KEYC_OWN;
+    if (fits_c)  // fields in [2, 62]: never all ones
+      key = ((unsigned)(dl + 4) << 18) | ((unsigned)(dx + 32) << 12) | ((unsigned)(dy + 32) << 6) |
+            (unsigned)(dz + 32);
+  } else {
+    key = M2L_KEY_OWN;
+    if (abs(dx) < 63 && abs(dy) < 63 && abs(dz) < 63 && dl >= -4 && dl <= 3)  // never all ones
+      key = ((unsigned)(dl + 4) << 21) | ((unsigned)(dx + 64) << 14) | ((unsigned)(dy + 64) << 7) |
+            (unsigned)(dz + 64);
+  }
+  // below the class: the spatial block of the target, so that each class is ordered by block
+  // and a run (class, block) is contiguous whatever the target levels
+  return (key << (3 * bl)) | cell_block(gt, bl);
+}
+
+// a warp per target cell over its list segment (the target's grid record read once): class keys,
+// the (source, target) records, and -- for the index sort -- pair indices and per-pair targets
+__global__ void k_m2l_keys(int ncells, const int *__restrict__ off, const int *__restrict__ cnt,
                           const unsigned *__restrict__ src, CellsView C, int bl,
                           unsigned *__restrict__ keys, unsigned *__restrict__ idx,
-                          uint2 *__restrict__ pst, int compact, int *wide) {
+                          int *__restrict__ pair_t, uint2 *__restrict__ pst, int compact,
+                          int *wide) {
   bool any_wide = false;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npairs; e += gridDim.x * blockDim.x) {
-    const unsigned s = src[e];
-    const int t = pair_t[e];
-    pst[e] = make_uint2(s, (unsigned)t);  // one 8-byte record for the class-sorted gather
-    const int4 gt = C.grid[t], gs = C.grid[s];
-    const int dl = gt.w - gs.w;
-    const int sh = FMM_LEVELS - max(gt.w, gs.w);
-    const int dx = (gt.x - gs.x) >> sh, dy = (gt.y - gs.y) >> sh, dz = (gt.z - gs.z) >> sh;
-    const bool fits_c = abs(dx) <= M2L_KEYC_LIM && abs(dy) <= M2L_KEYC_LIM &&
-                        abs(dz) <= M2L_KEYC_LIM && dl >= -4 && dl <= 3;
-    any_wide |= !fits_c;
-    unsigned key;
-    if (compact) {
-      key = M2L_KEYC_OWN;
-      if (fits_c)  // fields in [2, 62]: never all ones
-        key = ((unsigned)(dl + 4) << 18) | ((unsigned)(dx + 32) << 12) | ((unsigned)(dy + 32) << 6) |
-              (unsigned)(dz + 32);
-    } else {
-      key = M2L_KEY_OWN;
-      if (abs(dx) < 63 && abs(dy) < 63 && abs(dz) < 63 && dl >= -4 && dl <= 3)  // never all ones
-        key = ((unsigned)(dl + 4) << 21) | ((unsigned)(dx + 64) << 14) | ((unsigned)(dy + 64) << 7) |
-              (unsigned)(dz + 64);
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < ncells; t += nw) {
+    const int o = off[t], c = cnt[t];
+    if (c <= 0) continue;
+    const int4 gt = C.grid[t];
+    for (int k = lane; k < c; k += 32) {
+      const int e = o + k;
+      const unsigned s = src[e];
+      pst[e] = make_uint2(s, (unsigned)t);  // one 8-byte record for the class sort / gather
+      keys[e] = m2l_class_key(gt, C.grid[s], bl, compact, any_wide);
+      if (idx) {  // (null: the sort carries the records instead)
+        idx[e] = (unsigned)e;
+        pair_t[e] = t;
+      }
     }
-    // below the class: the spatial block of the target, so that each class is ordered by block
-    // and a run (class, block) is contiguous whatever the target levels
-    keys[e] = (key << (3 * bl)) | cell_block(gt, bl);
-    if (idx) idx[e] = (unsigned)e;  // (null: the sort carries the records instead)
   }
-  if (__any_sync(__activemask(), any_wide) && (threadIdx.x & 31) == (__ffs(__activemask()) - 1))
-    atomicOr(wide, 1);
+  if (__any_sync(0xffffffffu, any_wide) && lane == 0) atomicOr(wide, 1);
 }
 
 // Spatial block (Morton index at level bl) of a cell, from its doubled-grid centre. Work items are
@@ -663,12 +669,11 @@ bool m2l_gemm_supported(int p) {
 int m2l_y_stride(int p) { return (2 * nc_of(p) + 3) & ~3; }
 
 cudaError_t m2l_prepare(const M2LWork &W, int npairs, int ncells, cudaStream_t st) {
-  k_m2l_pair_targets<<<148 * 8, 128, 0, st>>>(ncells, W.off, W.cnt, W.pair_t);
   const int b = (npairs + 255) / 256 < 148 * 16 ? (npairs + 255) / 256 : 148 * 16;
   cudaMemsetAsync(W.counters + 6, 0, sizeof(int), st);
-  k_m2l_keys<<<b > 0 ? b : 1, 256, 0, st>>>(npairs, W.pair_t, W.src, W.C, W.blk_level, W.keys_in,
-                                            W.spst ? nullptr : W.idx_in, W.pst, W.compact_key,
-                                            W.counters + 6);
+  k_m2l_keys<<<148 * 8, 128, 0, st>>>(ncells, W.off, W.cnt, W.src, W.C, W.blk_level, W.keys_in,
+                                      W.spst ? nullptr : W.idx_in, W.pair_t, W.pst, W.compact_key,
+                                      W.counters + 6);
   const int kbits = (W.compact_key ? M2L_KEYC_BITS : M2L_KEY_BITS) + 3 * W.blk_level;
   size_t bytes = 0;
   cudaError_t e;
