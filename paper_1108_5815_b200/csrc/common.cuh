@@ -110,10 +110,17 @@ struct FmmChk {
 #ifdef FMM_CHECK
 #include <cstdio>
 static __device__ FmmChk g_fmm_chk;
+// the bounds only grow (atomicMax, stream-ordered): handles of an in-process group publish on
+// their own streams, and a plain copy from one could land after a later, larger one of another
 #define FMM_CHK_DEFINE_SETTER(name)                                                             \
-  void name(const FmmChk &c, cudaStream_t st) {                                                 \
-    cudaMemcpyToSymbolAsync(g_fmm_chk, &c, sizeof c, 0, cudaMemcpyHostToDevice, st);           \
-  }
+  static __global__ void k_chk_max_##name(FmmChk c) {                                           \
+    atomicMax(&g_fmm_chk.pos, c.pos);                                                           \
+    atomicMax(&g_fmm_chk.cells, c.cells);                                                       \
+    atomicMax(&g_fmm_chk.rows, c.rows);                                                         \
+    atomicMax(&g_fmm_chk.yrows, c.yrows);                                                       \
+    atomicMax(&g_fmm_chk.lists, c.lists);                                                       \
+  }                                                                                             \
+  void name(const FmmChk &c, cudaStream_t st) { k_chk_max_##name<<<1, 1, 0, st>>>(c); }
 #define FMM_DCHECK(cond, what)                                                                  \
   do {                                                                                          \
     if (!(cond)) {                                                                              \

@@ -1,7 +1,8 @@
 #!/bin/bash
 # Scratch entry point for one gpurun call (edited per experiment; tools/profile_r2final.sh is the
-# reproducible evidence run): M2L parity suites, then A/B of the fused key pass.
-L=paper_1108_5815_b200
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_rotation.py tests/test_gpu_dist.py -m gpu -x -q > gpurun_out/gputest.log 2>&1; tail -2 gpurun_out/gputest.log
-CFGS="C2 C4" tools/ab_bench.sh "new:" "old:FMM_LIB=$L/libfmm_old.so" "new2:" "old2:FMM_LIB=$L/libfmm_old.so"
-python tools/ab_show.py 'gpurun_out/ab_*.json'
+# reproducible evidence run): the checked build three times, the full GPU suite, smoke(), bench.
+out=gpurun_out
+for k in 1 2 3; do timeout 600 python -m pytest tests/test_gpu_check.py -m gpu -x -q > $out/chk_$k.log 2>&1; tail -n 1 $out/chk_$k.log; done
+timeout 1800 python -m pytest tests -m gpu -x -q > $out/gputest.log 2>&1; tail -n 2 $out/gputest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $out/smoke.log 2>&1; tail -n 1 $out/smoke.log
+timeout 900 python bench.py > $out/r2f_bench.json 2> $out/r2f_bench.err; tail -c 300 $out/r2f_bench.json
